@@ -1,0 +1,441 @@
+"""Benchmark of the B200 online hot path (BASELINE.json metric:
+"F/F* matvec ms & HBM GB/s (% roofline); online mean+forecast latency").
+
+Workload (N = 1): BASELINE config 3, Cascadia-shaped single GPU -- Nd=600,
+Nt=420, Nm=32768 (F-hat = 132.4 GB FP64 complex in HBM).  One step = one
+d = F m plus one m = F* d through the C ABI (the Hessian-matvec pattern),
+inputs resident in HBM.  N > 1 (torchrun, one rank per GPU): the parameter
+dimension is sharded -- every rank holds its own 32768-column shard of an
+Nm = 32768 N kernel (weak scaling); F m ends with an NCCL all-reduce of the
+Nd x Nt partial output, F* d starts from an NCCL broadcast of d.
+
+value  = algorithmic bytes of the step over all ranks / max-over-ranks
+         device time (CUDA events), GB/s;
+e2e    = same metric with pinned-host inputs copied in and results copied
+         out inside the timed region (the user-facing API call);
+online = BASELINE config 2 (Nd=64, Nm=16384, Nt=128, Nq=8, n=8192):
+         posterior mean + forecast latency through InferenceEngine;
+roofline = the GEMV kernels (the dominant stage) against the measured HBM
+         copy bandwidth in MEASURED_PEAKS.json;
+cpu_baseline = the reference's own apply_raw / apply_adjoint_raw
+         (oracle/_ref, verbatim sources) on all host cores, on a bounded
+         column sample of the same workload.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "F/F* matvec ms & HBM GB/s (% roofline); online mean+forecast latency"
+WORKLOADS = {
+    # name: (Nd, Nm per GPU, Nt, seed)
+    "cascadia": (600, 32768, 420, 20250810),
+    "small": (64, 16384, 128, 4321),
+    "toy": (8, 1024, 64, 2024),
+}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def algorithmic_bytes(nd, nm, nt):
+    # F-hat once + input and output series
+    return 16 * (nt + 1) * nd * nm + 8 * nt * (nm + nd)
+
+
+def gemv_bytes(nd, nm, nt):
+    # per GEMV launch: F-hat + x-hat (Nf x Nm) + y-hat (Nf x Nd), complex FP64
+    return 16 * (nt + 1) * (nd * nm + nm + nd)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own code (oracle/_ref) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_reference_run(nd, nt, seed, nm_sample, threads, reps):
+    import ctypes as C
+    from oracle import oracle as orc  # baseline leg only
+    if not orc.ref_available():
+        return None
+    R = orc.ref()
+    tb, ta, tj = C.c_double(), C.c_double(), C.c_double()
+    st = R.ref_bench(nd, nm_sample, nm_sample, nt, seed, threads, reps,
+                     C.byref(tb), C.byref(ta), C.byref(tj))
+    if st != 0:
+        raise RuntimeError("ref_bench: %s" % R.ref_last_error().decode())
+    byt = algorithmic_bytes(nd, nm_sample, nt)
+    return {"t_build": tb.value, "t_apply": ta.value, "t_adjoint": tj.value,
+            "gbs": 2 * byt / (ta.value + tj.value) / 1e9,
+            "sample": "Nd=%d Nt=%d, %d generated columns of the Cascadia kernel in %d shards "
+                      "(one reference MatvecPlan per thread), median of %d F+F* pairs"
+                      % (nd, nt, nm_sample, threads, reps)}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    nd, nm, nt, seed = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    nm_sample = min(nm, args.cpu_sample_cols)
+    t0 = time.time()
+    res = cpu_reference_run(nd, nt, seed, nm_sample, threads, max(1, args.steps))
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    ms = (res["t_apply"] + res["t_adjoint"]) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["gbs"], "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (counter-based generator)",
+        "config": {"workload": "%s (Nd=%d, Nt=%d); reference timed on a %d-column sample"
+                               % (args.workload, nd, nt, nm_sample)},
+        "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": threads,
+                         "kind": "reference", "sample": res["sample"]},
+        "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def bench_online(ltb, torch, reps=20):
+    """BASELINE config 2: posterior mean + forecast latency (device time)."""
+    nd, nm, nt, seed = WORKLOADS["small"]
+    nq = 8
+    g = ltb.MatvecPlan.generated(nd, nm, nt, seed=seed, tag=ltb.KernelTag.Gstar)
+    fq = ltb.MatvecPlan.generated(nq, nm, nt, seed=seed, tag=ltb.KernelTag.Fq)
+    eng = ltb.InferenceEngine(g, fq)
+    eng.set_factor_generated(seed)
+    d = torch.rand(nd * nt, dtype=torch.float64, device="cuda")
+    m = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
+    q = torch.empty(nq * nt, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        eng.infer_raw(d, m, q)
+    dev = sorted(eng.infer_raw(d, m, q) for _ in range(reps))
+    # stage breakdown: K^{-1} alone (wall, includes one sync), G* and F_q alone
+    y = d.clone()
+    solve = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.solve_k_inplace(y)
+        solve.append(time.perf_counter() - t0)
+    solve.sort()
+    sg, sq = ltb.MatvecPlan.Scratch(g), ltb.MatvecPlan.Scratch(fq)
+    sg.timing(True)
+    sq.timing(True)
+    for _ in range(reps):
+        g.apply_adjoint_raw(d, m, sg)
+        fq.apply_raw(m, q, sq)
+    gst, fqt = sg.stage_ms(), sq.stage_ms()
+    dh = d.cpu().numpy()
+    mh = torch.empty(nm * nt, dtype=torch.float64).pin_memory().numpy()
+    qh = torch.empty(nq * nt, dtype=torch.float64).pin_memory().numpy()
+    e2e = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        eng.infer_raw(dh, mh, qh)
+        e2e.append(time.perf_counter() - t0)
+    e2e.sort()
+    n = nd * nt
+    byts = 2 * 8 * (n * (n + 1) // 2) + algorithmic_bytes(nd, nm, nt) + algorithmic_bytes(nq, nm, nt)
+    med = dev[len(dev) // 2]
+    out = {"config": "small inversion (Nd=64, Nm=16384, Nt=128, Nq=8, n=8192, synthetic factor)",
+           "latency_ms": med * 1e3, "latency_min_ms": dev[0] * 1e3,
+           "e2e_ms": e2e[len(e2e) // 2] * 1e3,
+           "bytes": byts, "achieved_gbs": byts / med / 1e9,
+           "solve_k_ms": solve[len(solve) // 2] * 1e3,
+           "gstar_ms": sum(gst["Fstar"]) / reps, "fq_ms": sum(fqt["F"]) / reps,
+           "paper_online_s": 0.2}
+    eng.close()
+    return out
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_16344_b200 as ltb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    # one dedicated stream for our kernels, the copies and the collectives
+    torch.cuda.set_stream(torch.cuda.Stream())
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nd, nm, nt, seed = WORKLOADS[args.workload]
+    t_build = time.time()
+    plan = ltb.MatvecPlan.generated(nd, nm, nt, seed=seed, tag=ltb.KernelTag.F, stream=1,
+                                    nm_total=nm * world, c0=rank * nm)
+    torch.cuda.synchronize()
+    t_build = time.time() - t_build
+    stream = torch.cuda.current_stream()
+    s = ltb.MatvecPlan.Scratch(plan, stream=stream)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1000 + rank)
+    m = torch.rand(nm * nt, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    gen.manual_seed(7)
+    d = torch.rand(nd * nt, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    d_out = torch.empty(nd * nt, dtype=torch.float64, device="cuda")
+    m_out = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
+
+    def step():
+        plan.apply_raw(m, d_out, s)
+        if world > 1:
+            dist.all_reduce(d_out)
+            dist.broadcast(d, 0)
+        plan.apply_adjoint_raw(d, m_out, s)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    clocks = ClockSampler(local).start()
+    time.sleep(0.3)  # let the sampler attach before the timed region
+    s.timing(True)
+    launches0 = ltb.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    launches = ltb.kernel_launches() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = s.stage_ms()
+    s.timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    step_bytes = 2 * algorithmic_bytes(nd, nm, nt)
+    value = world * step_bytes / (ms * 1e-3) / 1e9
+
+    # ---- e2e: pinned host inputs in, results out, inside the timed region
+    m_h = m.cpu().pin_memory()
+    d_h = d.cpu().pin_memory()
+    dout_h = torch.empty(nd * nt, dtype=torch.float64).pin_memory()
+    mout_h = torch.empty(nm * nt, dtype=torch.float64).pin_memory()
+    m_dev = torch.empty_like(m)
+    d_dev = torch.empty_like(d)
+
+    def step_e2e():
+        m_dev.copy_(m_h, non_blocking=True)
+        plan.apply_raw(m_dev, d_out, s)
+        if world > 1:
+            dist.all_reduce(d_out)
+        dout_h.copy_(d_out, non_blocking=True)
+        if rank == 0:
+            d_dev.copy_(d_h, non_blocking=True)
+        if world > 1:
+            dist.broadcast(d_dev, 0)
+        plan.apply_adjoint_raw(d_dev, m_out, s)
+        mout_h.copy_(m_out, non_blocking=True)
+
+    for _ in range(2):
+        step_e2e()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_e2e()
+    e1.record(stream)
+    barrier()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_e2e = float(t.item())
+    e2e_value = world * step_bytes / (ms_e2e * 1e-3) / 1e9
+    h2d = 8 * (nm * nt + (nd * nt if rank == 0 else 0))
+    d2h = 8 * (nd * nt + nm * nt)
+
+    # ---- roofline of the dominant kernels (GEMV-N / GEMV-H), live events
+    peak, peak_kind = peaks()
+    ncall = stages["calls"]
+    gemv_n_ms = stages["F"][1] / max(1, ncall[0])
+    gemv_h_ms = stages["Fstar"][1] / max(1, ncall[1])
+    gb = gemv_bytes(nd, nm, nt)
+    ach_n = gb / (gemv_n_ms * 1e-3) / 1e9
+    ach_h = gb / (gemv_h_ms * 1e-3) / 1e9
+    total_stage = sum(stages["F"]) + sum(stages["Fstar"])
+    traffic = load_traffic()
+    dominant = "gemv_h" if gemv_h_ms >= gemv_n_ms else "gemv_n"
+    roof = {
+        "bound": "hbm", "kernel": dominant,
+        "achieved": ach_h if dominant == "gemv_h" else ach_n,
+        "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+        "frac": (ach_h if dominant == "gemv_h" else ach_n) / peak,
+        "traffic": (traffic or {}).get(dominant),
+        "algorithmic_bytes_per_launch": gb,
+        "gemv_n": {"ms": gemv_n_ms, "achieved": ach_n, "frac": ach_n / peak},
+        "gemv_h": {"ms": gemv_h_ms, "achieved": ach_h, "frac": ach_h / peak},
+        "stage_share": {
+            "F_r2c": stages["F"][0] / total_stage, "gemv_n": stages["F"][1] / total_stage,
+            "F_c2r": stages["F"][2] / total_stage, "Fstar_r2c": stages["Fstar"][0] / total_stage,
+            "gemv_h": stages["Fstar"][1] / total_stage, "Fstar_c2r": stages["Fstar"][2] / total_stage},
+    }
+    f_ms = sum(stages["F"]) / max(1, ncall[0])
+    fs_ms = sum(stages["Fstar"]) / max(1, ncall[1])
+
+    online = None
+    if rank == 0 and not args.no_online:
+        online = bench_online(ltb, torch)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            res = cpu_reference_run(nd, nt, seed, min(nm, args.cpu_sample_cols), os.cpu_count() or 1, 3)
+            if res:
+                cpu = {"value": res["gbs"], "unit": "GB/s", "cores": os.cpu_count() or 1,
+                       "kind": "reference", "sample": res["sample"],
+                       "ms_per_pair_extrapolated_to_workload":
+                           (res["t_apply"] + res["t_adjoint"]) * 1e3 * nm / min(nm, args.cpu_sample_cols)}
+        except Exception as exc:  # baseline failure must not hide the GPU number
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count() or 1,
+                   "kind": "reference", "sample": "failed: %s" % exc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (counter-based generator kernel, torch.rand vectors)",
+            "config": {"workload": "%s: Nd=%d, Nt=%d, Nm=%d per GPU (Nm_total=%d), F-hat %.1f GB/GPU"
+                                   % (args.workload, nd, nt, nm, nm * world,
+                                      16 * (nt + 1) * nd * nm / 1e9),
+                       "step": "one F m + one F* d", "l2": "inputs larger than L2 (F-hat streamed)",
+                       "parallelism": "Nm sharded x%d (NCCL all-reduce of F m, broadcast of d)" % world},
+            "f_ms": f_ms, "fstar_ms": fs_ms,
+            "hbm_frac_step": value / world / peak,
+            "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": roof,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "online": online,
+            "cpu_baseline": cpu,
+            "plan_build_s": t_build,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    del s, plan
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cascadia", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-online", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-cols", type=int, default=2048)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,183 @@
+/*
+ * ltb.h -- C ABI of the B200-native online hot path of arXiv 2504.16344
+ * (libltb.so, built from paper_2504_16344_b200/csrc for sm_100a).
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.
+ * Each entry point names the reference interface it replaces (paths relative
+ * to the reference's proj/ directory).  INTEGRATION.md shows the
+ * reference-side binding (a drop-in fft_matvec.cpp over this ABI, and the
+ * ctypes stub the Python tests use).
+ *
+ * Conventions -- identical to the reference's MatvecPlan
+ * (include/ltibayes/fft_matvec.hpp:12-28):
+ *   - series are SpaceMajorRows: row r's N_t samples contiguous
+ *     (core.hpp:53,73-77);
+ *   - kernels are [row][col][lag], lag contiguous (core.hpp:114-140);
+ *   - padded length exactly 2 N_t, N_f = N_t + 1 frequencies, forward
+ *     transform unnormalised, inverse scaled by 1/(2 N_t), first N_t samples
+ *     kept;
+ *   - F-hat is stored per frequency as a column-major rows x cols complex
+ *     block, row fastest (fft_matvec.cpp:44-46): khat[f][c][r].
+ *
+ * Errors: every call returns an ltb_status; ltb_last_error() gives the
+ * thread-local message.  The codes map one-to-one onto the reference's
+ * exception taxonomy (core.hpp:12-35): DimensionError, LayoutError,
+ * NumericalError, CapacityError, StateError.
+ *
+ * Threading: a plan is immutable after creation and may be shared; each
+ * concurrent caller needs its own scratch (= MatvecPlan::Scratch,
+ * fft_matvec.hpp:45-58), which owns a CUDA stream and device workspace.
+ * Host-pointer calls are synchronous (the reference's apply_raw semantics);
+ * device-pointer calls are asynchronous on the scratch's stream.
+ */
+#ifndef LTB_H
+#define LTB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LTB_OK = 0,
+  LTB_DIMENSION = 1, /* DimensionError  (core.hpp:12) */
+  LTB_LAYOUT = 2,    /* LayoutError     (core.hpp:15) */
+  LTB_NUMERICAL = 3, /* NumericalError  (core.hpp:24) */
+  LTB_CAPACITY = 4,  /* CapacityError   (core.hpp:27) */
+  LTB_STATE = 5,     /* StateError      (core.hpp:30) */
+  LTB_CUDA = 6,      /* CUDA runtime failure (no reference analogue) */
+  LTB_INVALID = 7    /* null handle / bad argument */
+} ltb_status;
+
+typedef enum { LTB_PTR_HOST = 0, LTB_PTR_DEVICE = 1 } ltb_ptr_kind;
+
+/* KernelTag (core.hpp:103) */
+typedef enum { LTB_TAG_F = 0, LTB_TAG_FQ = 1, LTB_TAG_GSTAR = 2, LTB_TAG_GQSTAR = 3 } ltb_tag;
+
+/* Layout (core.hpp:53) */
+typedef enum { LTB_TIME_MAJOR_BLOCKS = 0, LTB_SPACE_MAJOR_ROWS = 1 } ltb_layout;
+
+typedef struct ltb_plan ltb_plan;
+typedef struct ltb_scratch ltb_scratch;
+typedef struct ltb_engine ltb_engine;
+
+typedef struct {
+  int device;    /* CUDA ordinal; -1 = current device */
+  int unit_cols; /* GEMV work-unit width in columns; 0 = automatic */
+} ltb_opts;
+
+const char* ltb_last_error(void);
+const char* ltb_version(void);
+/* number of kernels this library launched since load (all threads) */
+uint64_t ltb_kernel_launches(void);
+
+/* ---- MatvecPlan (fft_matvec.hpp:29-78, ctor fft_matvec.cpp:73-111) ---- */
+
+/* Plan from an explicit kernel tensor [rows][cols][nt] (host or device
+ * pointer).  Scans for non-finite entries (core.cpp:73-77 -> LTB_NUMERICAL)
+ * and builds F-hat on the device. */
+ltb_status ltb_plan_create(const double* kernel_rck, int rows, int cols, int nt, int tag,
+                           int ptr_kind, const ltb_opts* opts, ltb_plan** out);
+
+/* Plan whose kernel is generated in place on the device by the counter
+ * generator: k(r, c, t) = U(seed, stream, (r * nm_total + c0 + c) * nt + t),
+ * c in [0, cols) -- a column shard [c0, c0+cols) of an rows x nm_total
+ * kernel.  Needed at Cascadia scale, where the 66 GB time-domain kernel
+ * cannot round-trip through host memory. */
+ltb_status ltb_plan_create_generated(int rows, int cols, int nt, int tag, uint64_t seed,
+                                     uint64_t stream, long long nm_total, long long c0,
+                                     const ltb_opts* opts, ltb_plan** out);
+
+ltb_status ltb_plan_destroy(ltb_plan* plan);
+
+/* rows_out / n_cols / n_time / padded_len / n_freq / tag (fft_matvec.hpp:38-43) */
+ltb_status ltb_plan_dims(const ltb_plan* plan, int* rows_out, int* n_cols, int* n_time,
+                         int* padded_len, int* n_freq, int* tag);
+
+/* device bytes held by the plan (F-hat + tables) */
+ltb_status ltb_plan_bytes(const ltb_plan* plan, size_t* bytes);
+
+/* kernel_hat_sqnorm (fft_matvec.cpp:124-137) */
+ltb_status ltb_kernel_hat_sqnorm(const ltb_plan* plan, double* out);
+
+/* copy F-hat frequencies [f0, f0+nfreq) to host, [f][c][r] complex
+ * interleaved (test/diagnostic access) */
+ltb_status ltb_plan_copy_kernel_hat(const ltb_plan* plan, int f0, int nfreq, double* host_out);
+
+/* ---- Scratch (fft_matvec.hpp:45-58) ---- */
+/* cuda_stream: a cudaStream_t to run on, NULL for a private (non-blocking)
+ * stream, or (void*)1 (cudaStreamLegacy) for the legacy default stream */
+ltb_status ltb_scratch_create(const ltb_plan* plan, void* cuda_stream, ltb_scratch** out);
+ltb_status ltb_scratch_destroy(ltb_scratch* s);
+ltb_status ltb_scratch_sync(ltb_scratch* s);
+/* the scratch's cudaStream_t (for event timing by the caller) */
+void* ltb_scratch_stream(ltb_scratch* s);
+
+/* Per-stage device timing of the applies run on this scratch: with timing
+ * enabled, CUDA events are recorded on the scratch's stream around each
+ * kernel.  enable != 0 clears and starts accumulation, 0 stops it. */
+ltb_status ltb_scratch_timing(ltb_scratch* s, int enable);
+/* Accumulated milliseconds since timing was enabled (synchronizes):
+ * ms[0..2] = F (pad+r2c, GEMV-N, c2r), ms[3..5] = F* (pad+r2c, GEMV-H, c2r);
+ * calls[0] / calls[1] = number of F / F* applies timed. */
+ltb_status ltb_scratch_stage_ms(ltb_scratch* s, double* ms6, int* calls2);
+
+/* ---- apply_raw / apply_adjoint_raw (fft_matvec.cpp:139-217) ---- */
+/* d = F m: in n_cols*N_t, out rows_out*N_t, SpaceMajorRows */
+ltb_status ltb_apply(const ltb_plan* plan, ltb_scratch* s, const double* in, double* out,
+                     int ptr_kind);
+/* m = F* d: in rows_out*N_t, out n_cols*N_t */
+ltb_status ltb_apply_adjoint(const ltb_plan* plan, ltb_scratch* s, const double* in,
+                             double* out, int ptr_kind);
+
+/* ---- typed apply / apply_adjoint (fft_matvec.cpp:221-265) ----
+ * Checks the layout tag (LTB_LAYOUT unless SpaceMajorRows: "no silent
+ * reindex") and the series dims (LTB_DIMENSION), then applies. */
+ltb_status ltb_apply_series(const ltb_plan* plan, ltb_scratch* s, const double* in,
+                            int n_rows, int n_time, int layout, double* out, int ptr_kind);
+ltb_status ltb_apply_adjoint_series(const ltb_plan* plan, ltb_scratch* s, const double* in,
+                                    int n_rows, int n_time, int layout, double* out,
+                                    int ptr_kind);
+
+/* ---- online subset of InferenceEngine (bayes_engine.hpp:83-107) ---- */
+
+/* Engine over the G* plan (prior-premultiplied kernel, bayes_engine.cpp:105,
+ * 112) and an optional F_q plan for the forecast.  The plans must outlive
+ * the engine. */
+ltb_status ltb_engine_create(const ltb_plan* plan_gstar, const ltb_plan* plan_fq,
+                             const ltb_opts* opts, ltb_engine** out);
+ltb_status ltb_engine_destroy(ltb_engine* e);
+
+/* set_factor (bayes_engine.cpp:211-217): lower Cholesky factor of K,
+ * n = N_d * N_t, column-major with leading dimension ld; only the lower
+ * triangle is read (the strict upper part may hold K itself,
+ * bayes_engine.cpp:180-193).  Repacked on the device into lower tiles. */
+ltb_status ltb_engine_set_factor(ltb_engine* e, const double* L, int n, size_t ld,
+                                 int ptr_kind);
+/* synthetic factor generated on the device (oracle orc_gen_factor) */
+ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed);
+
+/* solve_k_inplace (bayes_engine.cpp:236-240): y <- L^{-T} L^{-1} y */
+ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, int ptr_kind);
+
+/* infer_map timed region (bayes_engine.cpp:311-320): m_map = G* K^{-1} d.
+ * seconds (nullable) receives the device time of the call. */
+ltb_status ltb_engine_infer_map(const ltb_engine* e, ltb_scratch* s, const double* d,
+                                double* m_map, double* seconds, int ptr_kind);
+
+/* forecast q = F_q m (acceptance_main.cpp:243-264 route) */
+ltb_status ltb_engine_forecast(const ltb_engine* e, ltb_scratch* s, const double* m,
+                               double* q, int ptr_kind);
+
+/* infer_map + forecast in one call: m_map and q (either nullable) */
+ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e, ltb_scratch* s,
+                                         const double* d, double* m_map, double* q,
+                                         double* seconds, int ptr_kind);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LTB_H */

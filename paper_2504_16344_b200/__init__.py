@@ -1,0 +1,13 @@
+"""B200-native online hot path of arXiv 2504.16344 (block-Toeplitz F / F*
+matvec, K^{-1} apply, posterior mean and QoI forecast).
+
+The compute path is libltb.so (sm_100a CUDA kernels behind the C ABI in
+include/ltb.h); this package is the host-side mirror of the reference's
+``ltibayes`` C++ API.  See DESIGN.md.
+"""
+from ._lib import build, kernel_launches, last_error, load  # noqa: F401
+from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, CudaError,  # noqa: F401
+                     DimensionError, KernelTag, Layout, LayoutError, LtbError, MatvecPlan,
+                     NumericalError, ObsSeries, QoISeries, SpaceTimeField, StateError,
+                     algorithmic_bytes, reindex)
+from .engine import InferenceEngine, MapResult  # noqa: F401

@@ -1,0 +1,86 @@
+"""Loader for libltb.so (the sm_100a hot path behind include/ltb.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+usable, every compute call raises.  ``build()`` compiles the library in-tree
+with nvcc (``paper_2504_16344_b200/Makefile``).
+"""
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libltb.so")
+
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+# every symbol declared in include/ltb.h, with its ctypes signature
+SIGNATURES = {
+    "ltb_last_error": ([], C.c_char_p),
+    "ltb_version": ([], C.c_char_p),
+    "ltb_kernel_launches": ([], C.c_uint64),
+    "ltb_plan_create": ([_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_plan_create_generated": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                   C.c_longlong, C.c_longlong, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_plan_destroy": ([_vp], C.c_int),
+    "ltb_plan_dims": ([_vp] + [C.POINTER(C.c_int)] * 6, C.c_int),
+    "ltb_plan_bytes": ([_vp, C.POINTER(C.c_size_t)], C.c_int),
+    "ltb_kernel_hat_sqnorm": ([_vp, _dp], C.c_int),
+    "ltb_plan_copy_kernel_hat": ([_vp, C.c_int, C.c_int, _dp], C.c_int),
+    "ltb_scratch_create": ([_vp, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_scratch_destroy": ([_vp], C.c_int),
+    "ltb_scratch_sync": ([_vp], C.c_int),
+    "ltb_scratch_stream": ([_vp], _vp),
+    "ltb_scratch_timing": ([_vp, C.c_int], C.c_int),
+    "ltb_scratch_stage_ms": ([_vp, _dp, C.POINTER(C.c_int)], C.c_int),
+    "ltb_apply": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_apply_adjoint": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_apply_series": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int], C.c_int),
+    "ltb_apply_adjoint_series": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int], C.c_int),
+    "ltb_engine_create": ([_vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_engine_destroy": ([_vp], C.c_int),
+    "ltb_engine_set_factor": ([_vp, _vp, C.c_int, C.c_size_t, C.c_int], C.c_int),
+    "ltb_engine_set_factor_generated": ([_vp, C.c_int, C.c_uint64], C.c_int),
+    "ltb_engine_solve_k": ([_vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_engine_infer_map": ([_vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
+    "ltb_engine_forecast": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_engine_infer_and_forecast": ([_vp, _vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
+}
+
+_lib = None
+
+
+class LtbOpts(C.Structure):
+    _fields_ = [("device", C.c_int), ("unit_cols", C.c_int)]
+
+
+def build(force=False):
+    """Compile libltb.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.check_call(["make", "-s", "-C", HERE])
+    else:
+        subprocess.check_call(["make", "-s", "-C", HERE], stdout=subprocess.DEVNULL)
+
+
+def load():
+    """Load libltb.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                "libltb.so not built (%s); run __graft_entry__.build() or make -C %s" % (LIB_PATH, HERE))
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def last_error():
+    return load().ltb_last_error().decode(errors="replace")
+
+
+def kernel_launches():
+    return int(load().ltb_kernel_launches())

@@ -1,0 +1,580 @@
+// ltb_capi.cu -- the C ABI (include/ltb.h) over the sm_100a kernels.
+//
+// Object model mirrors the reference's MatvecPlan (fft_matvec.cpp:41-69):
+//   ltb_plan    <-> MatvecPlan::Impl   (owns F-hat, now in HBM, plus the
+//                                       FFT descriptor / twiddle table)
+//   ltb_scratch <-> MatvecPlan::Scratch (owns x-hat / d-hat workspaces, a
+//                                       CUDA stream, host staging buffers)
+//   ltb_engine  <-> online subset of InferenceEngine (bayes_engine.cpp)
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <atomic>
+
+#include "../../include/ltb.h"
+#include "ltb_gen.cuh"
+#include "ltb_kernels.h"
+#include "ltb_trsv.h"
+
+using namespace ltb;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+ltb_status fail(ltb_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define LTB_CUDA_TRY(expr)                                                            \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(LTB_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                          \
+  } while (0)
+
+#define LTB_LAUNCH(expr, nkernels)  \
+  do {                              \
+    LTB_CUDA_TRY(expr);             \
+    g_launches += (nkernels);       \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// radix schedule for the Stockham FFT: 8s, then 4 / 2, then 3, 5, 7, then
+// any remaining primes (generic butterfly)
+bool fft_radices(int n, int* radix, int* nstages) {
+  int m = n, k = 0;
+  auto push = [&](int r) {
+    if (k >= kMaxStages) return false;
+    radix[k++] = r;
+    return true;
+  };
+  while (m % 8 == 0) { if (!push(8)) return false; m /= 8; }
+  while (m % 4 == 0) { if (!push(4)) return false; m /= 4; }
+  while (m % 2 == 0) { if (!push(2)) return false; m /= 2; }
+  for (int p : {3, 5, 7}) while (m % p == 0) { if (!push(p)) return false; m /= p; }
+  for (int p = 11; m > 1; p += 2) {
+    while (m % p == 0) { if (!push(p)) return false; m /= p; }
+    if ((long long)p * p > m && m > 1) { if (!push(m)) return false; m = 1; }
+  }
+  *nstages = k;
+  return true;
+}
+
+// W[j] = exp(-2 pi i j / n) in long double, exact at quadrant points and
+// mirrored so W[n-j] = conj(W[j])
+std::vector<double2> twiddles(int n) {
+  std::vector<double2> w(n);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int j = 0; j <= n / 2; ++j) {
+    double c, s;
+    if ((4LL * j) % n == 0) {
+      const int q = (int)((4LL * j) / n);
+      c = q == 0 ? 1.0 : (q == 2 ? -1.0 : 0.0);
+      s = q == 1 ? 1.0 : 0.0;
+    } else {
+      const long double a = two_pi * (long double)j / (long double)n;
+      c = (double)cosl(a);
+      s = (double)sinl(a);
+    }
+    w[j] = make_double2(c, -s);
+    if (j > 0 && j < n - j) w[n - j] = make_double2(c, s);
+  }
+  return w;
+}
+
+}  // namespace
+
+struct ltb_plan {
+  int device = 0;
+  int rows = 0, cols = 0, nt = 0, npad = 0, nf = 0, tag = 0;
+  double2* fhat = nullptr;
+  double2* tw = nullptr;
+  FftDesc fft{};
+  GemvShape shape{};
+  size_t bytes = 0;
+};
+
+struct ltb_scratch {
+  const ltb_plan* plan = nullptr;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double2* xhat = nullptr;      // nf * cols
+  double2* dhat = nullptr;      // nf * rows
+  double2* partials = nullptr;  // GEMV-N unit partials
+  unsigned* tickets = nullptr;
+  double* red = nullptr;        // 1024 + 4 doubles
+  double* stage_in = nullptr;   // host-pointer staging (lazily allocated)
+  double* stage_out = nullptr;
+  size_t stage_in_n = 0, stage_out_n = 0;
+  // per-stage timing (ltb_scratch_timing): 4 events per timed apply
+  bool timing = false;
+  std::vector<cudaEvent_t> events;
+  std::vector<int> event_dir;  // 0 = F, 1 = F*, per quadruple
+  size_t next_quad = 0;
+};
+
+namespace {
+cudaEvent_t* timing_quad(ltb_scratch* s, int dir) {
+  if (!s->timing) return nullptr;
+  const size_t q = s->next_quad++;
+  if (4 * (q + 1) > s->events.size()) {
+    for (int k = 0; k < 4; ++k) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      s->events.push_back(e);
+    }
+    s->event_dir.push_back(dir);
+  }
+  s->event_dir[q] = dir;
+  return &s->events[4 * q];
+}
+}  // namespace
+
+extern "C" {
+
+const char* ltb_last_error(void) { return g_err.c_str(); }
+const char* ltb_version(void) { return "ltb 0.1 (sm_100a)"; }
+uint64_t ltb_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"
+
+namespace {
+
+ltb_status plan_init(ltb_plan* p, int rows, int cols, int nt, int tag, const ltb_opts* opts) {
+  if (rows < 1 || cols < 1 || nt < 1)
+    return fail(LTB_DIMENSION, "MatvecPlan: kernel dims must be >= 1 (rows=%d cols=%d nt=%d)", rows,
+                cols, nt);
+  if (tag < 0 || tag > 3) return fail(LTB_INVALID, "MatvecPlan: bad kernel tag %d", tag);
+  p->device = (opts && opts->device >= 0) ? opts->device : -1;
+  if (p->device < 0) cudaGetDevice(&p->device);
+  p->rows = rows;
+  p->cols = cols;
+  p->nt = nt;
+  p->npad = 2 * nt;
+  p->nf = nt + 1;
+  p->tag = tag;
+  int B = 0;
+  if (fft_smem_bytes(p->npad, &B) > 227 * 1024)
+    return fail(LTB_CAPACITY, "MatvecPlan: N_t=%d exceeds the shared-memory FFT limit", nt);
+  if (!fft_radices(p->npad, p->fft.radix, &p->fft.nstages))
+    return fail(LTB_CAPACITY, "MatvecPlan: too many FFT stages for 2*N_t=%d", p->npad);
+  p->fft.n = p->npad;
+  p->shape = gemv_shape(rows, cols, p->nf, opts ? opts->unit_cols : 0);
+  const size_t fhat_bytes = sizeof(double2) * (size_t)p->nf * rows * cols;
+  size_t free_b = 0, total_b = 0;
+  LTB_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  if (fhat_bytes + (64u << 20) > free_b)
+    return fail(LTB_CAPACITY, "MatvecPlan: F-hat needs %zu bytes, %zu free on device %d", fhat_bytes,
+                free_b, p->device);
+  LTB_CUDA_TRY(cudaMalloc(&p->fhat, fhat_bytes));
+  const auto w = twiddles(p->npad);
+  LTB_CUDA_TRY(cudaMalloc(&p->tw, sizeof(double2) * w.size()));
+  LTB_CUDA_TRY(cudaMemcpy(p->tw, w.data(), sizeof(double2) * w.size(), cudaMemcpyHostToDevice));
+  p->fft.tw = p->tw;
+  p->bytes = fhat_bytes + sizeof(double2) * w.size();
+  return LTB_OK;
+}
+
+void plan_free(ltb_plan* p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  cudaFree(p->fhat);
+  cudaFree(p->tw);
+  delete p;
+}
+
+__global__ void count_nonfinite_kernel(const double* x, long long n, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) ++local;
+  if (local) atomicAdd(bad, local);
+}
+
+ltb_status ensure_stage(ltb_scratch* s, size_t nin, size_t nout) {
+  if (nin > s->stage_in_n) {
+    cudaFree(s->stage_in);
+    s->stage_in = nullptr;
+    LTB_CUDA_TRY(cudaMalloc(&s->stage_in, sizeof(double) * nin));
+    s->stage_in_n = nin;
+  }
+  if (nout > s->stage_out_n) {
+    cudaFree(s->stage_out);
+    s->stage_out = nullptr;
+    LTB_CUDA_TRY(cudaMalloc(&s->stage_out, sizeof(double) * nout));
+    s->stage_out_n = nout;
+  }
+  return LTB_OK;
+}
+
+// d = F m on device pointers, async on s->stream (fft_matvec.cpp:139-179)
+ltb_status apply_dev(const ltb_plan* p, ltb_scratch* s, const double* m, double* d) {
+  const cudaStream_t st = s->stream;
+  cudaEvent_t* ev = timing_quad(s, 0);
+  if (ev) cudaEventRecord(ev[0], st);
+  // K1: pad + r2c of the n_cols input rows -> x-hat[f][c]
+  RfftSrc src{m, 0, 1, 0, 0};
+  LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, p->cols, s->xhat, p->cols, st), 1);
+  if (ev) cudaEventRecord(ev[1], st);
+  // K2: y-hat[f][r] = sum_c F-hat[f][c][r] x-hat[f][c]  (+ in-kernel unit
+  // reduction; the launcher also zeroes the tickets with a memset node)
+  LTB_LAUNCH(launch_gemv_n(p->shape, p->fhat, s->xhat, s->partials, s->dhat, s->tickets, st), 1);
+  if (ev) cudaEventRecord(ev[2], st);
+  // K4: c2r + truncate + 1/(2 N_t) of the rows_out output rows
+  LTB_LAUNCH(launch_irfft_rows(p->fft, s->dhat, p->rows, 0, 1, p->nt, p->rows, 1.0 / p->npad, d,
+                               st),
+             1);
+  if (ev) cudaEventRecord(ev[3], st);
+  return LTB_OK;
+}
+
+// m = F* d on device pointers (fft_matvec.cpp:181-217)
+ltb_status apply_adjoint_dev(const ltb_plan* p, ltb_scratch* s, const double* d, double* m) {
+  const cudaStream_t st = s->stream;
+  cudaEvent_t* ev = timing_quad(s, 1);
+  if (ev) cudaEventRecord(ev[0], st);
+  RfftSrc src{d, 0, 1, 0, 0};
+  LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, p->rows, s->dhat, p->rows, st), 1);
+  if (ev) cudaEventRecord(ev[1], st);
+  LTB_LAUNCH(launch_gemv_h(p->shape, p->fhat, s->dhat, s->xhat, st), 1);
+  if (ev) cudaEventRecord(ev[2], st);
+  LTB_LAUNCH(launch_irfft_rows(p->fft, s->xhat, p->cols, 0, 1, p->nt, p->cols, 1.0 / p->npad, m,
+                               st),
+             1);
+  if (ev) cudaEventRecord(ev[3], st);
+  return LTB_OK;
+}
+
+using DevFn = ltb_status (*)(const ltb_plan*, ltb_scratch*, const double*, double*);
+
+ltb_status run_apply(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
+                     int ptr_kind, bool adjoint) {
+  if (!p || !s) return fail(LTB_INVALID, "apply: null plan or scratch");
+  if (s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");
+  if (!in || !out) return fail(LTB_INVALID, "apply: null input/output");
+  DeviceGuard g(p->device);
+  const size_t nin = (size_t)(adjoint ? p->rows : p->cols) * p->nt;
+  const size_t nout = (size_t)(adjoint ? p->cols : p->rows) * p->nt;
+  DevFn fn = adjoint ? apply_adjoint_dev : apply_dev;
+  if (ptr_kind == LTB_PTR_DEVICE) return fn(p, s, in, out);
+  if (ptr_kind != LTB_PTR_HOST) return fail(LTB_INVALID, "apply: bad ptr_kind %d", ptr_kind);
+  ltb_status st = ensure_stage(s, std::max(nin, nout), std::max(nin, nout));
+  if (st != LTB_OK) return st;
+  LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in, in, sizeof(double) * nin, cudaMemcpyHostToDevice, s->stream));
+  st = fn(p, s, s->stage_in, s->stage_out);
+  if (st != LTB_OK) return st;
+  LTB_CUDA_TRY(cudaMemcpyAsync(out, s->stage_out, sizeof(double) * nout, cudaMemcpyDeviceToHost, s->stream));
+  LTB_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return LTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ltb_status ltb_plan_create(const double* kernel, int rows, int cols, int nt, int tag, int ptr_kind,
+                           const ltb_opts* opts, ltb_plan** out) {
+  if (!out) return fail(LTB_INVALID, "ltb_plan_create: null out");
+  *out = nullptr;
+  if (!kernel) return fail(LTB_INVALID, "ltb_plan_create: null kernel");
+  if (rows < 1 || cols < 1 || nt < 1)
+    return fail(LTB_DIMENSION, "MatvecPlan: kernel tensor size does not match dims");
+  const size_t n = (size_t)rows * cols * nt;
+  // core.cpp:73-77: reject non-finite kernel entries
+  if (ptr_kind == LTB_PTR_HOST) {
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(kernel[i])) return fail(LTB_NUMERICAL, "MatvecPlan: non-finite kernel entry");
+  }
+  ltb_plan* p = new ltb_plan();
+  ltb_status st = plan_init(p, rows, cols, nt, tag, opts);
+  if (st != LTB_OK) {
+    plan_free(p);
+    return st;
+  }
+  DeviceGuard g(p->device);
+  double* dk = nullptr;
+  unsigned long long* bad = nullptr;
+  auto cleanup = [&](ltb_status s_) {
+    cudaFree(dk);
+    cudaFree(bad);
+    if (s_ != LTB_OK) plan_free(p);
+    return s_;
+  };
+  const double* src_ptr = kernel;
+  if (ptr_kind == LTB_PTR_HOST) {
+    if (cudaMalloc(&dk, sizeof(double) * n) != cudaSuccess ||
+        cudaMemcpy(dk, kernel, sizeof(double) * n, cudaMemcpyHostToDevice) != cudaSuccess)
+      return cleanup(fail(LTB_CUDA, "MatvecPlan: kernel upload failed: %s",
+                          cudaGetErrorString(cudaGetLastError())));
+    src_ptr = dk;
+  } else {
+    if (cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess)
+      return cleanup(fail(LTB_CUDA, "MatvecPlan: alloc failed"));
+    cudaMemset(bad, 0, sizeof(unsigned long long));
+    count_nonfinite_kernel<<<148 * 8, 256>>>(kernel, (long long)n, bad);
+    g_launches += 1;
+    unsigned long long hb = 0;
+    cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+    if (hb) return cleanup(fail(LTB_NUMERICAL, "MatvecPlan: non-finite kernel entry"));
+  }
+  // K7: F-hat[f][c][r] = r2c(pad(k[r][c][:]))[f]; logical row g = c*rows + r
+  RfftSrc src{src_ptr, 0, rows, (long long)cols, 0};
+  cudaError_t e = launch_rfft_rows(p->fft, src, nt, (long long)rows * cols, p->fhat,
+                                   (long long)rows * cols, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cleanup(fail(LTB_CUDA, "MatvecPlan: plan build: %s", cudaGetErrorString(e)));
+  g_launches += 1;
+  *out = p;
+  return cleanup(LTB_OK);
+}
+
+ltb_status ltb_plan_create_generated(int rows, int cols, int nt, int tag, uint64_t seed,
+                                     uint64_t stream, long long nm_total, long long c0,
+                                     const ltb_opts* opts, ltb_plan** out) {
+  if (!out) return fail(LTB_INVALID, "ltb_plan_create_generated: null out");
+  *out = nullptr;
+  if (c0 < 0 || nm_total < c0 + cols)
+    return fail(LTB_DIMENSION, "generated plan: shard [%lld, %lld) outside nm_total=%lld", c0,
+                c0 + cols, nm_total);
+  ltb_plan* p = new ltb_plan();
+  ltb_status st = plan_init(p, rows, cols, nt, tag, opts);
+  if (st != LTB_OK) {
+    plan_free(p);
+    return st;
+  }
+  DeviceGuard g(p->device);
+  RfftSrc src{nullptr, gen_key(seed, stream), rows, nm_total, c0};
+  cudaError_t e = launch_rfft_rows(p->fft, src, nt, (long long)rows * cols, p->fhat,
+                                   (long long)rows * cols, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    plan_free(p);
+    return fail(LTB_CUDA, "generated plan build: %s", cudaGetErrorString(e));
+  }
+  g_launches += 1;
+  *out = p;
+  return LTB_OK;
+}
+
+ltb_status ltb_plan_destroy(ltb_plan* p) {
+  plan_free(p);
+  return LTB_OK;
+}
+
+ltb_status ltb_plan_dims(const ltb_plan* p, int* rows, int* cols, int* nt, int* npad, int* nf,
+                         int* tag) {
+  if (!p) return fail(LTB_INVALID, "ltb_plan_dims: null plan");
+  if (rows) *rows = p->rows;
+  if (cols) *cols = p->cols;
+  if (nt) *nt = p->nt;
+  if (npad) *npad = p->npad;
+  if (nf) *nf = p->nf;
+  if (tag) *tag = p->tag;
+  return LTB_OK;
+}
+
+ltb_status ltb_plan_bytes(const ltb_plan* p, size_t* bytes) {
+  if (!p || !bytes) return fail(LTB_INVALID, "ltb_plan_bytes: null argument");
+  *bytes = p->bytes;
+  return LTB_OK;
+}
+
+ltb_status ltb_kernel_hat_sqnorm(const ltb_plan* p, double* out) {
+  if (!p || !out) return fail(LTB_INVALID, "ltb_kernel_hat_sqnorm: null argument");
+  DeviceGuard g(p->device);
+  double* work = nullptr;
+  LTB_CUDA_TRY(cudaMalloc(&work, sizeof(double) * (1024 + 4)));
+  const long long bc = (long long)p->rows * p->cols;
+  double h[3];
+  cudaError_t e = launch_sqnorm(p->fhat, bc * p->nf, work, work + 1024, 0);
+  if (e == cudaSuccess) e = launch_sqnorm(p->fhat, bc, work, work + 1025, 0);
+  if (e == cudaSuccess) e = launch_sqnorm(p->fhat + bc * (p->nf - 1), bc, work, work + 1026, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(h, work + 1024, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(work);
+  if (e != cudaSuccess) return fail(LTB_CUDA, "kernel_hat_sqnorm: %s", cudaGetErrorString(e));
+  g_launches += 6;
+  // interior frequencies appear twice in the full circulant spectrum
+  *out = 2 * h[0] - (h[1] + h[2]);
+  return LTB_OK;
+}
+
+ltb_status ltb_plan_copy_kernel_hat(const ltb_plan* p, int f0, int nfreq, double* host_out) {
+  if (!p || !host_out) return fail(LTB_INVALID, "copy_kernel_hat: null argument");
+  if (f0 < 0 || nfreq < 0 || f0 + nfreq > p->nf)
+    return fail(LTB_DIMENSION, "copy_kernel_hat: frequency range out of bounds");
+  DeviceGuard g(p->device);
+  const size_t bc = (size_t)p->rows * p->cols;
+  LTB_CUDA_TRY(cudaMemcpy(host_out, p->fhat + bc * f0, sizeof(double2) * bc * nfreq,
+                          cudaMemcpyDeviceToHost));
+  return LTB_OK;
+}
+
+ltb_status ltb_scratch_create(const ltb_plan* p, void* stream, ltb_scratch** out) {
+  if (!p || !out) return fail(LTB_INVALID, "ltb_scratch_create: null argument");
+  *out = nullptr;
+  DeviceGuard g(p->device);
+  ltb_scratch* s = new ltb_scratch();
+  s->plan = p;
+  s->device = p->device;
+  auto bail = [&](cudaError_t e) {
+    ltb_scratch_destroy(s);
+    return fail(LTB_CUDA, "ltb_scratch_create: %s", cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if (stream) {
+    s->stream = (cudaStream_t)stream;
+  } else {
+    if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(e);
+    s->own_stream = true;
+  }
+  const size_t nx = (size_t)p->nf * p->cols, nd = (size_t)p->nf * p->rows;
+  if ((e = cudaMalloc(&s->xhat, sizeof(double2) * nx)) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->dhat, sizeof(double2) * nd)) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->partials, sizeof(double2) * gemv_n_partials(p->shape))) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->tickets, sizeof(unsigned) * (size_t)p->nf * gemv_n_row_tiles(p->shape))) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->red, sizeof(double) * (1024 + 8))) != cudaSuccess) return bail(e);
+  *out = s;
+  return LTB_OK;
+}
+
+ltb_status ltb_scratch_destroy(ltb_scratch* s) {
+  if (!s) return LTB_OK;
+  DeviceGuard g(s->device);
+  // a borrowed stream may already be gone (its owner tears down first);
+  // cudaFree below synchronizes the device anyway
+  if (s->own_stream && s->stream) cudaStreamSynchronize(s->stream);
+  cudaFree(s->xhat);
+  cudaFree(s->dhat);
+  cudaFree(s->partials);
+  cudaFree(s->tickets);
+  cudaFree(s->red);
+  cudaFree(s->stage_in);
+  cudaFree(s->stage_out);
+  for (cudaEvent_t e : s->events) cudaEventDestroy(e);
+  if (s->own_stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return LTB_OK;
+}
+
+ltb_status ltb_scratch_sync(ltb_scratch* s) {
+  if (!s) return fail(LTB_INVALID, "ltb_scratch_sync: null scratch");
+  DeviceGuard g(s->device);
+  LTB_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return LTB_OK;
+}
+
+void* ltb_scratch_stream(ltb_scratch* s) { return s ? (void*)s->stream : nullptr; }
+
+ltb_status ltb_scratch_timing(ltb_scratch* s, int enable) {
+  if (!s) return fail(LTB_INVALID, "ltb_scratch_timing: null scratch");
+  DeviceGuard g(s->device);
+  LTB_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->timing = enable != 0;
+  s->next_quad = 0;
+  return LTB_OK;
+}
+
+ltb_status ltb_scratch_stage_ms(ltb_scratch* s, double* ms6, int* calls2) {
+  if (!s || !ms6 || !calls2) return fail(LTB_INVALID, "ltb_scratch_stage_ms: null argument");
+  DeviceGuard g(s->device);
+  LTB_CUDA_TRY(cudaStreamSynchronize(s->stream));
+  for (int k = 0; k < 6; ++k) ms6[k] = 0.0;
+  calls2[0] = calls2[1] = 0;
+  for (size_t q = 0; q < s->next_quad; ++q) {
+    const int dir = s->event_dir[q];
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      LTB_CUDA_TRY(cudaEventElapsedTime(&ms, s->events[4 * q + k], s->events[4 * q + k + 1]));
+      ms6[3 * dir + k] += ms;
+    }
+    calls2[dir] += 1;
+  }
+  return LTB_OK;
+}
+
+ltb_status ltb_apply(const ltb_plan* p, ltb_scratch* s, const double* in, double* out, int ptr_kind) {
+  return run_apply(p, s, in, out, ptr_kind, false);
+}
+
+ltb_status ltb_apply_adjoint(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
+                             int ptr_kind) {
+  return run_apply(p, s, in, out, ptr_kind, true);
+}
+
+static ltb_status check_series(const ltb_plan* p, int n_rows, int n_time, int layout, bool adjoint) {
+  if (!p) return fail(LTB_INVALID, "apply: null plan");
+  const char* what = adjoint ? "MatvecPlan::apply_adjoint" : "MatvecPlan::apply";
+  // BlockSeries::check_consistent (core.cpp:29-38)
+  if (n_rows < 1 || n_time < 1) return fail(LTB_DIMENSION, "%s: series dims must be >= 1", what);
+  // check_layout (fft_matvec.cpp:221-228)
+  if (layout != LTB_SPACE_MAJOR_ROWS)
+    return fail(LTB_LAYOUT, "%s: requires SpaceMajorRows input, got TimeMajorBlocks (no silent reindex)",
+                what);
+  const int want_rows = adjoint ? p->rows : p->cols;
+  if (n_rows != want_rows || n_time != p->nt)
+    return fail(LTB_DIMENSION, "%s: input dims (%d,%d) do not match kernel (%d,%d)", what, n_rows,
+                n_time, want_rows, p->nt);
+  return LTB_OK;
+}
+
+ltb_status ltb_apply_series(const ltb_plan* p, ltb_scratch* s, const double* in, int n_rows,
+                            int n_time, int layout, double* out, int ptr_kind) {
+  ltb_status st = check_series(p, n_rows, n_time, layout, false);
+  return st != LTB_OK ? st : run_apply(p, s, in, out, ptr_kind, false);
+}
+
+ltb_status ltb_apply_adjoint_series(const ltb_plan* p, ltb_scratch* s, const double* in,
+                                    int n_rows, int n_time, int layout, double* out,
+                                    int ptr_kind) {
+  ltb_status st = check_series(p, n_rows, n_time, layout, true);
+  return st != LTB_OK ? st : run_apply(p, s, in, out, ptr_kind, true);
+}
+
+}  // extern "C"
+
+// ---- internal hooks for ltb_engine.cu ----
+namespace ltb_internal {
+ltb_status set_error(ltb_status st, const char* msg) {
+  g_err = msg;
+  return st;
+}
+ltb_status apply_device(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
+                        bool adjoint) {
+  if (!p || !s) return fail(LTB_INVALID, "apply: null plan or scratch");
+  if (s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");
+  return adjoint ? apply_adjoint_dev(p, s, in, out) : apply_dev(p, s, in, out);
+}
+cudaStream_t scratch_stream(ltb_scratch* s) { return s->stream; }
+int plan_device(const ltb_plan* p) { return p->device; }
+void plan_dims(const ltb_plan* p, int* rows, int* cols, int* nt) {
+  *rows = p->rows;
+  *cols = p->cols;
+  *nt = p->nt;
+}
+void count_launches(uint64_t n) { g_launches += n; }
+}  // namespace ltb_internal

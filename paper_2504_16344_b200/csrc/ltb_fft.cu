@@ -1,0 +1,173 @@
+// ltb_fft.cu -- batched pad + r2c (K1, and K7 plan build) and c2r +
+// truncate + scale (K4, with the GEMV-N partial reduction fused into its
+// load) for sm_100a.  See ltb_fft.cuh for the algorithm.
+#include "ltb_gen.cuh"
+#include "ltb_kernels.h"
+
+namespace ltb {
+
+namespace {
+
+constexpr int kFftThreads = 256;
+constexpr size_t kFftSmemBudget = 110 * 1024;  // two CTAs per SM at N = 840
+constexpr size_t kFftSmemMax = 227 * 1024;
+
+LTB_DEV long long in_row_of(const RfftSrc& s, long long g) {
+  return (g % s.P) * s.Q + g / s.P + s.c0;
+}
+
+__global__ void __launch_bounds__(kFftThreads)
+    rfft_rows_kernel(const FftDesc d, const RfftSrc src, int nt, long long nrows, double2* out,
+                     long long ld, int B) {
+  extern __shared__ double2 smem[];
+  const int N = d.n;
+  double2* b0 = smem;
+  double2* b1 = smem + (size_t)B * N;
+  const long long g0 = (long long)blockIdx.x * 2 * B;
+
+  // load pairs (rows g0+2s, g0+2s+1) as z = a + i b, zero padded past nt
+  for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
+    const int s = idx / N, n = idx - s * N;
+    double va = 0.0, vb = 0.0;
+    if (n < nt) {
+      const long long ga = g0 + 2 * s, gb = ga + 1;
+      if (src.in) {
+        if (ga < nrows) va = __ldg(src.in + in_row_of(src, ga) * nt + n);
+        if (gb < nrows) vb = __ldg(src.in + in_row_of(src, gb) * nt + n);
+      } else {
+        if (ga < nrows) va = gen_uniform_keyed(src.gen_key, (uint64_t)(in_row_of(src, ga) * nt + n));
+        if (gb < nrows) vb = gen_uniform_keyed(src.gen_key, (uint64_t)(in_row_of(src, gb) * nt + n));
+      }
+    }
+    b0[idx] = make_double2(va, vb);
+  }
+  __syncthreads();
+  const double2* Y = fft_batched(d, b0, b1, B);
+
+  // unpack: A[k] = (Z[k] + conj Z[N-k]) / 2, B[k] = -i (Z[k] - conj Z[N-k]) / 2
+  const int nf = nt + 1;
+  const int tile = 2 * B;
+  for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
+    const int k = idx / tile, j = idx - k * tile;
+    const long long g = g0 + j;
+    if (g >= nrows) continue;
+    const int s = j >> 1;
+    const double2 zk = Y[(size_t)s * N + k];
+    const double2 zn = Y[(size_t)s * N + (k == 0 ? 0 : N - k)];
+    double2 v;
+    if ((j & 1) == 0) {
+      v = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
+    } else {
+      // d = zk - conj(zn); B = -i d / 2 = (d.y, -d.x) / 2
+      const double dx = zk.x - zn.x, dy = zk.y + zn.y;
+      v = make_double2(0.5 * dy, -0.5 * dx);
+    }
+    out[(long long)k * ld + g] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kFftThreads)
+    irfft_rows_kernel(const FftDesc d, const double2* __restrict__ in, long long ld_f,
+                      long long ld_p, int nparts, int nt, long long nrows, double scale,
+                      double* __restrict__ out, int B) {
+  extern __shared__ double2 smem[];
+  const int N = d.n;
+  const int nf = nt + 1;
+  const int tile = 2 * B;
+  double2* b0 = smem;
+  double2* b1 = smem + (size_t)B * N;  // also the staging area (2B * nf <= B N + 2B)
+  const long long g0 = (long long)blockIdx.x * tile;
+
+  // gather the half spectra of the 2B rows (summing the GEMV-N partial slabs
+  // in a fixed order), FFTW c2r semantics: Im of DC / Nyquist ignored
+  for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
+    const int k = idx / tile, j = idx - k * tile;
+    const long long g = g0 + j;
+    double2 v = make_double2(0.0, 0.0);
+    if (g < nrows) {
+      const double2* p = in + (long long)k * ld_f + g;
+      v = p[0];
+      for (int q = 1; q < nparts; ++q) v = cadd(v, p[(long long)q * ld_p]);
+    }
+    if (k == 0 || k == nt) v.y = 0.0;
+    b1[(size_t)j * nf + k] = v;
+  }
+  __syncthreads();
+  // conj of the full Hermitian spectrum Z = A + i B of each pair
+  for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
+    const int s = idx / N, k = idx - s * N;
+    double2 a, b;
+    if (k <= nt) {
+      a = b1[(size_t)(2 * s) * nf + k];
+      b = b1[(size_t)(2 * s + 1) * nf + k];
+    } else {
+      a = conjg(b1[(size_t)(2 * s) * nf + (N - k)]);
+      b = conjg(b1[(size_t)(2 * s + 1) * nf + (N - k)]);
+    }
+    // Z = (a.x - b.y) + i (a.y + b.x); store conj(Z)
+    b0[idx] = make_double2(a.x - b.y, -(a.y + b.x));
+  }
+  __syncthreads();
+  // ifft(Z) = conj(fft(conj Z)): a = Re Y, b = -Im Y
+  const double2* Y = fft_batched(d, b0, b1, B);
+  for (int idx = threadIdx.x; idx < tile * nt; idx += blockDim.x) {
+    const int j = idx / nt, n = idx - j * nt;
+    const long long g = g0 + j;
+    if (g >= nrows) continue;
+    const double2 y = Y[(size_t)(j >> 1) * N + n];
+    const double v = (j & 1) ? -y.y : y.x;
+    out[g * nt + n] = v * scale;
+  }
+}
+
+int pairs_for(int n) {
+  const size_t per = (size_t)(2 * n + 2) * sizeof(double2);
+  int b = (int)(kFftSmemBudget / per);
+  if (b < 1) b = 1;
+  if (b > 16) b = 16;
+  return b;
+}
+
+}  // namespace
+
+size_t fft_smem_bytes(int n, int* pairs_per_cta) {
+  const int b = pairs_for(n);
+  if (pairs_per_cta) *pairs_per_cta = b;
+  return (size_t)(2 * b * n + 2 * b) * sizeof(double2);
+}
+
+static cudaError_t prep_smem(const void* fn, size_t smem) {
+  if (smem > kFftSmemMax) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long long nrows,
+                             double2* out, long long ld, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  int B;
+  const size_t smem = fft_smem_bytes(d.n, &B);
+  cudaError_t e = prep_smem((const void*)rfft_rows_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const long long grid = (nrows + 2 * B - 1) / (2 * B);
+  rfft_rows_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(d, src, nt, nrows, out, ld, B);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_f,
+                              long long ld_p, int nparts, int nt, long long nrows,
+                              double scale, double* out, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  int B;
+  const size_t smem = fft_smem_bytes(d.n, &B);
+  cudaError_t e = prep_smem((const void*)irfft_rows_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const long long grid = (nrows + 2 * B - 1) / (2 * B);
+  irfft_rows_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(d, in, ld_f, ld_p, nparts, nt,
+                                                               nrows, scale, out, B);
+  return cudaGetLastError();
+}
+
+}  // namespace ltb

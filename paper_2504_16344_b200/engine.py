@@ -1,0 +1,121 @@
+"""Online subset of the reference's ``InferenceEngine`` over libltb.so.
+
+Mirrors ``proj/include/ltibayes/bayes_engine.hpp:83-107``: ``set_factor``,
+``solve_k_inplace``, ``infer_map`` (the timed region of
+bayes_engine.cpp:307-320: copy d, K^{-1} via the Cholesky pair, G* apply) and
+the F_q forecast of ``m_map`` (acceptance_main.cpp:243-264).  The offline
+phases (form_K, factorize, form_Q, ...) are out of scope; their artifacts --
+the factor and the G*/F_q kernels -- are inputs here.
+"""
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .matvec import (Layout, MatvecPlan, ObsSeries, QoISeries, SpaceTimeField, StateError,
+                     DimensionError, LayoutError, _buffer, _opts, check)
+
+
+@dataclass
+class MapResult:
+    m_map: SpaceTimeField
+    seconds: float
+    q_map: QoISeries = None
+
+
+class InferenceEngine:
+    """Device-resident online engine: factor of K, G* plan, optional F_q plan."""
+
+    def __init__(self, plan_gstar, plan_fq=None, device=None):
+        self.plan_g = plan_gstar
+        self.plan_fq = plan_fq
+        h = C.c_void_p()
+        opts = _opts(device)
+        check(_lib.load().ltb_engine_create(plan_gstar._h, plan_fq._h if plan_fq else None,
+                                            C.byref(opts), C.byref(h)))
+        self._h = h
+        self._scratch = MatvecPlan.Scratch(plan_gstar)
+        self.n_sensors = plan_gstar.rows_out()
+        self.n_space = plan_gstar.n_cols()
+        self.n_time = plan_gstar.n_time()
+        self.n_qoi = plan_fq.rows_out() if plan_fq else 0
+
+    def n_data(self):
+        return self.n_sensors * self.n_time
+
+    def close(self):
+        if getattr(self, "_h", None):
+            # the engine's internal F_q scratch borrows this scratch's stream:
+            # destroy the engine first
+            _lib.load().ltb_engine_destroy(self._h)
+            self._h = None
+            self._scratch.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_factor(self, chol_lower):
+        """bayes_engine.cpp:211-217.  ``chol_lower`` is the (n, n) factor;
+        only its lower triangle is read."""
+        L = np.asarray(chol_lower, dtype=np.float64)
+        n = L.shape[0]
+        if L.shape != (n, n):
+            raise DimensionError("set_factor: wrong factor dims")
+        Lf = np.asfortranarray(L)  # the ABI takes column-major (Eigen) storage
+        check(_lib.load().ltb_engine_set_factor(self._h, C.c_void_p(Lf.ctypes.data), n, n, 0))
+
+    def set_factor_generated(self, seed):
+        check(_lib.load().ltb_engine_set_factor_generated(self._h, self.n_data(), seed))
+
+    def solve_k_inplace(self, y, scratch=None):
+        """bayes_engine.cpp:236-240: y <- K^{-1} y (numpy or CUDA tensor)."""
+        p, kind, keep = _buffer(y, self.n_data(), "solve_k_inplace", writable=True)
+        check(_lib.load().ltb_engine_solve_k(self._h, (scratch or self._scratch)._h, p, kind))
+        return y
+
+    def _check_obs(self, d, what):
+        d.check_consistent(what)
+        if d.layout != Layout.SpaceMajorRows:
+            raise LayoutError("%s: requires SpaceMajorRows" % what)
+        if d.n_rows != self.n_sensors or d.n_time != self.n_time:
+            raise DimensionError("%s: dims do not match engine" % what)
+
+    def infer_map(self, d_obs, with_forecast=False):
+        """m_map = G* K^{-1} d_obs (+ q_map = F_q m_map); ``seconds`` is the
+        device time of the call."""
+        self._check_obs(d_obs, "infer_map")
+        m = SpaceTimeField(self.n_space, self.n_time, Layout.SpaceMajorRows)
+        q = QoISeries(self.n_qoi, self.n_time, Layout.SpaceMajorRows) if with_forecast else None
+        secs = C.c_double()
+        check(_lib.load().ltb_engine_infer_and_forecast(
+            self._h, self._scratch._h, C.c_void_p(d_obs.values.ctypes.data),
+            C.c_void_p(m.values.ctypes.data), C.c_void_p(q.values.ctypes.data) if q else None,
+            C.byref(secs), 0))
+        return MapResult(m, secs.value, q)
+
+    def infer_raw(self, d, m_map, q=None, scratch=None):
+        """Raw-pointer variant (numpy host arrays or CUDA tensors); returns the
+        device seconds."""
+        pd, kd, _a = _buffer(d, self.n_data(), "infer d")
+        pm, km, _b = _buffer(m_map, self.n_space * self.n_time, "infer m_map", writable=True)
+        pq = None
+        if q is not None:
+            pq, kq, _c = _buffer(q, self.n_qoi * self.n_time, "infer q", writable=True)
+        secs = C.c_double()
+        check(_lib.load().ltb_engine_infer_and_forecast(self._h, (scratch or self._scratch)._h,
+                                                        pd, pm, pq, C.byref(secs), kd))
+        return secs.value
+
+    def forecast(self, m_map):
+        """q = F_q m (the F_q route pinned to Q d by acceptance criterion 5)."""
+        if self.plan_fq is None:
+            raise StateError("engine: no F_q plan (forecast unavailable)")
+        q = QoISeries(self.n_qoi, self.n_time, Layout.SpaceMajorRows)
+        check(_lib.load().ltb_engine_forecast(self._h, self._scratch._h,
+                                              C.c_void_p(np.ascontiguousarray(m_map.values).ctypes.data),
+                                              C.c_void_p(q.values.ctypes.data), 0))
+        return q
