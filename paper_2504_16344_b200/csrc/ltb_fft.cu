@@ -9,7 +9,7 @@ namespace ltb {
 namespace {
 
 constexpr int kFftThreads = 256;
-constexpr size_t kFftSmemBudget = 110 * 1024;  // two CTAs per SM at N = 840
+constexpr size_t kFftSmemBudget = 56 * 1024;  // >= 4 CTAs per SM
 constexpr size_t kFftSmemMax = 227 * 1024;
 
 LTB_DEV long long in_row_of(const RfftSrc& s, long long g) {
@@ -25,6 +25,34 @@ __global__ void __launch_bounds__(kFftThreads)
   double2* b1 = smem + (size_t)B * N;
   const long long g0 = (long long)blockIdx.x * 2 * B;
 
+  if (src.bulk) {
+    // contiguous input rows g0 .. g0+2B-1: ONE bulk async copy (TMA 1-D) into
+    // the ping-pong buffer, then pair them up from shared memory
+    __shared__ uint64_t bar;
+    double* stage = reinterpret_cast<double*>(b1);
+    const long long rows_here = min((long long)2 * B, nrows - g0);
+    const long long nvals = rows_here * nt;
+    const unsigned bulk_bytes = (unsigned)((nvals * 8) & ~15ll);
+    const double* gsrc = src.in + g0 * nt;  // 16-byte aligned: g0 even, base checked by host
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(&bar, bulk_bytes);
+      if (bulk_bytes) bulk_g2s(stage, gsrc, bulk_bytes, &bar, policy_evict_first());
+      if (nvals * 8 > bulk_bytes) stage[nvals - 1] = __ldg(gsrc + nvals - 1);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
+      const int s = idx / N, n = idx - s * N;
+      double va = 0.0, vb = 0.0;
+      if (n < nt) {
+        if (2 * s < rows_here) va = stage[(size_t)(2 * s) * nt + n];
+        if (2 * s + 1 < rows_here) vb = stage[(size_t)(2 * s + 1) * nt + n];
+      }
+      b0[idx] = make_double2(va, vb);
+    }
+  } else
   // load pairs (rows g0+2s, g0+2s+1) as z = a + i b, zero padded past nt
   for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
     const int s = idx / N, n = idx - s * N;
@@ -80,14 +108,15 @@ __global__ void __launch_bounds__(kFftThreads)
 
   // gather the half spectra of the 2B rows (summing the GEMV-N partial slabs
   // in a fixed order), FFTW c2r semantics: Im of DC / Nyquist ignored
+#pragma unroll 8
   for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
     const int k = idx / tile, j = idx - k * tile;
     const long long g = g0 + j;
     double2 v = make_double2(0.0, 0.0);
     if (g < nrows) {
       const double2* p = in + (long long)k * ld_f + g;
-      v = p[0];
-      for (int q = 1; q < nparts; ++q) v = cadd(v, p[(long long)q * ld_p]);
+      v = __ldg(p);
+      for (int q = 1; q < nparts; ++q) v = cadd(v, __ldg(p + (long long)q * ld_p));
     }
     if (k == 0 || k == nt) v.y = 0.0;
     b1[(size_t)j * nf + k] = v;
@@ -152,7 +181,9 @@ cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long 
   cudaError_t e = prep_smem((const void*)rfft_rows_kernel, smem);
   if (e != cudaSuccess) return e;
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
-  rfft_rows_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(d, src, nt, nrows, out, ld, B);
+  RfftSrc s2 = src;
+  s2.bulk = (src.in && src.P == 1 && src.c0 == 0 && ((uintptr_t)src.in & 15) == 0) ? 1 : 0;
+  rfft_rows_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(d, s2, nt, nrows, out, ld, B);
   return cudaGetLastError();
 }
 

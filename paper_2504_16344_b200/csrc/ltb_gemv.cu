@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
                        unsigned* __restrict__ tickets, int RT, int CL, int cps, int NS) {
   extern __shared__ __align__(128) unsigned char bulk_smem[];
   __shared__ bool last;
-  const size_t stage_elems = (size_t)cps * s.nd;
+  // stage = [cps columns of F-hat | the cps matching x-hat values]
+  const size_t chunk_elems = (size_t)cps * s.nd;
+  const size_t stage_elems = chunk_elems + cps;
   double2* stages = reinterpret_cast<double2*>(bulk_smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(bulk_smem + NS * stage_elems * sizeof(double2));
   const int unit = blockIdx.x;
@@ -162,8 +164,11 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
     for (int i = 0; i < NS && i < nchunks; ++i) {
       const int cols = min(cps, ncols - i * cps);
       const unsigned bytes = (unsigned)(cols * s.nd * sizeof(double2));
-      mbar_arrive_expect_tx(full + i, bytes);
-      bulk_g2s(stages + (size_t)i * stage_elems, src + (size_t)i * stage_elems, bytes, full + i, policy);
+      const unsigned xbytes = (unsigned)(cols * sizeof(double2));
+      double2* dst = stages + (size_t)i * stage_elems;
+      mbar_arrive_expect_tx(full + i, bytes + xbytes);
+      bulk_g2s(dst, src + (size_t)i * chunk_elems, bytes, full + i, policy);
+      bulk_g2s(dst + chunk_elems, Xu + (size_t)i * cps, xbytes, full + i, policy);
     }
   }
   __syncthreads();
@@ -176,9 +181,10 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
     mbar_wait(full + st, (unsigned)((i / NS) & 1));
     const int cols = min(cps, ncols - i * cps);
     const double2* S = stages + (size_t)st * stage_elems;
+    const double2* XS = S + chunk_elems;
     if (active) {
       for (int cc = cl; cc < cols; cc += CL) {
-        const double2 xv = __ldg(Xu + (size_t)i * cps + cc);
+        const double2 xv = XS[cc];
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const int r = rt + k * RT;
@@ -191,8 +197,11 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
       const int j = i + NS;
       const int cols2 = min(cps, ncols - j * cps);
       const unsigned bytes = (unsigned)(cols2 * s.nd * sizeof(double2));
-      mbar_arrive_expect_tx(full + st, bytes);
-      bulk_g2s(stages + (size_t)st * stage_elems, src + (size_t)j * stage_elems, bytes, full + st, policy);
+      const unsigned xbytes = (unsigned)(cols2 * sizeof(double2));
+      double2* dst = stages + (size_t)st * stage_elems;
+      mbar_arrive_expect_tx(full + st, bytes + xbytes);
+      bulk_g2s(dst, src + (size_t)j * chunk_elems, bytes, full + st, policy);
+      bulk_g2s(dst + chunk_elems, Xu + (size_t)j * cps, xbytes, full + st, policy);
     }
   }
 
@@ -239,6 +248,90 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
 }
 
 // ---------------------------------------------------------------------------
+// GEMV-H, TMA-staged: F-hat chunks of `cps` columns arrive by bulk async copy
+// as in GEMV-N; a group of GS lanes owns one column at a time, lane l holding
+// d-hat_f[l + GS k] (k < RPL) in registers for the whole unit.  With GS >= 8 a
+// quarter-warp reads one contiguous 128-byte line per shared load, so the
+// reads are conflict-free; 32/GS columns close their dot products in the
+// same log2(GS)-level shuffle tree.  Loops are warp-uniform so every lane
+// takes part in every shuffle.
+// ---------------------------------------------------------------------------
+template <int GS, int RPL>
+__global__ void __launch_bounds__(kGemvThreads)
+    gemv_h_bulk_kernel(GemvShape s, const double2* __restrict__ fhat,
+                       const double2* __restrict__ dhat, double2* __restrict__ xo, int cps, int NS) {
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  const size_t stage_elems = (size_t)cps * s.nd;
+  double2* stages = reinterpret_cast<double2*>(bulk_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(bulk_smem + NS * stage_elems * sizeof(double2));
+  const int unit = blockIdx.x;
+  const int f = unit / s.units_per_f;
+  const int u = unit - f * s.units_per_f;
+  const long long c_begin = (long long)u * s.unit_cols;
+  const long long c_end = min(s.nm, c_begin + s.unit_cols);
+  const int ncols = (int)(c_end - c_begin);
+  const int nchunks = (ncols + cps - 1) / cps;
+  const int t = threadIdx.x;
+  const double2* src = fhat + ((long long)f * s.nm + c_begin) * s.nd;
+  uint64_t policy = 0;
+  if (t == 0) {
+    for (int k = 0; k < NS; ++k) mbar_init(full + k, 1);
+    fence_mbar_init();
+    policy = policy_evict_first();
+    for (int i = 0; i < NS && i < nchunks; ++i) {
+      const int cols = min(cps, ncols - i * cps);
+      const unsigned bytes = (unsigned)(cols * s.nd * sizeof(double2));
+      mbar_arrive_expect_tx(full + i, bytes);
+      bulk_g2s(stages + (size_t)i * stage_elems, src + (size_t)i * stage_elems, bytes, full + i, policy);
+    }
+  }
+  const int lane = t % GS;
+  constexpr int GPW = 32 / GS;  // column groups per warp
+  const int warp = t / 32, gw = (t % 32) / GS, nwarps = blockDim.x / 32;
+  double2 dv[RPL];
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int r = lane + GS * k;
+    dv[k] = r < s.nd ? __ldg(dhat + (long long)f * s.nd + r) : make_double2(0.0, 0.0);
+  }
+  double2* xout = xo + (long long)f * s.nm + c_begin;
+  __syncthreads();
+  for (int i = 0; i < nchunks; ++i) {
+    const int st = i % NS;
+    mbar_wait(full + st, (unsigned)((i / NS) & 1));
+    const int cols = min(cps, ncols - i * cps);
+    const double2* S = stages + (size_t)st * stage_elems;
+    for (int base = warp * GPW; base < cols; base += nwarps * GPW) {
+      const int cc = base + gw;
+      const bool ok = cc < cols;
+      double2 acc = make_double2(0.0, 0.0);
+      if (ok) {
+        const double2* col = S + (size_t)cc * s.nd;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+          const int r = lane + GS * k;
+          if (r < s.nd) cmac_conj(acc, col[r], dv[k]);
+        }
+      }
+#pragma unroll
+      for (int m = GS / 2; m > 0; m >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, m, GS);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, m, GS);
+      }
+      if (ok && lane == 0) xout[(size_t)i * cps + cc] = acc;
+    }
+    __syncthreads();  // stage st fully consumed
+    if (t == 0 && i + NS < nchunks) {
+      const int j = i + NS;
+      const int cols2 = min(cps, ncols - j * cps);
+      const unsigned bytes = (unsigned)(cols2 * s.nd * sizeof(double2));
+      mbar_arrive_expect_tx(full + st, bytes);
+      bulk_g2s(stages + (size_t)st * stage_elems, src + (size_t)j * stage_elems, bytes, full + st, policy);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // GEMV-H: GS lanes per column (GS = 32 for Nd >= 32), lane l owns rows
 // l + j GS; d-hat_f staged once per unit in shared memory; the dot product
 // closes with a width-GS shuffle tree.  KU independent 128-bit loads per lane
@@ -256,12 +349,17 @@ __global__ void __launch_bounds__(kGemvThreads)
   const long long c_end = min(s.nm, c_begin + s.unit_cols);
   for (int r = threadIdx.x; r < s.nd; r += blockDim.x) dsm[r] = __ldg(dhat + (long long)f * s.nd + r);
   __syncthreads();
-  const int lane = threadIdx.x % GS, grp = threadIdx.x / GS, ngrp = blockDim.x / GS;
+  const int lane = threadIdx.x % GS;
+  constexpr int GPW = 32 / GS;
+  const int warp = threadIdx.x / 32, gw = (threadIdx.x % 32) / GS, nwarps = blockDim.x / 32;
   const double2* Ff = fhat + (long long)f * s.nm * s.nd;
-  for (long long c = c_begin + grp; c < c_end; c += ngrp) {
+  // warp-uniform trip count: every lane reaches every shuffle
+  for (long long base = c_begin + warp * GPW; base < c_end; base += (long long)nwarps * GPW) {
+    const long long c = base + gw;
+    const bool ok = c < c_end;
     const double2* col = Ff + c * s.nd;
     double2 acc = make_double2(0.0, 0.0);
-    for (int r0 = lane; r0 < s.nd; r0 += GS * KU) {
+    for (int r0 = lane; ok && r0 < s.nd; r0 += GS * KU) {
       double2 a[KU];
 #pragma unroll
       for (int k = 0; k < KU; ++k) {
@@ -279,7 +377,7 @@ __global__ void __launch_bounds__(kGemvThreads)
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, m, GS);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, m, GS);
     }
-    if (lane == 0) xo[(long long)f * s.nm + c] = acc;
+    if (ok && lane == 0) xo[(long long)f * s.nm + c] = acc;
   }
 }
 
@@ -385,7 +483,7 @@ cudaError_t launch_gemv_n(const GemvShape& s, const double2* fhat, const double2
   const bool want_bulk = !(knob && strcmp(knob, "ldg") == 0);
   if (want_bulk && tiles == 1 && 2 * col_bytes <= kBulkSmem) {
     const int cps = (int)std::max<size_t>(1, kBulkStage / col_bytes);
-    const size_t stage_bytes = (size_t)cps * col_bytes;
+    const size_t stage_bytes = (size_t)cps * (col_bytes + sizeof(double2));
     const int ns = (int)std::min<size_t>(kBulkMaxStages, kBulkSmem / stage_bytes);
     const size_t red_bytes = (size_t)c.cl * c.rt * c.rpt * sizeof(double2);
     const size_t smem_al = std::max((size_t)ns * stage_bytes, red_bytes) + 8 * kBulkMaxStages;
@@ -418,9 +516,44 @@ cudaError_t launch_gemv_n(const GemvShape& s, const double2* fhat, const double2
 
 cudaError_t launch_gemv_h(const GemvShape& s, const double2* fhat, const double2* dhat,
                           double2* xo, cudaStream_t st) {
+  const dim3 grid((unsigned)((long long)s.nf * s.units_per_f));
+  // TMA-staged path for Nd <= 768 (d-hat fits the lanes' registers);
+  // LTB_GEMV_H=ldg forces the register-staged kernel (A/B tuning knob)
+  static const char* knob = getenv("LTB_GEMV_H");
+  const bool want_bulk = !(knob && strcmp(knob, "ldg") == 0);
+  const size_t col_bytes = (size_t)s.nd * sizeof(double2);
+  if (want_bulk && s.nd <= 768) {
+    const int gsb = s.nd <= 64 ? 8 : (s.nd <= 128 ? 16 : 32);
+    const int need = (s.nd + gsb - 1) / gsb;
+    const int cps = (int)std::max<size_t>(1, kBulkStage / col_bytes);
+    const size_t stage_bytes = (size_t)cps * col_bytes;
+    const int ns = (int)std::min<size_t>(kBulkMaxStages, kBulkSmem / stage_bytes);
+    const size_t smem_b = (size_t)ns * stage_bytes + 8 * kBulkMaxStages;
+#define LTB_HB(G, R)                                                                            \
+  do {                                                                                          \
+    cudaFuncSetAttribute(gemv_h_bulk_kernel<G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem_b);                                                          \
+    gemv_h_bulk_kernel<G, R><<<grid, kGemvThreads, smem_b, st>>>(s, fhat, dhat, xo, cps, ns);   \
+  } while (0)
+    if (gsb == 8) {
+      if (need <= 1) LTB_HB(8, 1);
+      else if (need <= 2) LTB_HB(8, 2);
+      else if (need <= 4) LTB_HB(8, 4);
+      else LTB_HB(8, 8);
+    } else if (gsb == 16) {
+      LTB_HB(16, 8);
+    } else {
+      if (need <= 8) LTB_HB(32, 8);
+      else if (need <= 12) LTB_HB(32, 12);
+      else if (need <= 16) LTB_HB(32, 16);
+      else if (need <= 20) LTB_HB(32, 20);
+      else LTB_HB(32, 24);
+    }
+#undef LTB_HB
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)s.nd * sizeof(double2);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  const dim3 grid((unsigned)((long long)s.nf * s.units_per_f));
   constexpr int KU = 8;
   int gs = 1;
   while (gs < 32 && gs < s.nd) gs *= 2;

@@ -17,6 +17,7 @@ struct RfftSrc {
   int P;
   long long Q;
   long long c0;
+  int bulk = 0;  // set by the launcher: contiguous, 16-byte aligned rows
 };
 
 // Forward: rows [0, nrows) of real length nt, zero padded to N = 2 nt,
