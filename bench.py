@@ -212,7 +212,8 @@ def bench_online(ltb, torch, reps=20):
         eng.solve_k_inplace(y)
         solve.append(time.perf_counter() - t0)
     solve.sort()
-    sg, sq = ltb.MatvecPlan.Scratch(g), ltb.MatvecPlan.Scratch(fq)
+    sg = ltb.MatvecPlan.Scratch(g)
+    sq = ltb.MatvecPlan.Scratch(fq, stream=sg.stream_handle)  # same stream: serialized
     sg.timing(True)
     sq.timing(True)
     for _ in range(reps):
@@ -257,12 +258,12 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nd, nm, nt, seed = WORKLOADS[args.workload]
     t_build = time.time()
-    plan = ltb.MatvecPlan.generated(nd, nm, nt, seed=seed, tag=ltb.KernelTag.F, stream=1,
-                                    nm_total=nm * world, c0=rank * nm)
+    from paper_2504_16344_b200.dist import ShardedMatvec
+    sm = ShardedMatvec(nd, nm * world, nt, seed, tag=ltb.KernelTag.F)
+    plan, s = sm.local, sm.scratch
     torch.cuda.synchronize()
     t_build = time.time() - t_build
     stream = torch.cuda.current_stream()
-    s = ltb.MatvecPlan.Scratch(plan, stream=stream)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1000 + rank)
     m = torch.rand(nm * nt, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
@@ -272,11 +273,8 @@ def run_ours(args):
     m_out = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
 
     def step():
-        plan.apply_raw(m, d_out, s)
-        if world > 1:
-            dist.all_reduce(d_out)
-            dist.broadcast(d, 0)
-        plan.apply_adjoint_raw(d, m_out, s)
+        sm.apply(m, d_out)          # local F + all-reduce over ranks
+        sm.apply_adjoint(d, m_out)  # broadcast d + local F*
 
     def barrier():
         if world > 1:
@@ -319,15 +317,11 @@ def run_ours(args):
 
     def step_e2e():
         m_dev.copy_(m_h, non_blocking=True)
-        plan.apply_raw(m_dev, d_out, s)
-        if world > 1:
-            dist.all_reduce(d_out)
+        sm.apply(m_dev, d_out)
         dout_h.copy_(d_out, non_blocking=True)
         if rank == 0:
             d_dev.copy_(d_h, non_blocking=True)
-        if world > 1:
-            dist.broadcast(d_dev, 0)
-        plan.apply_adjoint_raw(d_dev, m_out, s)
+        sm.apply_adjoint(d_dev, m_out)
         mout_h.copy_(m_out, non_blocking=True)
 
     for _ in range(2):
@@ -417,7 +411,7 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
-    del s, plan
+    del s, plan, sm
     return 0
 
 

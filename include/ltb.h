@@ -141,6 +141,14 @@ ltb_status ltb_apply_adjoint_series(const ltb_plan* plan, ltb_scratch* s, const 
                                     int n_rows, int n_time, int layout, double* out,
                                     int ptr_kind);
 
+/* ---- dense_apply (fft_matvec.hpp:80-87, fft_matvec.cpp:267-315) ----
+ * FFT-free time-domain block-Toeplitz product (the reference's test oracle,
+ * kept so the drop-in fft_matvec.cpp is link-complete).  Raises
+ * LTB_CAPACITY when rows*nt*cols*nt*8 > mem_cap_bytes (0 = no cap). */
+ltb_status ltb_dense_apply(const double* kernel_rck, int rows, int cols, int nt, const double* v,
+                           int adjoint, unsigned long long mem_cap_bytes, double* out,
+                           int ptr_kind);
+
 /* ---- online subset of InferenceEngine (bayes_engine.hpp:83-107) ---- */
 
 /* Engine over the G* plan (prior-premultiplied kernel, bayes_engine.cpp:105,

@@ -37,6 +37,8 @@ SIGNATURES = {
     "ltb_apply_adjoint": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_apply_series": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int], C.c_int),
     "ltb_apply_adjoint_series": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int], C.c_int),
+    "ltb_dense_apply": ([_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, C.c_ulonglong, _vp,
+                         C.c_int], C.c_int),
     "ltb_engine_create": ([_vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
     "ltb_engine_destroy": ([_vp], C.c_int),
     "ltb_engine_set_factor": ([_vp, _vp, C.c_int, C.c_size_t, C.c_int], C.c_int),

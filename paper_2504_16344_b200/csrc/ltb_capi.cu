@@ -12,6 +12,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <algorithm>
 #include <atomic>
 
 #include "../../include/ltb.h"
@@ -578,3 +579,75 @@ void plan_dims(const ltb_plan* p, int* rows, int* cols, int* nt) {
 }
 void count_launches(uint64_t n) { g_launches += n; }
 }  // namespace ltb_internal
+
+// ---- dense_apply (fft_matvec.cpp:267-315): FFT-free time-domain product ----
+namespace {
+// forward: out[r][j] = sum_c sum_{l<=j} k[r][c][l] m[c][j-l]
+// adjoint: out[c][j] = sum_r sum_{l<nt-j} k[r][c][l] d[r][j+l]
+__global__ void dense_apply_kernel(const double* __restrict__ k, int rows, int cols, int nt,
+                                   const double* __restrict__ v, int adjoint,
+                                   double* __restrict__ out) {
+  const long long total = (long long)(adjoint ? cols : rows) * nt;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(o / nt), j = (int)(o % nt);
+    double acc = 0.0;
+    if (!adjoint) {
+      for (int c = 0; c < cols; ++c) {
+        const double* kr = k + ((size_t)row * cols + c) * nt;
+        const double* mc = v + (size_t)c * nt;
+        for (int l = 0; l <= j; ++l) acc = fma(kr[l], mc[j - l], acc);
+      }
+    } else {
+      for (int r = 0; r < rows; ++r) {
+        const double* kr = k + ((size_t)r * cols + row) * nt;
+        const double* dr = v + (size_t)r * nt;
+        for (int l = 0; l + j < nt; ++l) acc = fma(kr[l], dr[j + l], acc);
+      }
+    }
+    out[o] = acc;
+  }
+}
+}  // namespace
+
+extern "C" ltb_status ltb_dense_apply(const double* kernel, int rows, int cols, int nt,
+                                      const double* v, int adjoint, unsigned long long cap,
+                                      double* out, int ptr_kind) {
+  if (!kernel || !v || !out) return fail(LTB_INVALID, "dense_apply: null argument");
+  if (rows < 1 || cols < 1 || nt < 1)
+    return fail(LTB_DIMENSION, "dense_apply: kernel tensor size does not match dims");
+  const unsigned long long implied =
+      (unsigned long long)rows * nt * (unsigned long long)cols * nt * 8ull;
+  if (cap != 0 && implied > cap)
+    return fail(LTB_CAPACITY, "dense_apply: implied dense operator needs %llu bytes, above the cap of %llu",
+                implied, cap);
+  const size_t nk = (size_t)rows * cols * nt;
+  const size_t nin = (size_t)(adjoint ? rows : cols) * nt, nout = (size_t)(adjoint ? cols : rows) * nt;
+  const double *dk = kernel, *dv = v;
+  double* dout = out;
+  double *tk = nullptr, *tv = nullptr, *to = nullptr;
+  auto done = [&](ltb_status s_) {
+    cudaFree(tk);
+    cudaFree(tv);
+    cudaFree(to);
+    return s_;
+  };
+  if (ptr_kind == LTB_PTR_HOST) {
+    if (cudaMalloc(&tk, nk * 8) != cudaSuccess || cudaMalloc(&tv, nin * 8) != cudaSuccess ||
+        cudaMalloc(&to, nout * 8) != cudaSuccess ||
+        cudaMemcpy(tk, kernel, nk * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(tv, v, nin * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return done(fail(LTB_CUDA, "dense_apply: staging failed"));
+    dk = tk;
+    dv = tv;
+    dout = to;
+  }
+  const long long blocks = std::min<long long>(((long long)nout + 255) / 256, 148 * 16);
+  dense_apply_kernel<<<(unsigned)blocks, 256>>>(dk, rows, cols, nt, dv, adjoint, dout);
+  g_launches += 1;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && ptr_kind == LTB_PTR_HOST) e = cudaMemcpy(out, to, nout * 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return done(fail(LTB_CUDA, "dense_apply: %s", cudaGetErrorString(e)));
+  return done(LTB_OK);
+}

@@ -131,7 +131,7 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
   size_t free_b = 0, total_b = 0;
   ENG_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t nb = (size_t)(n + kTB - 1) / kTB;
-  const size_t need = (nb * (nb + 1) / 2 + nb) * kTB * kTB * sizeof(double);
+  const size_t need = (nb * (nb + 1) / 2 + nb + 2 * nb * kLook) * kTB * kTB * sizeof(double);
   if (need + (64u << 20) > free_b)
     return efail(LTB_CAPACITY, "set_factor: packed factor needs %zu bytes, %zu free", need, free_b);
   ENG_CUDA(trsv_alloc(e->factor, n));
@@ -144,8 +144,8 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
 }
 
 ltb_status factor_finish(ltb_engine* e) {
-  cudaError_t err = trsv_invert_diag(e->factor, 0);
-  count_launches(1);
+  cudaError_t err = trsv_prepare(e->factor, 0);
+  count_launches(2);
   if (err == cudaErrorInvalidValue)
     return efail(LTB_NUMERICAL, "set_factor: zero or non-finite diagonal in the Cholesky factor");
   ENG_CUDA(err);

@@ -8,19 +8,26 @@
 
 namespace ltb {
 
-constexpr int kTB = 64;  // factor tile edge
+constexpr int kTB = 64;    // factor tile edge
+constexpr int kLook = 2;   // diagonal-chain lookahead depth (tiles per chain step)
 
 // Lower factor packed as 64x64 tiles (I, J), J <= I, tile index
 // I (I+1)/2 + J, each tile column-major (row fastest).  The last tile row /
-// column is padded with the identity.  dinv[I] holds L_II^{-1}
-// (column-major), inverted on the device once at set_factor time.
+// column is padded with the identity.  Precomputed once at set_factor time:
+//   dinv[I]     = L_II^{-1}
+//   mf[I][k-1]  = L_II^{-1} L_{I,I-k}          (k = 1..kLook, forward chain)
+//   mb[I][k-1]  = L_II^{-T} L_{I+k,I}^T        (k = 1..kLook, transposed chain)
 struct TriFactor {
   int n = 0;
   int nb = 0;
   double* tiles = nullptr;
   double* dinv = nullptr;
-  unsigned* flags = nullptr;  // 2 * nb epoch flags (forward, transposed)
-  int* status = nullptr;      // device error word (spin timeout)
+  double* mf = nullptr;
+  double* mb = nullptr;
+  double* cbuf = nullptr;     // nb * 64 worker results c_I
+  unsigned* cflag = nullptr;  // 2 * nb epoch flags (forward, transposed)
+  unsigned long long* prog = nullptr;  // 2 progress words
+  int* status = nullptr;      // device error word (spin timeout / bad pivot)
   unsigned epoch = 0;
   size_t bytes = 0;
 };
@@ -31,9 +38,12 @@ void trsv_free(TriFactor& t);
 cudaError_t trsv_pack_colmajor(TriFactor& t, const double* L, size_t ld, cudaStream_t st);
 // pack the synthetic factor (ltb_gen.cuh gen_factor_entry)
 cudaError_t trsv_pack_generated(TriFactor& t, uint64_t seed, cudaStream_t st);
-cudaError_t trsv_invert_diag(TriFactor& t, cudaStream_t st);
-// y <- L^{-T} L^{-1} y (device vector of length n); returns cudaErrorLaunchTimeout
-// if a dependency wait timed out.  Launches 2 kernels.
+// invert the diagonal tiles and build the chain tiles; returns
+// cudaErrorInvalidValue on a zero / non-finite pivot
+cudaError_t trsv_prepare(TriFactor& t, cudaStream_t st);
+// y <- L^{-T} L^{-1} y (device vector of length nb * 64, zero padded).
+// Launches 2 cooperative kernels; a dependency-wait timeout is reported
+// through t.status.
 cudaError_t trsv_solve(TriFactor& t, double* y, cudaStream_t st);
 
 }  // namespace ltb
