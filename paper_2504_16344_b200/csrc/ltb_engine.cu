@@ -159,14 +159,21 @@ ltb_status require_factor(const ltb_engine* e) {
   return LTB_OK;
 }
 
-// y (device, length n) <- K^{-1} y on stream st, through the padded buffer
-ltb_status solve_dev(const ltb_engine* e_, const double* in, double* out, cudaStream_t st) {
+// K^{-1} in (device, length n) on stream st through the padded buffer; the
+// solution is left in trsv_result(factor) and copied to `out` if given
+ltb_status solve_dev(const ltb_engine* e_, const double* in, double* out, cudaStream_t st,
+                     cudaMemcpyKind kind = cudaMemcpyDeviceToDevice) {
   ltb_engine* e = const_cast<ltb_engine*>(e_);
   const size_t n = (size_t)e->factor.n;
-  ENG_CUDA(cudaMemcpyAsync(e->ypad, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ENG_CUDA(cudaMemcpyAsync(e->ypad, in, n * sizeof(double),
+                           kind == cudaMemcpyDeviceToHost ? cudaMemcpyHostToDevice : kind, st));
   ENG_CUDA(trsv_solve(e->factor, e->ypad, st));
-  count_launches(2);
-  if (out) ENG_CUDA(cudaMemcpyAsync(out, e->ypad, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  count_launches(1);
+  if (out)
+    ENG_CUDA(cudaMemcpyAsync(out, trsv_result(e->factor), n * sizeof(double),
+                             kind == cudaMemcpyDeviceToHost ? cudaMemcpyDeviceToHost
+                                                            : cudaMemcpyDeviceToDevice,
+                             st));
   return LTB_OK;
 }
 
@@ -248,16 +255,10 @@ ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, in
   Guard gd(e->device);
   const cudaStream_t strm = scratch_stream(s);
   const size_t n = (size_t)e->factor.n;
-  if (ptr_kind == LTB_PTR_DEVICE) {
-    st = solve_dev(e, y, y, strm);
-    return st != LTB_OK ? st : check_solve_status(e, strm);
-  }
-  ltb_engine* em = const_cast<ltb_engine*>(e);
-  ENG_CUDA(cudaMemcpyAsync(em->ypad, y, n * sizeof(double), cudaMemcpyHostToDevice, strm));
-  ENG_CUDA(trsv_solve(em->factor, em->ypad, strm));
-  count_launches(2);
-  ENG_CUDA(cudaMemcpyAsync(y, em->ypad, n * sizeof(double), cudaMemcpyDeviceToHost, strm));
-  return check_solve_status(e, strm);
+  (void)n;
+  st = solve_dev(e, y, y, strm,
+                 ptr_kind == LTB_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+  return st != LTB_OK ? st : check_solve_status(e, strm);
 }
 
 ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, const double* d,
@@ -295,7 +296,7 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
   // y = K^{-1} d  (bayes_engine.cpp:312-313)
   if ((st = solve_dev(e, din, nullptr, strm)) != LTB_OK) return st;
   // m_map = G* y  (:316-319)
-  if ((st = apply_device(e->g, s, e->ypad, mout, true)) != LTB_OK) return st;
+  if ((st = apply_device(e->g, s, trsv_result(e->factor), mout, true)) != LTB_OK) return st;
   // q = F_q m_map
   if (q && (st = apply_device(e->fq, sq, mout, qout, false)) != LTB_OK) return st;
   if (ptr_kind == LTB_PTR_HOST) {

@@ -3,26 +3,27 @@
 //
 // Single-RHS TRSV is a GEMV over the packed factor (HBM bound, ~0.25
 // flop/byte) plus a sequential dependency chain over the nb = n/64 diagonal
-// blocks.  The design splits the two:
+// blocks.  Design (one cooperative persistent launch for BOTH sweeps):
 //
-//   * one persistent cooperative launch per sweep; CTA 0 is the CHAIN CTA,
-//     CTAs 1..G-1 are WORKERS;
+//   * CTA 0 is the CHAIN CTA, CTAs 1..G-1 are WORKERS;
 //   * worker rows (round robin) stream their panel tiles as soon as the
-//     needed solution blocks are published, but stop kLook tiles short of
-//     the diagonal and hand the chain c_I = L_II^{-1} (b_I - sum_{J<I-kLook}
+//     needed solution blocks exist, but stop kLook tiles short of the
+//     diagonal and hand the chain c_I = L_II^{-1} (b_I - sum_{J<I-kLook}
 //     L_IJ y_J);
 //   * the chain finishes y_I = c_I - sum_{k=1..kLook} M_{I,k} y_{I-k} with the
 //     precomputed M_{I,k} = L_II^{-1} L_{I,I-k} (prefetched into registers a
 //     step ahead) and the last kLook blocks of y kept in shared memory, so
-//     the critical path per block is one 64 x (64 kLook) GEMV plus one flag
-//     round trip -- the workers' streaming latency is hidden behind kLook
-//     chain steps;
-//   * rows complete in chain order, so one 64-bit progress word
-//     (epoch << 32 | rows done) tells every worker which blocks are final;
-//     worker results use per-row epoch flags.
-//
-// The transposed sweep is the mirror image (rows in decreasing order, panel
-// tiles read down the block column, M'_{I,k} = L_II^{-T} L_{I+k,I}^T).
+//     the critical path per 64-block is one 64 x (64 kLook) GEMV plus one
+//     L2 round trip;
+//   * no flags: every hand-off buffer (c_I, y, x) is pre-filled with a NaN
+//     sentinel (all ones, never produced by arithmetic, which yields the
+//     canonical NaN) and consumers poll the VALUES themselves with
+//     gpu-scope relaxed loads -- one L2 round trip per hand-off instead of
+//     flag + data;
+//   * the transposed sweep is the mirror image (rows descending, panel tiles
+//     down the block column, M'_{I,k} = L_II^{-T} L_{I+k,I}^T) and follows in
+//     the same launch: a worker moves on to its transposed rows as soon as its
+//     forward rows are done.
 #include <math.h>
 
 #include "ltb_common.cuh"
@@ -36,23 +37,13 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kPad = 65;                               // padded smem tile stride
 constexpr int kTile = kTB * kTB;
+constexpr unsigned long long kSentinel = ~0ull;        // all-ones NaN
 constexpr unsigned long long kSpinNs = 4000000000ull;  // 4 s dependency-wait timeout
 
-LTB_DEV unsigned long long ld_acquire64(const unsigned long long* p) {
+LTB_DEV unsigned long long ld_relaxed_u64(const double* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
-}
-LTB_DEV unsigned ld_acquire32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-LTB_DEV void st_release64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-LTB_DEV void st_release32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 LTB_DEV unsigned long long globaltimer() {
   unsigned long long t;
@@ -60,270 +51,257 @@ LTB_DEV unsigned long long globaltimer() {
   return t;
 }
 
-// Wait until the progress word reaches `need`.  On timeout (or once any CTA
-// has timed out) set *status and return `need`, so the kernel still runs to
+// Poll a hand-off value until it is no longer the sentinel.  On timeout (or
+// once any CTA timed out) set *status and return 0.0 so the kernel runs to
 // completion and the host reports the error instead of the GPU hanging.
-LTB_DEV unsigned long long wait_progress(const unsigned long long* prog, unsigned long long need,
-                                         int* status) {
-  unsigned long long v = ld_acquire64(prog);
-  if (v >= need) return v;
+LTB_DEV double poll_value(const double* p, int* status) {
+  unsigned long long v = ld_relaxed_u64(p);
+  if (v != kSentinel) return __longlong_as_double((long long)v);
   const unsigned long long t0 = globaltimer();
   while (true) {
-    v = ld_acquire64(prog);
-    if (v >= need) return v;
-    if (*(volatile int*)status) return need;
+    __nanosleep(20);
+    v = ld_relaxed_u64(p);
+    if (v != kSentinel) return __longlong_as_double((long long)v);
+    if (*(volatile int*)status) return 0.0;
     if (globaltimer() - t0 > kSpinNs) {
       atomicExch(status, 1);
-      return need;
+      return 0.0;
     }
-    __nanosleep(32);
-  }
-}
-
-LTB_DEV void wait_flag(const unsigned* flag, unsigned epoch, int* status) {
-  if (ld_acquire32(flag) == epoch) return;
-  const unsigned long long t0 = globaltimer();
-  while (ld_acquire32(flag) != epoch) {
-    if (*(volatile int*)status) return;
-    if (globaltimer() - t0 > kSpinNs) {
-      atomicExch(status, 1);
-      return;
-    }
-    __nanosleep(32);
   }
 }
 
 LTB_DEV size_t tile_off(int I, int J) { return ((size_t)I * (I + 1) / 2 + J) * kTile; }
 
-// ---------------------------------------------------------------------------
-// forward sweep: y <- L^{-1} y
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 1)
-    trsv_fwd_kernel(const double* __restrict__ tiles, const double* __restrict__ dinv,
-                    const double* __restrict__ mf, double* y, double* cbuf, unsigned* cflag,
-                    unsigned long long* prog, unsigned epoch, int nb, int* status) {
-  __shared__ double sD[kTB * kPad];
-  __shared__ double red[4][kTB];
-  __shared__ double rr[kTB];
-  __shared__ double ys[kLook][kTB];
-  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
-  const unsigned long long base = (unsigned long long)epoch << 32;
+struct SweepArgs {
+  const double* tiles;
+  const double* dinv;
+  const double* mf;
+  const double* mb;
+  const double* b;  // right-hand side (padded)
+  double* yf;       // forward result   (sentinel on entry)
+  double* xb;       // transposed result (sentinel on entry) = the solution
+  double* cf;       // forward worker hand-offs  (sentinel on entry)
+  double* cb;       // transposed worker hand-offs (sentinel on entry)
+  int nb;
+  int* status;
+};
 
-  if (blockIdx.x == 0) {
-    // ---------------- chain CTA ----------------
-    double mreg[kLook][16], mnext[kLook][16];
-    for (int I = 0; I < nb; ++I) {
-      // prefetch the chain tiles of step I+1 (independent of everything else)
-      if (I + 1 < nb) {
-#pragma unroll
-        for (int k = 0; k < kLook; ++k) {
-          if (k + 1 <= I + 1) {
-            const double* M = mf + ((size_t)(I + 1) * kLook + k) * kTile;
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk) mnext[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
-          }
-        }
-      }
-      double p = 0.0;
+struct ChainSmem {
+  double ring[kLook][kTB];
+  double red[4][kTB];
+};
+
+struct WorkerSmem {
+  double sD[kTB * kPad];
+  double red[4][kTB];
+  double rr[kTB];
+  double sR[2 * kTB];
+};
+
+// ---------------- chain, forward: y_I = c_I - sum_k M_{I,k} y_{I-k} ----------
+LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
+  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  double mreg[kLook][16], mnext[kLook][16];
+  for (int I = 0; I < a.nb; ++I) {
+    if (I + 1 < a.nb) {  // prefetch next step's chain tiles
 #pragma unroll
       for (int k = 0; k < kLook; ++k) {
-        if (k + 1 <= I) {
-          const double* yv = ys[(I - k - 1) % kLook] + 16 * q;
+        if (k + 1 <= I + 1) {
+          const double* M = a.mf + ((size_t)(I + 1) * kLook + k) * kTile;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) p = fma(mreg[k][kk], yv[kk], p);
+          for (int kk = 0; kk < 16; ++kk) mnext[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
         }
       }
-      red[q][i] = p;
-      __syncthreads();
-      if (tid < kTB) {
-        wait_flag(cflag + I, epoch, status);
-        const double c = __ldcg(cbuf + (size_t)I * kTB + tid);
-        const double v = c - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
-        y[(size_t)I * kTB + tid] = v;
-        ys[I % kLook][tid] = v;
-        __threadfence();
+    }
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < kLook; ++k) {
+      if (k + 1 <= I) {
+        const double* yv = sm.ring[(I - k - 1) % kLook] + 16 * q;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) p = fma(mreg[k][kk], yv[kk], p);
       }
-      __syncthreads();
-      if (tid == 0) st_release64(prog, base + I + 1);
-#pragma unroll
-      for (int k = 0; k < kLook; ++k)
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) mreg[k][kk] = mnext[k][kk];
     }
-    return;
-  }
-
-  // ---------------- workers ----------------
-  const int W = gridDim.x - 1, w = blockIdx.x - 1;
-  unsigned long long seen = 0;
-  for (int I = w; I < nb; I += W) {
-    const double* D = dinv + (size_t)I * kTile;
-    for (int e = tid; e < kTile; e += kThreads) sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
-    const int jmax = I - kLook;  // panel tiles J < jmax; the chain does the rest
-    const double* row = tiles + tile_off(I, 0);
-    double a[16], an[16];
-    double acc = 0.0;
-    if (jmax > 0) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = __ldg(row + (16 * q + k) * kTB + i);
-    }
-    for (int J = 0; J < jmax; ++J) {
-      if (J + 1 < jmax) {
-        const double* nt = row + (size_t)(J + 1) * kTile;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) an[k] = __ldg(nt + (16 * q + k) * kTB + i);
-      }
-      if (seen < base + J + 1) seen = wait_progress(prog, base + J + 1, status);
-      const double* yJ = y + (size_t)J * kTB + 16 * q;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) acc = fma(a[k], __ldcg(yJ + k), acc);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = an[k];
-    }
-    red[q][i] = acc;
-    __syncthreads();
-    if (tid < kTB)
-      rr[tid] = __ldcg(y + (size_t)I * kTB + tid) -
-                ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
-    __syncthreads();
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) s = fma(sD[(16 * q + k) * kPad + i], rr[16 * q + k], s);
-    red[q][i] = s;
+    sm.red[q][i] = p;
     __syncthreads();
     if (tid < kTB) {
-      cbuf[(size_t)I * kTB + tid] = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
-      __threadfence();
+      const double c = poll_value(a.cf + (size_t)I * kTB + tid, a.status);
+      const double v = c - ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
+      a.yf[(size_t)I * kTB + tid] = v;
+      sm.ring[I % kLook][tid] = v;
     }
     __syncthreads();
-    if (tid == 0) st_release32(cflag + I, epoch);
+#pragma unroll
+    for (int k = 0; k < kLook; ++k)
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) mreg[k][kk] = mnext[k][kk];
   }
 }
 
-// ---------------------------------------------------------------------------
-// transposed sweep: y <- L^{-T} y
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 1)
-    trsv_bwd_kernel(const double* __restrict__ tiles, const double* __restrict__ dinv,
-                    const double* __restrict__ mb, double* y, double* cbuf, unsigned* cflag,
-                    unsigned long long* prog, unsigned epoch, int nb, int* status) {
-  __shared__ double sD[kTB * kPad];
-  __shared__ double sR[2 * kTB];
-  __shared__ double sP[4][kTB];
-  __shared__ double rr[kTB];
-  __shared__ double xs[kLook][kTB];
-  const int tid = threadIdx.x;
-  const unsigned long long base = (unsigned long long)epoch << 32;
-
-  if (blockIdx.x == 0) {
-    // ---------------- chain CTA ----------------
-    const int i = tid & 63, q = tid >> 6;
-    double mreg[kLook][16], mnext[kLook][16];
-    for (int I = nb - 1; I >= 0; --I) {
-      if (I - 1 >= 0) {
-#pragma unroll
-        for (int k = 0; k < kLook; ++k) {
-          if (I - 1 + k + 1 < nb) {
-            const double* M = mb + ((size_t)(I - 1) * kLook + k) * kTile;
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk) mnext[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
-          }
-        }
-      }
-      double p = 0.0;
+// ---------------- chain, transposed: x_I = c_I - sum_k M'_{I,k} x_{I+k} ------
+LTB_DEV void chain_transposed(const SweepArgs& a, ChainSmem& sm) {
+  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  double mreg[kLook][16], mnext[kLook][16];
+  for (int I = a.nb - 1; I >= 0; --I) {
+    if (I - 1 >= 0) {
 #pragma unroll
       for (int k = 0; k < kLook; ++k) {
-        if (I + k + 1 < nb) {
-          const double* xv = xs[(I + k + 1) % kLook] + 16 * q;
+        if (I + k < a.nb) {  // tile (I-1, k): block row I+k exists
+          const double* M = a.mb + ((size_t)(I - 1) * kLook + k) * kTile;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) p = fma(mreg[k][kk], xv[kk], p);
+          for (int kk = 0; kk < 16; ++kk) mnext[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
         }
       }
-      sP[q][i] = p;
-      __syncthreads();
-      if (tid < kTB) {
-        wait_flag(cflag + nb + I, epoch, status);
-        const double c = __ldcg(cbuf + (size_t)I * kTB + tid);
-        const double v = c - ((sP[0][tid] + sP[1][tid]) + (sP[2][tid] + sP[3][tid]));
-        y[(size_t)I * kTB + tid] = v;
-        xs[I % kLook][tid] = v;
-        __threadfence();
+    }
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < kLook; ++k) {
+      if (I + k + 1 < a.nb) {
+        const double* xv = sm.ring[(I + k + 1) % kLook] + 16 * q;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) p = fma(mreg[k][kk], xv[kk], p);
       }
-      __syncthreads();
-      if (tid == 0) st_release64(prog, base + (unsigned long long)(nb - I));
-#pragma unroll
-      for (int k = 0; k < kLook; ++k)
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) mreg[k][kk] = mnext[k][kk];
     }
-    return;
-  }
-
-  // ---------------- workers ----------------
-  // thread (j = tid & 63, q = tid >> 6) reads row j of tile L_JI, columns
-  // [16q, 16q+16), keeping 16 partial sums of (L_JI^T x_J)
-  const int j = tid & 63, q = tid >> 6;
-  const int W = gridDim.x - 1, w = blockIdx.x - 1;
-  unsigned long long seen = 0;
-  for (int I = nb - 1 - w; I >= 0; I -= W) {
-    const double* D = dinv + (size_t)I * kTile;
-    for (int e = tid; e < kTile; e += kThreads) sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
-    double acc[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-    const int jmin = I + kLook;  // panel tiles J > jmin; the chain does the rest
-    double a[16], an[16];
-    if (nb - 1 > jmin) {
-      const double* t = tiles + tile_off(nb - 1, I);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = __ldg(t + (16 * q + k) * kTB + j);
-    }
-    for (int J = nb - 1; J > jmin; --J) {
-      if (J - 1 > jmin) {
-        const double* t = tiles + tile_off(J - 1, I);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) an[k] = __ldg(t + (16 * q + k) * kTB + j);
-      }
-      const unsigned long long need = base + (unsigned long long)(nb - J);
-      if (seen < need) seen = wait_progress(prog, need, status);
-      const double xj = __ldcg(y + (size_t)J * kTB + j);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) acc[k] = fma(a[k], xj, acc[k]);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = an[k];
-    }
-    // reduce over j: 32-lane shuffle tree per partial, then the two warps of
-    // each column quarter meet in shared memory
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      double v = acc[k];
-#pragma unroll
-      for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-      acc[k] = v;
-    }
-    if ((j & 31) == 0) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) sR[(j >> 5) * kTB + 16 * q + k] = acc[k];
-    }
-    __syncthreads();
-    if (tid < kTB) rr[tid] = __ldcg(y + (size_t)I * kTB + tid) - (sR[tid] + sR[kTB + tid]);
-    __syncthreads();
-    {
-      const int ii = tid & 63, part = tid >> 6;
-      double s = 0.0;
-      // (Dinv^T)[ii][jj] = Dinv[jj][ii] = sD[ii * kPad + jj]
-#pragma unroll
-      for (int k = 0; k < 16; ++k) s = fma(sD[ii * kPad + 16 * part + k], rr[16 * part + k], s);
-      sP[part][ii] = s;
-    }
+    sm.red[q][i] = p;
     __syncthreads();
     if (tid < kTB) {
-      cbuf[(size_t)I * kTB + tid] = (sP[0][tid] + sP[1][tid]) + (sP[2][tid] + sP[3][tid]);
-      __threadfence();
+      const double c = poll_value(a.cb + (size_t)I * kTB + tid, a.status);
+      const double v = c - ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
+      a.xb[(size_t)I * kTB + tid] = v;
+      sm.ring[I % kLook][tid] = v;
     }
     __syncthreads();
-    if (tid == 0) st_release32(cflag + nb + I, epoch);
+#pragma unroll
+    for (int k = 0; k < kLook; ++k)
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) mreg[k][kk] = mnext[k][kk];
   }
+}
+
+// ---------------- worker, forward row I ---------------------------------------
+// thread (i = tid & 63, q = tid >> 6) owns row i, columns [16q, 16q+16)
+LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, int I) {
+  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  const double* D = a.dinv + (size_t)I * kTile;
+  for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
+  const int jmax = I - kLook;  // panel tiles J < jmax; the chain does the rest
+  const double* row = a.tiles + tile_off(I, 0);
+  double t[16], tn[16];
+  double acc = 0.0;
+  if (jmax > 0) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t[k] = __ldg(row + (16 * q + k) * kTB + i);
+  }
+  for (int J = 0; J < jmax; ++J) {
+    if (J + 1 < jmax) {
+      const double* nt = row + (size_t)(J + 1) * kTile;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) tn[k] = __ldg(nt + (16 * q + k) * kTB + i);
+    }
+    const double* yJ = a.yf + (size_t)J * kTB + 16 * q;
+    unsigned long long raw[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) raw[k] = ld_relaxed_u64(yJ + k);  // 16 loads in flight
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double yv = raw[k] != kSentinel ? __longlong_as_double((long long)raw[k])
+                                            : poll_value(yJ + k, a.status);
+      acc = fma(t[k], yv, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t[k] = tn[k];
+  }
+  sm.red[q][i] = acc;
+  __syncthreads();
+  if (tid < kTB)
+    sm.rr[tid] = __ldg(a.b + (size_t)I * kTB + tid) -
+                 ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s = fma(sm.sD[(16 * q + k) * kPad + i], sm.rr[16 * q + k], s);
+  sm.red[q][i] = s;
+  __syncthreads();
+  if (tid < kTB)
+    a.cf[(size_t)I * kTB + tid] = (sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]);
+  __syncthreads();
+}
+
+// ---------------- worker, transposed row I ------------------------------------
+// thread (j = tid & 63, q = tid >> 6) reads row j of tile L_JI, columns
+// [16q, 16q+16), keeping 16 partial sums of (L_JI^T x_J)
+LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, int I) {
+  const int tid = threadIdx.x, j = tid & 63, q = tid >> 6;
+  const int nb = a.nb;
+  const double* D = a.dinv + (size_t)I * kTile;
+  for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
+  double acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+  const int jmin = I + kLook;  // panel tiles J > jmin; the chain does the rest
+  double t[16], tn[16];
+  if (nb - 1 > jmin) {
+    const double* tp = a.tiles + tile_off(nb - 1, I);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t[k] = __ldg(tp + (16 * q + k) * kTB + j);
+  }
+  for (int J = nb - 1; J > jmin; --J) {
+    if (J - 1 > jmin) {
+      const double* tp = a.tiles + tile_off(J - 1, I);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) tn[k] = __ldg(tp + (16 * q + k) * kTB + j);
+    }
+    const double xj = poll_value(a.xb + (size_t)J * kTB + j, a.status);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = fma(t[k], xj, acc[k]);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t[k] = tn[k];
+  }
+  // reduce over j: 32-lane shuffle tree per partial, then the two warps of
+  // each column quarter meet in shared memory
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    acc[k] = v;
+  }
+  if ((j & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sm.sR[(j >> 5) * kTB + 16 * q + k] = acc[k];
+  }
+  __syncthreads();
+  // y_I is the forward result: final (polled, the forward chain wrote it)
+  if (tid < kTB)
+    sm.rr[tid] = poll_value(a.yf + (size_t)I * kTB + tid, a.status) - (sm.sR[tid] + sm.sR[kTB + tid]);
+  __syncthreads();
+  {
+    const int ii = tid & 63, part = tid >> 6;
+    double s = 0.0;
+    // (Dinv^T)[ii][jj] = Dinv[jj][ii] = sD[ii * kPad + jj]
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s = fma(sm.sD[ii * kPad + 16 * part + k], sm.rr[16 * part + k], s);
+    sm.red[part][ii] = s;
+  }
+  __syncthreads();
+  if (tid < kTB)
+    a.cb[(size_t)I * kTB + tid] = (sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const SweepArgs a) {
+  __shared__ union {
+    ChainSmem chain;
+    WorkerSmem worker;
+  } sm;
+  if (blockIdx.x == 0) {
+    chain_forward(a, sm.chain);
+    chain_transposed(a, sm.chain);
+    return;
+  }
+  const int W = gridDim.x - 1, w = blockIdx.x - 1;
+  for (int I = w; I < a.nb; I += W) worker_forward_row(a, sm.worker, I);
+  for (int I = a.nb - 1 - w; I >= 0; I -= W) worker_transposed_row(a, sm.worker, I);
 }
 
 // tile (I, J) for tile index t = I (I+1)/2 + J
@@ -437,20 +415,16 @@ cudaError_t trsv_alloc(TriFactor& t, int n) {
   t.nb = (n + kTB - 1) / kTB;
   const size_t ntiles = (size_t)t.nb * (t.nb + 1) / 2;
   const size_t chain = (size_t)t.nb * kLook * kTile;
-  t.bytes = (ntiles + t.nb + 2 * chain / kTile) * kTile * sizeof(double);
+  const size_t vec = (size_t)t.nb * kTB;
+  t.bytes = (ntiles + t.nb + 2 * chain / kTile) * kTile * sizeof(double) + 5 * vec * sizeof(double);
   cudaError_t e;
   if ((e = cudaMalloc(&t.tiles, ntiles * kTile * sizeof(double))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.dinv, (size_t)t.nb * kTile * sizeof(double))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.mf, chain * sizeof(double))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.mb, chain * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.cbuf, (size_t)t.nb * kTB * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.cflag, 2 * (size_t)t.nb * sizeof(unsigned))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.prog, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.work, 4 * vec * sizeof(double))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.status, sizeof(int))) != cudaSuccess) return e;
-  cudaMemset(t.cflag, 0, 2 * (size_t)t.nb * sizeof(unsigned));
-  cudaMemset(t.prog, 0, 2 * sizeof(unsigned long long));
   cudaMemset(t.status, 0, sizeof(int));
-  t.epoch = 0;
   return cudaSuccess;
 }
 
@@ -459,9 +433,7 @@ void trsv_free(TriFactor& t) {
   cudaFree(t.dinv);
   cudaFree(t.mf);
   cudaFree(t.mb);
-  cudaFree(t.cbuf);
-  cudaFree(t.cflag);
-  cudaFree(t.prog);
+  cudaFree(t.work);
   cudaFree(t.status);
   t = TriFactor();
 }
@@ -499,29 +471,37 @@ cudaError_t trsv_prepare(TriFactor& t, cudaStream_t st) {
   return cudaSuccess;
 }
 
-cudaError_t trsv_solve(TriFactor& t, double* y, cudaStream_t st) {
+double* trsv_result(TriFactor& t) { return t.work + (size_t)t.nb * kTB; }
+
+cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
   if (g_coop_grid < 0) {
-    int dev = 0, sms = 0, per = 0, per2 = 0;
+    int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_fwd_kernel, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, trsv_bwd_kernel, kThreads, 0);
-    g_coop_grid = sms * (per < per2 ? per : per2);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, 0);
+    g_coop_grid = sms * per;
     if (g_coop_grid < 2) g_coop_grid = 2;
   }
   // one chain CTA + up to one worker per block row
   const int grid = t.nb + 1 < g_coop_grid ? t.nb + 1 : g_coop_grid;
-  ++t.epoch;
-  unsigned long long* prog_f = t.prog;
-  unsigned long long* prog_b = t.prog + 1;
-  void* args_f[] = {(void*)&t.tiles, (void*)&t.dinv, (void*)&t.mf, (void*)&y, (void*)&t.cbuf,
-                    (void*)&t.cflag, (void*)&prog_f, (void*)&t.epoch, (void*)&t.nb, (void*)&t.status};
-  cudaError_t e =
-      cudaLaunchCooperativeKernel((const void*)trsv_fwd_kernel, grid, kThreads, args_f, 0, st);
+  const size_t vec = (size_t)t.nb * kTB;
+  // hand-off buffers [yf | xb | cf | cb] <- sentinel (all-ones bytes)
+  cudaError_t e = cudaMemsetAsync(t.work, 0xFF, 4 * vec * sizeof(double), st);
   if (e != cudaSuccess) return e;
-  void* args_b[] = {(void*)&t.tiles, (void*)&t.dinv, (void*)&t.mb, (void*)&y, (void*)&t.cbuf,
-                    (void*)&t.cflag, (void*)&prog_b, (void*)&t.epoch, (void*)&t.nb, (void*)&t.status};
-  return cudaLaunchCooperativeKernel((const void*)trsv_bwd_kernel, grid, kThreads, args_b, 0, st);
+  SweepArgs a;
+  a.tiles = t.tiles;
+  a.dinv = t.dinv;
+  a.mf = t.mf;
+  a.mb = t.mb;
+  a.b = b;
+  a.yf = t.work;
+  a.xb = t.work + vec;
+  a.cf = t.work + 2 * vec;
+  a.cb = t.work + 3 * vec;
+  a.nb = t.nb;
+  a.status = t.status;
+  void* args[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((const void*)trsv_kernel, grid, kThreads, args, 0, st);
 }
 
 }  // namespace ltb

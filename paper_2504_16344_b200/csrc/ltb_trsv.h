@@ -24,11 +24,8 @@ struct TriFactor {
   double* dinv = nullptr;
   double* mf = nullptr;
   double* mb = nullptr;
-  double* cbuf = nullptr;     // nb * 64 worker results c_I
-  unsigned* cflag = nullptr;  // 2 * nb epoch flags (forward, transposed)
-  unsigned long long* prog = nullptr;  // 2 progress words
-  int* status = nullptr;      // device error word (spin timeout / bad pivot)
-  unsigned epoch = 0;
+  double* work = nullptr;  // 4 * nb * 64 hand-off buffers [yf | x | cf | cb]
+  int* status = nullptr;   // device error word (spin timeout / bad pivot)
   size_t bytes = 0;
 };
 
@@ -41,9 +38,10 @@ cudaError_t trsv_pack_generated(TriFactor& t, uint64_t seed, cudaStream_t st);
 // invert the diagonal tiles and build the chain tiles; returns
 // cudaErrorInvalidValue on a zero / non-finite pivot
 cudaError_t trsv_prepare(TriFactor& t, cudaStream_t st);
-// y <- L^{-T} L^{-1} y (device vector of length nb * 64, zero padded).
-// Launches 2 cooperative kernels; a dependency-wait timeout is reported
-// through t.status.
-cudaError_t trsv_solve(TriFactor& t, double* y, cudaStream_t st);
+// x = L^{-T} L^{-1} b for a device vector b of length nb * 64 (zero padded);
+// the result is left in trsv_result(t).  One memset + one cooperative
+// launch; a dependency-wait timeout is reported through t.status.
+cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st);
+double* trsv_result(TriFactor& t);
 
 }  // namespace ltb
