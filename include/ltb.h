@@ -179,6 +179,13 @@ ltb_status ltb_engine_infer_map(const ltb_engine* e, ltb_scratch* s, const doubl
 ltb_status ltb_engine_forecast(const ltb_engine* e, ltb_scratch* s, const double* m,
                                double* q, int ptr_kind);
 
+/* diagnostics: enable != 0 makes the TRSV sweeps record globaltimer stamps
+ * (forward chain steps, transposed chain steps, forward worker hand-offs,
+ * transposed worker hand-offs: 4 nb values, then the launch start); with
+ * host_out the last record (up to n values) is copied out.  enable = 0
+ * stops recording. */
+ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned long long* host_out, int n);
+
 /* infer_map + forecast in one call: m_map and q (either nullable) */
 ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e, ltb_scratch* s,
                                          const double* d, double* m_map, double* q,

@@ -46,6 +46,7 @@ SIGNATURES = {
     "ltb_engine_solve_k": ([_vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_engine_infer_map": ([_vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
     "ltb_engine_forecast": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_engine_trsv_trace": ([_vp, C.c_int, C.POINTER(C.c_ulonglong), C.c_int], C.c_int),
     "ltb_engine_infer_and_forecast": ([_vp, _vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
 }
 

@@ -4,6 +4,7 @@
 // plan.  infer_map's timed region (:311-320) = copy d -> TRSV pair -> G*
 // adjoint apply; the forecast is F_q m (acceptance_main.cpp:243-264).
 #include <cstdarg>
+#include <algorithm>
 #include <cstdio>
 #include <string>
 
@@ -331,3 +332,26 @@ ltb_status ltb_engine_forecast(const ltb_engine* e_, ltb_scratch* s, const doubl
 }
 
 }  // extern "C"
+
+// ---- diagnostics: per-step timestamps of the TRSV sweeps ----
+extern "C" ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned long long* host_out,
+                                            int n) {
+  if (!e) return efail(LTB_INVALID, "trsv_trace: null engine");
+  Guard gd(e->device);
+  if (!e->factorized) return efail(LTB_STATE, "trsv_trace: no factor");
+  const size_t need = 4 * (size_t)e->factor.nb + 1;
+  if (enable && !e->factor.trace) {
+    ENG_CUDA(cudaMalloc(&e->factor.trace, need * sizeof(unsigned long long)));
+    ENG_CUDA(cudaMemset(e->factor.trace, 0, need * sizeof(unsigned long long)));
+  }
+  if (host_out && e->factor.trace) {
+    ENG_CUDA(cudaDeviceSynchronize());
+    ENG_CUDA(cudaMemcpy(host_out, e->factor.trace,
+                        std::min(need, (size_t)n) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
+  if (!enable && e->factor.trace) {
+    cudaFree(e->factor.trace);
+    e->factor.trace = nullptr;
+  }
+  return LTB_OK;
+}

@@ -1,6 +1,12 @@
 // ltb_fft.cu -- batched pad + r2c (K1, and K7 plan build) and c2r +
-// truncate + scale (K4, with the GEMV-N partial reduction fused into its
-// load) for sm_100a.  See ltb_fft.cuh for the algorithm.
+// truncate + scale (K4) for sm_100a.  See ltb_fft.cuh for the algorithm.
+//
+// Shared memory per CTA: two padded ping-pong buffers of B sequences
+// (B*NP complex each, NP = padded_len(2 Nt)); the c2r kernel also stages the
+// 2B half spectra (unpadded, 2B*Nf) in the second buffer before building
+// the Hermitian sequences.
+#include <algorithm>
+
 #include "ltb_gen.cuh"
 #include "ltb_kernels.h"
 
@@ -11,6 +17,7 @@ namespace {
 constexpr int kFftThreads = 256;
 constexpr size_t kFftSmemBudget = 56 * 1024;  // >= 4 CTAs per SM
 constexpr size_t kFftSmemMax = 227 * 1024;
+constexpr long long kFftTargetCtas = 8 * 148;  // shrink tiles for few rows
 
 LTB_DEV long long in_row_of(const RfftSrc& s, long long g) {
   return (g % s.P) * s.Q + g / s.P + s.c0;
@@ -19,18 +26,19 @@ LTB_DEV long long in_row_of(const RfftSrc& s, long long g) {
 __global__ void __launch_bounds__(kFftThreads)
     rfft_rows_kernel(const FftDesc d, const RfftSrc src, int nt, long long nrows, double2* out,
                      long long ld, int B) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int N = d.n;
+  const int NP = padded_len(N);
   double2* b0 = smem;
-  double2* b1 = smem + (size_t)B * N;
+  double2* b1 = smem + (size_t)B * NP;
   const long long g0 = (long long)blockIdx.x * 2 * B;
+  const long long rows_here = min((long long)2 * B, nrows - g0);
 
   if (src.bulk) {
     // contiguous input rows g0 .. g0+2B-1: ONE bulk async copy (TMA 1-D) into
     // the ping-pong buffer, then pair them up from shared memory
     __shared__ uint64_t bar;
     double* stage = reinterpret_cast<double*>(b1);
-    const long long rows_here = min((long long)2 * B, nrows - g0);
     const long long nvals = rows_here * nt;
     const unsigned bulk_bytes = (unsigned)((nvals * 8) & ~15ll);
     const double* gsrc = src.in + g0 * nt;  // 16-byte aligned: g0 even, base checked by host
@@ -50,38 +58,40 @@ __global__ void __launch_bounds__(kFftThreads)
         if (2 * s < rows_here) va = stage[(size_t)(2 * s) * nt + n];
         if (2 * s + 1 < rows_here) vb = stage[(size_t)(2 * s + 1) * nt + n];
       }
-      b0[idx] = make_double2(va, vb);
+      b0[(size_t)s * NP + pidx(n)] = make_double2(va, vb);
     }
-  } else
-  // load pairs (rows g0+2s, g0+2s+1) as z = a + i b, zero padded past nt
-  for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
-    const int s = idx / N, n = idx - s * N;
-    double va = 0.0, vb = 0.0;
-    if (n < nt) {
-      const long long ga = g0 + 2 * s, gb = ga + 1;
-      if (src.in) {
-        if (ga < nrows) va = __ldg(src.in + in_row_of(src, ga) * nt + n);
-        if (gb < nrows) vb = __ldg(src.in + in_row_of(src, gb) * nt + n);
-      } else {
-        if (ga < nrows) va = gen_uniform_keyed(src.gen_key, (uint64_t)(in_row_of(src, ga) * nt + n));
-        if (gb < nrows) vb = gen_uniform_keyed(src.gen_key, (uint64_t)(in_row_of(src, gb) * nt + n));
+  } else {
+    // strided rows (plan build from a host kernel) or generated values
+    for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
+      const int s = idx / N, n = idx - s * N;
+      double va = 0.0, vb = 0.0;
+      if (n < nt) {
+        const long long ga = g0 + 2 * s, gb = ga + 1;
+        if (src.in) {
+          if (ga < nrows) va = __ldg(src.in + in_row_of(src, ga) * nt + n);
+          if (gb < nrows) vb = __ldg(src.in + in_row_of(src, gb) * nt + n);
+        } else {
+          if (ga < nrows) va = gen_uniform_keyed(src.gen_key, (uint64_t)(in_row_of(src, ga) * nt + n));
+          if (gb < nrows) vb = gen_uniform_keyed(src.gen_key, (uint64_t)(in_row_of(src, gb) * nt + n));
+        }
       }
+      b0[(size_t)s * NP + pidx(n)] = make_double2(va, vb);
     }
-    b0[idx] = make_double2(va, vb);
   }
   __syncthreads();
   const double2* Y = fft_batched(d, b0, b1, B);
 
-  // unpack: A[k] = (Z[k] + conj Z[N-k]) / 2, B[k] = -i (Z[k] - conj Z[N-k]) / 2
+  // unpack: A[k] = (Z[k] + conj Z[N-k]) / 2, B[k] = -i (Z[k] - conj Z[N-k]) / 2,
+  // written transposed: out[k * ld + g]
   const int nf = nt + 1;
   const int tile = 2 * B;
   for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
     const int k = idx / tile, j = idx - k * tile;
     const long long g = g0 + j;
     if (g >= nrows) continue;
-    const int s = j >> 1;
-    const double2 zk = Y[(size_t)s * N + k];
-    const double2 zn = Y[(size_t)s * N + (k == 0 ? 0 : N - k)];
+    const double2* ys = Y + (size_t)(j >> 1) * NP;
+    const double2 zk = ys[pidx(k)];
+    const double2 zn = ys[pidx(k == 0 ? 0 : N - k)];
     double2 v;
     if ((j & 1) == 0) {
       v = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
@@ -98,16 +108,17 @@ __global__ void __launch_bounds__(kFftThreads)
     irfft_rows_kernel(const FftDesc d, const double2* __restrict__ in, long long ld_f,
                       long long ld_p, int nparts, int nt, long long nrows, double scale,
                       double* __restrict__ out, int B) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int N = d.n;
+  const int NP = padded_len(N);
   const int nf = nt + 1;
   const int tile = 2 * B;
   double2* b0 = smem;
-  double2* b1 = smem + (size_t)B * N;  // also the staging area (2B * nf <= B N + 2B)
+  double2* b1 = smem + (size_t)B * NP;  // also the staging area (2B * nf)
   const long long g0 = (long long)blockIdx.x * tile;
 
-  // gather the half spectra of the 2B rows (summing the GEMV-N partial slabs
-  // in a fixed order), FFTW c2r semantics: Im of DC / Nyquist ignored
+  // gather the half spectra of the 2B rows (summing partial slabs in a fixed
+  // order when nparts > 1); FFTW c2r semantics: Im of DC / Nyquist ignored
 #pragma unroll 8
   for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
     const int k = idx / tile, j = idx - k * tile;
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(kFftThreads)
       b = conjg(b1[(size_t)(2 * s + 1) * nf + (N - k)]);
     }
     // Z = (a.x - b.y) + i (a.y + b.x); store conj(Z)
-    b0[idx] = make_double2(a.x - b.y, -(a.y + b.x));
+    b0[(size_t)s * NP + pidx(k)] = make_double2(a.x - b.y, -(a.y + b.x));
   }
   __syncthreads();
   // ifft(Z) = conj(fft(conj Z)): a = Re Y, b = -Im Y
@@ -143,29 +154,27 @@ __global__ void __launch_bounds__(kFftThreads)
     const int j = idx / nt, n = idx - j * nt;
     const long long g = g0 + j;
     if (g >= nrows) continue;
-    const double2 y = Y[(size_t)(j >> 1) * N + n];
+    const double2 y = Y[(size_t)(j >> 1) * NP + pidx(n)];
     const double v = (j & 1) ? -y.y : y.x;
     out[g * nt + n] = v * scale;
   }
 }
 
-int pairs_for(int n) {
-  const size_t per = (size_t)(2 * n + 2) * sizeof(double2);
-  int b = (int)(kFftSmemBudget / per);
-  if (b < 1) b = 1;
-  if (b > 16) b = 16;
-  return b;
+size_t smem_for(int n, int B) {
+  const size_t np = (size_t)padded_len(n);
+  const size_t stage = std::max(np * B, (size_t)2 * B * (n / 2 + 1));
+  return (np * B + stage) * sizeof(double2);
 }
 
-}  // namespace
-
-size_t fft_smem_bytes(int n, int* pairs_per_cta) {
-  const int b = pairs_for(n);
-  if (pairs_per_cta) *pairs_per_cta = b;
-  return (size_t)(2 * b * n + 2 * b) * sizeof(double2);
+int pairs_for(int n, long long nrows) {
+  int b = 16;
+  while (b > 1 && smem_for(n, b) > kFftSmemBudget) --b;
+  // few rows: smaller tiles so the grid still covers the machine
+  const long long want = (nrows + 2 * kFftTargetCtas - 1) / (2 * kFftTargetCtas);
+  return (int)std::max(1ll, std::min((long long)b, want));
 }
 
-static cudaError_t prep_smem(const void* fn, size_t smem) {
+cudaError_t prep_smem(const void* fn, size_t smem) {
   if (smem > kFftSmemMax) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -173,11 +182,19 @@ static cudaError_t prep_smem(const void* fn, size_t smem) {
   return cudaSuccess;
 }
 
+}  // namespace
+
+size_t fft_smem_bytes(int n, int* pairs_per_cta) {
+  const int b = pairs_for(n, 1ll << 40);
+  if (pairs_per_cta) *pairs_per_cta = b;
+  return smem_for(n, b);
+}
+
 cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long long nrows,
                              double2* out, long long ld, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
-  int B;
-  const size_t smem = fft_smem_bytes(d.n, &B);
+  const int B = pairs_for(d.n, nrows);
+  const size_t smem = smem_for(d.n, B);
   cudaError_t e = prep_smem((const void*)rfft_rows_kernel, smem);
   if (e != cudaSuccess) return e;
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
@@ -191,8 +208,8 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
                               long long ld_p, int nparts, int nt, long long nrows,
                               double scale, double* out, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
-  int B;
-  const size_t smem = fft_smem_bytes(d.n, &B);
+  const int B = pairs_for(d.n, nrows);
+  const size_t smem = smem_for(d.n, B);
   cudaError_t e = prep_smem((const void*)irfft_rows_kernel, smem);
   if (e != cudaSuccess) return e;
   const long long grid = (nrows + 2 * B - 1) / (2 * B);

@@ -22,6 +22,12 @@ namespace ltb {
 
 constexpr int kMaxStages = 32;
 
+// Shared-memory sequences are padded by one complex per 8 so the stride-R
+// scatter of the first Stockham stage (and the strided unpack) hits distinct
+// 16-byte bank groups within each quarter-warp phase.
+__host__ __device__ __forceinline__ int pidx(int x) { return x + (x >> 3); }
+__host__ __device__ __forceinline__ int padded_len(int n) { return n + (n >> 3) + 1; }
+
 struct FftDesc {
   int n;        // complex transform length N = 2 N_t
   int nstages;
@@ -137,13 +143,13 @@ LTB_DEV void stockham_butterfly(const double2* __restrict__ src, double2* __rest
   const int tstep = j * (N / (Ns * R));
   double2 v[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = src[i + r * T];
+  for (int r = 0; r < R; ++r) v[r] = src[pidx(i + r * T)];
 #pragma unroll
   for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * tstep));
   dft_small<R>(v);
   const int o = (i / Ns) * Ns * R + j;
 #pragma unroll
-  for (int r = 0; r < R; ++r) dst[o + r * Ns] = v[r];
+  for (int r = 0; r < R; ++r) dst[pidx(o + r * Ns)] = v[r];
 }
 
 // any radix (rare lengths): O(R^2) straight from shared memory
@@ -158,19 +164,21 @@ LTB_DEV void stockham_butterfly_generic(const double2* __restrict__ src, double2
   for (int q = 0; q < R; ++q) {
     double2 acc = make_double2(0.0, 0.0);
     for (int r = 0; r < R; ++r) {
-      double2 x = src[i + r * T];
+      double2 x = src[pidx(i + r * T)];
       if (r) x = cmul(x, __ldg(tw + r * tstep));
       cmac(acc, x, __ldg(tw + ((r * q) % R) * rstep));
     }
-    dst[o + q * Ns] = acc;
+    dst[pidx(o + q * Ns)] = acc;
   }
 }
 
-// Batched forward FFT of `nseq` sequences laid out back to back (stride N)
-// in `a`; `b` is the ping-pong buffer.  Returns the buffer holding the
-// result.  Must be called by all threads of the CTA.
+// Batched forward FFT of `nseq` sequences laid out back to back (stride
+// padded_len(N), element n at pidx(n)) in `a`; `b` is the ping-pong buffer.
+// Returns the buffer holding the result.  Must be called by all threads of
+// the CTA.
 LTB_DEV double2* fft_batched(const FftDesc& d, double2* a, double2* b, int nseq) {
   const int N = d.n;
+  const int NP = padded_len(N);
   int Ns = 1;
   for (int s = 0; s < d.nstages; ++s) {
     const int R = d.radix[s];
@@ -178,8 +186,8 @@ LTB_DEV double2* fft_batched(const FftDesc& d, double2* a, double2* b, int nseq)
     const int total = nseq * T;
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
       const int q = idx / T, i = idx - q * T;
-      const double2* src = a + (size_t)q * N;
-      double2* dst = b + (size_t)q * N;
+      const double2* src = a + (size_t)q * NP;
+      double2* dst = b + (size_t)q * NP;
       switch (R) {
         case 8: stockham_butterfly<8>(src, dst, d.tw, N, Ns, i); break;
         case 4: stockham_butterfly<4>(src, dst, d.tw, N, Ns, i); break;

@@ -84,6 +84,7 @@ struct SweepArgs {
   double* cb;       // transposed worker hand-offs (sentinel on entry)
   int nb;
   int* status;
+  unsigned long long* trace;  // optional: per-step timestamps (ltb_trsv_trace)
 };
 
 struct ChainSmem {
@@ -98,119 +99,137 @@ struct WorkerSmem {
   double sR[2 * kTB];
 };
 
+// The chain tiles of step I are loaded into registers one step ahead.  The
+// two register sets alternate (manual 2x unroll) so a prefetch is first
+// consumed one full step after it was issued -- its HBM latency overlaps
+// the poll of the previous step instead of stalling a register copy.
+LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double (&m)[kLook][16]) {
+  const int i = threadIdx.x & 63, q = threadIdx.x >> 6;
+#pragma unroll
+  for (int k = 0; k < kLook; ++k) {
+    if (k < nvalid) {
+      const double* M = mtiles + ((size_t)step * kLook + k) * kTile;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) m[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
+    }
+  }
+}
+
+// one chain step: out_I = c_I - sum_{k < nvalid} M_{I,k} ring[slot_k]
+template <bool kForward>
+LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
+                        const double (&m)[kLook][16]) {
+  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  double p = 0.0;
+#pragma unroll
+  for (int k = 0; k < kLook; ++k) {
+    if (k < nvalid) {
+      const int src = kForward ? I - k - 1 : I + k + 1;
+      const double* v = sm.ring[src % kLook] + 16 * q;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) p = fma(m[k][kk], v[kk], p);
+    }
+  }
+  sm.red[q][i] = p;
+  __syncthreads();
+  if (tid < kTB) {
+    const double* cbuf = kForward ? a.cf : a.cb;
+    const double c = poll_value(cbuf + (size_t)I * kTB + tid, a.status);
+    const double v = c - ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
+    (kForward ? a.yf : a.xb)[(size_t)I * kTB + tid] = v;
+    sm.ring[I % kLook][tid] = v;
+  }
+  __syncthreads();
+  if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : a.nb) + I] = globaltimer();
+}
+
 // ---------------- chain, forward: y_I = c_I - sum_k M_{I,k} y_{I-k} ----------
 LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
-  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
-  double mreg[kLook][16], mnext[kLook][16];
-  for (int I = 0; I < a.nb; ++I) {
-    if (I + 1 < a.nb) {  // prefetch next step's chain tiles
-#pragma unroll
-      for (int k = 0; k < kLook; ++k) {
-        if (k + 1 <= I + 1) {
-          const double* M = a.mf + ((size_t)(I + 1) * kLook + k) * kTile;
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) mnext[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
-        }
-      }
+  double mA[kLook][16], mB[kLook][16];
+  auto nvalid = [&](int I) { return I < kLook ? I : kLook; };
+  for (int I = 0; I < a.nb; I += 2) {
+    if (I + 1 < a.nb) load_chain_tiles(a.mf, I + 1, nvalid(I + 1), mB);
+    chain_step<true>(a, sm, I, nvalid(I), mA);
+    if (I + 1 < a.nb) {
+      if (I + 2 < a.nb) load_chain_tiles(a.mf, I + 2, nvalid(I + 2), mA);
+      chain_step<true>(a, sm, I + 1, nvalid(I + 1), mB);
     }
-    double p = 0.0;
-#pragma unroll
-    for (int k = 0; k < kLook; ++k) {
-      if (k + 1 <= I) {
-        const double* yv = sm.ring[(I - k - 1) % kLook] + 16 * q;
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) p = fma(mreg[k][kk], yv[kk], p);
-      }
-    }
-    sm.red[q][i] = p;
-    __syncthreads();
-    if (tid < kTB) {
-      const double c = poll_value(a.cf + (size_t)I * kTB + tid, a.status);
-      const double v = c - ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
-      a.yf[(size_t)I * kTB + tid] = v;
-      sm.ring[I % kLook][tid] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kLook; ++k)
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) mreg[k][kk] = mnext[k][kk];
   }
 }
 
 // ---------------- chain, transposed: x_I = c_I - sum_k M'_{I,k} x_{I+k} ------
 LTB_DEV void chain_transposed(const SweepArgs& a, ChainSmem& sm) {
-  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
-  double mreg[kLook][16], mnext[kLook][16];
-  for (int I = a.nb - 1; I >= 0; --I) {
+  double mA[kLook][16], mB[kLook][16];
+  const int nb = a.nb;
+  auto nvalid = [&](int I) { return nb - 1 - I < kLook ? nb - 1 - I : kLook; };
+  for (int I = nb - 1; I >= 0; I -= 2) {
+    if (I - 1 >= 0) load_chain_tiles(a.mb, I - 1, nvalid(I - 1), mB);
+    chain_step<false>(a, sm, I, nvalid(I), mA);
     if (I - 1 >= 0) {
-#pragma unroll
-      for (int k = 0; k < kLook; ++k) {
-        if (I + k < a.nb) {  // tile (I-1, k): block row I+k exists
-          const double* M = a.mb + ((size_t)(I - 1) * kLook + k) * kTile;
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) mnext[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
-        }
-      }
+      if (I - 2 >= 0) load_chain_tiles(a.mb, I - 2, nvalid(I - 2), mA);
+      chain_step<false>(a, sm, I - 1, nvalid(I - 1), mB);
     }
-    double p = 0.0;
-#pragma unroll
-    for (int k = 0; k < kLook; ++k) {
-      if (I + k + 1 < a.nb) {
-        const double* xv = sm.ring[(I + k + 1) % kLook] + 16 * q;
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) p = fma(mreg[k][kk], xv[kk], p);
-      }
-    }
-    sm.red[q][i] = p;
-    __syncthreads();
-    if (tid < kTB) {
-      const double c = poll_value(a.cb + (size_t)I * kTB + tid, a.status);
-      const double v = c - ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
-      a.xb[(size_t)I * kTB + tid] = v;
-      sm.ring[I % kLook][tid] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kLook; ++k)
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) mreg[k][kk] = mnext[k][kk];
   }
 }
 
-// ---------------- worker, forward row I ---------------------------------------
-// thread (i = tid & 63, q = tid >> 6) owns row i, columns [16q, 16q+16)
-LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, int I) {
+// ---------------- workers: TMA tile ring ------------------------------------
+// Panel tiles stream through a kRing-deep ring of 32 KB shared-memory stages
+// filled by 1-D bulk async copies (one elected thread, one mbarrier per
+// stage), so a worker keeps ~96 KB of the factor in flight without holding
+// it in registers.  A running tile counter carries the stage / phase across
+// rows and sweeps.
+constexpr int kRing = 4;
+
+struct TileRing {
+  double* stage;  // kRing * kTile doubles (dynamic shared memory)
+  uint64_t* full; // kRing mbarriers
+  unsigned next;  // tiles consumed so far by this CTA
+};
+
+LTB_DEV void ring_issue(TileRing& r, unsigned g, const double* src, uint64_t policy) {
+  const int s = g % kRing;
+  mbar_arrive_expect_tx(r.full + s, kTile * sizeof(double));
+  bulk_g2s(r.stage + (size_t)s * kTile, src, kTile * sizeof(double), r.full + s, policy);
+}
+
+// forward row I: thread (i = tid & 63, q = tid >> 6) owns row i, columns
+// [16q, 16q+16) of each tile L_IJ, J < I - kLook (contiguous in memory)
+LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ring, int I,
+                                uint64_t policy) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
-  const double* D = a.dinv + (size_t)I * kTile;
-  for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
   const int jmax = I - kLook;  // panel tiles J < jmax; the chain does the rest
   const double* row = a.tiles + tile_off(I, 0);
-  double t[16], tn[16];
+  const unsigned g0 = ring.next;
+  if (tid == 0)
+    for (int J = 0; J < jmax && J < kRing; ++J) ring_issue(ring, g0 + J, row + (size_t)J * kTile, policy);
+  const double* D = a.dinv + (size_t)I * kTile;
+  for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
   double acc = 0.0;
+  unsigned long long yraw[16];
   if (jmax > 0) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) t[k] = __ldg(row + (16 * q + k) * kTB + i);
+    for (int k = 0; k < 16; ++k) yraw[k] = ld_relaxed_u64(a.yf + 16 * q + k);
   }
   for (int J = 0; J < jmax; ++J) {
+    // resolve this tile's solution block (prefetched one tile ago)
+    double yv[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      yv[k] = yraw[k] != kSentinel ? __longlong_as_double((long long)yraw[k])
+                                   : poll_value(a.yf + (size_t)J * kTB + 16 * q + k, a.status);
     if (J + 1 < jmax) {
-      const double* nt = row + (size_t)(J + 1) * kTile;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) tn[k] = __ldg(nt + (16 * q + k) * kTB + i);
+      for (int k = 0; k < 16; ++k) yraw[k] = ld_relaxed_u64(a.yf + (size_t)(J + 1) * kTB + 16 * q + k);
     }
-    const double* yJ = a.yf + (size_t)J * kTB + 16 * q;
-    unsigned long long raw[16];
+    const unsigned g = g0 + J;
+    mbar_wait(ring.full + g % kRing, (g / kRing) & 1);
+    const double* T = ring.stage + (size_t)(g % kRing) * kTile;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) raw[k] = ld_relaxed_u64(yJ + k);  // 16 loads in flight
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const double yv = raw[k] != kSentinel ? __longlong_as_double((long long)raw[k])
-                                            : poll_value(yJ + k, a.status);
-      acc = fma(t[k], yv, acc);
-    }
-#pragma unroll
-    for (int k = 0; k < 16; ++k) t[k] = tn[k];
+    for (int k = 0; k < 16; ++k) acc = fma(T[(16 * q + k) * kTB + i], yv[k], acc);
+    __syncthreads();  // stage consumed
+    if (tid == 0 && J + kRing < jmax) ring_issue(ring, g + kRing, row + (size_t)(J + kRing) * kTile, policy);
   }
+  ring.next = g0 + (jmax > 0 ? jmax : 0);
   sm.red[q][i] = acc;
   __syncthreads();
   if (tid < kTB)
@@ -225,38 +244,41 @@ LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, int I) {
   if (tid < kTB)
     a.cf[(size_t)I * kTB + tid] = (sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]);
   __syncthreads();
+  if (a.trace && tid == 0) a.trace[2 * a.nb + I] = globaltimer();
 }
 
-// ---------------- worker, transposed row I ------------------------------------
-// thread (j = tid & 63, q = tid >> 6) reads row j of tile L_JI, columns
-// [16q, 16q+16), keeping 16 partial sums of (L_JI^T x_J)
-LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, int I) {
+// transposed row I: thread (j = tid & 63, q = tid >> 6) reads row j of tile
+// L_JI (J descending, J > I + kLook), columns [16q, 16q+16), keeping 16
+// partial sums of (L_JI^T x_J)
+LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ring, int I,
+                                   uint64_t policy) {
   const int tid = threadIdx.x, j = tid & 63, q = tid >> 6;
   const int nb = a.nb;
+  const int jmin = I + kLook;  // panel tiles J > jmin; the chain does the rest
+  const int ntile = nb - 1 - jmin > 0 ? nb - 1 - jmin : 0;
+  const unsigned g0 = ring.next;
+  if (tid == 0)
+    for (int t = 0; t < ntile && t < kRing; ++t) ring_issue(ring, g0 + t, a.tiles + tile_off(nb - 1 - t, I), policy);
   const double* D = a.dinv + (size_t)I * kTile;
   for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
   double acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-  const int jmin = I + kLook;  // panel tiles J > jmin; the chain does the rest
-  double t[16], tn[16];
-  if (nb - 1 > jmin) {
-    const double* tp = a.tiles + tile_off(nb - 1, I);
+  unsigned long long xraw = ntile > 0 ? ld_relaxed_u64(a.xb + (size_t)(nb - 1) * kTB + j) : 0ull;
+  for (int t = 0; t < ntile; ++t) {
+    const int J = nb - 1 - t;
+    const double xj = xraw != kSentinel ? __longlong_as_double((long long)xraw)
+                                        : poll_value(a.xb + (size_t)J * kTB + j, a.status);
+    if (t + 1 < ntile) xraw = ld_relaxed_u64(a.xb + (size_t)(J - 1) * kTB + j);
+    const unsigned g = g0 + t;
+    mbar_wait(ring.full + g % kRing, (g / kRing) & 1);
+    const double* T = ring.stage + (size_t)(g % kRing) * kTile;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) t[k] = __ldg(tp + (16 * q + k) * kTB + j);
+    for (int k = 0; k < 16; ++k) acc[k] = fma(T[(16 * q + k) * kTB + j], xj, acc[k]);
+    __syncthreads();  // stage consumed
+    if (tid == 0 && t + kRing < ntile) ring_issue(ring, g + kRing, a.tiles + tile_off(J - kRing, I), policy);
   }
-  for (int J = nb - 1; J > jmin; --J) {
-    if (J - 1 > jmin) {
-      const double* tp = a.tiles + tile_off(J - 1, I);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) tn[k] = __ldg(tp + (16 * q + k) * kTB + j);
-    }
-    const double xj = poll_value(a.xb + (size_t)J * kTB + j, a.status);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = fma(t[k], xj, acc[k]);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) t[k] = tn[k];
-  }
+  ring.next = g0 + ntile;
   // reduce over j: 32-lane shuffle tree per partial, then the two warps of
   // each column quarter meet in shared memory
 #pragma unroll
@@ -287,6 +309,7 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, int I) {
   if (tid < kTB)
     a.cb[(size_t)I * kTB + tid] = (sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]);
   __syncthreads();
+  if (a.trace && tid == 0) a.trace[3 * a.nb + I] = globaltimer();
 }
 
 __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const SweepArgs a) {
@@ -294,15 +317,30 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const SweepArgs a) {
     ChainSmem chain;
     WorkerSmem worker;
   } sm;
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[4 * a.nb] = globaltimer();
   if (blockIdx.x == 0) {
     chain_forward(a, sm.chain);
     chain_transposed(a, sm.chain);
     return;
   }
+  TileRing ring;
+  ring.stage = reinterpret_cast<double*>(ring_smem);
+  ring.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kRing * kTile * sizeof(double));
+  ring.next = 0;
+  uint64_t policy = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(ring.full + s, 1);
+    fence_mbar_init();
+    policy = policy_evict_first();
+  }
+  __syncthreads();
   const int W = gridDim.x - 1, w = blockIdx.x - 1;
-  for (int I = w; I < a.nb; I += W) worker_forward_row(a, sm.worker, I);
-  for (int I = a.nb - 1 - w; I >= 0; I -= W) worker_transposed_row(a, sm.worker, I);
+  for (int I = w; I < a.nb; I += W) worker_forward_row(a, sm.worker, ring, I, policy);
+  for (int I = a.nb - 1 - w; I >= 0; I -= W) worker_transposed_row(a, sm.worker, ring, I, policy);
 }
+
+constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
 
 // tile (I, J) for tile index t = I (I+1)/2 + J
 LTB_DEV void tile_ij(long long t, int* I, int* J) {
@@ -435,6 +473,7 @@ void trsv_free(TriFactor& t) {
   cudaFree(t.mb);
   cudaFree(t.work);
   cudaFree(t.status);
+  cudaFree(t.trace);
   t = TriFactor();
 }
 
@@ -478,7 +517,8 @@ cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, 0);
+    cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, kRingSmem);
     g_coop_grid = sms * per;
     if (g_coop_grid < 2) g_coop_grid = 2;
   }
@@ -500,8 +540,9 @@ cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
   a.cb = t.work + 3 * vec;
   a.nb = t.nb;
   a.status = t.status;
+  a.trace = t.trace;
   void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((const void*)trsv_kernel, grid, kThreads, args, 0, st);
+  return cudaLaunchCooperativeKernel((const void*)trsv_kernel, grid, kThreads, args, kRingSmem, st);
 }
 
 }  // namespace ltb

@@ -26,6 +26,7 @@ struct TriFactor {
   double* mb = nullptr;
   double* work = nullptr;  // 4 * nb * 64 hand-off buffers [yf | x | cf | cb]
   int* status = nullptr;   // device error word (spin timeout / bad pivot)
+  unsigned long long* trace = nullptr;  // diagnostic timestamps, 4 nb + 1 (optional)
   size_t bytes = 0;
 };
 

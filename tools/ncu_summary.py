@@ -1,0 +1,70 @@
+"""Summarise ncu output for profiles/ (dev tool).
+
+    python tools/ncu_summary.py report X.ncu-rep  > profiles/...md
+    python tools/ncu_summary.py launches X.csv    > profiles/...md
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of theoretical peak"),
+    ("dram__cycles_active.avg.pct_of_peak_sustained_elapsed", "DRAM cycles active %"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__block_size", "block"),
+    ("launch__grid_size", "grid"),
+    ("launch__occupancy_limit_shared_mem", "CTA limit (smem)"),
+    ("launch__occupancy_limit_registers", "CTA limit (regs)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("smsp__inst_executed.sum", "instructions"),
+]
+
+
+def report(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    out = ["| kernel | " + " | ".join(label for _, label in METRICS) + " |",
+           "|---" * (len(METRICS) + 1) + "|"]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+        name = name.replace("ltb::<unnamed>::", "").replace("ltb::", "")
+        cells = []
+        for key, _ in METRICS:
+            if key in hdr:
+                j = hdr.index(key)
+                cells.append("%s %s" % (r[j], units[j]) if units[j] else r[j])
+            else:
+                cells.append("n/a")
+        out.append("| %s | %s |" % (name, " | ".join(cells)))
+    print("\n".join(out))
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in rows[1:]:
+        name = r[ki].split("(")[0].replace("void ", "").replace("ltb::<unnamed>::", "")
+        tot[name] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        cnt[name] += 1
+    total = sum(tot.values())
+    print("| kernel | launches | total ms | mean ms | share |")
+    print("|---|---|---|---|---|")
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        print("| %s | %d | %.3f | %.4f | %.1f%% |" % (k, cnt[k], v, v / cnt[k], 100 * v / total))
+
+
+if __name__ == "__main__":
+    {"report": report, "launches": launches}[sys.argv[1]](sys.argv[2])
