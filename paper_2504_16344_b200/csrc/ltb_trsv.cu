@@ -34,7 +34,9 @@ namespace ltb {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kQ = 8;                // column groups per 64-row tile
+constexpr int kThreads = 64 * kQ;   // 512: thread (row, group)
+constexpr int kCPT = kTB / kQ;      // 8 tile columns per thread
 constexpr int kPad = 65;                               // padded smem tile stride
 constexpr int kTile = kTB * kTB;
 constexpr unsigned long long kSentinel = ~0ull;        // all-ones NaN
@@ -87,14 +89,22 @@ struct SweepArgs {
   unsigned long long* trace;  // optional: per-step timestamps (ltb_trsv_trace)
 };
 
+// fixed-order sum of the kQ column-group partials of row r
+LTB_DEV double red_sum(const double (&red)[kQ][kTB], int r) {
+  double s = 0.0;
+#pragma unroll
+  for (int g = 0; g < kQ; ++g) s += red[g][r];
+  return s;
+}
+
 struct ChainSmem {
   double ring[kLook][kTB];
-  double red[4][kTB];
+  double red[kQ][kTB];
 };
 
 struct WorkerSmem {
   double sD[kTB * kPad];
-  double red[4][kTB];
+  double red[kQ][kTB];
   double rr[kTB];
   double sR[2 * kTB];
 };
@@ -103,14 +113,14 @@ struct WorkerSmem {
 // two register sets alternate (manual 2x unroll) so a prefetch is first
 // consumed one full step after it was issued -- its HBM latency overlaps
 // the poll of the previous step instead of stalling a register copy.
-LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double (&m)[kLook][16]) {
+LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double (&m)[kLook][kCPT]) {
   const int i = threadIdx.x & 63, q = threadIdx.x >> 6;
 #pragma unroll
   for (int k = 0; k < kLook; ++k) {
     if (k < nvalid) {
       const double* M = mtiles + ((size_t)step * kLook + k) * kTile;
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) m[k][kk] = __ldg(M + (16 * q + kk) * kTB + i);
+      for (int kk = 0; kk < kCPT; ++kk) m[k][kk] = __ldg(M + (kCPT * q + kk) * kTB + i);
     }
   }
 }
@@ -118,16 +128,16 @@ LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double
 // one chain step: out_I = c_I - sum_{k < nvalid} M_{I,k} ring[slot_k]
 template <bool kForward>
 LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
-                        const double (&m)[kLook][16]) {
+                        const double (&m)[kLook][kCPT]) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
   double p = 0.0;
 #pragma unroll
   for (int k = 0; k < kLook; ++k) {
     if (k < nvalid) {
       const int src = kForward ? I - k - 1 : I + k + 1;
-      const double* v = sm.ring[src % kLook] + 16 * q;
+      const double* v = sm.ring[src % kLook] + kCPT * q;
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) p = fma(m[k][kk], v[kk], p);
+      for (int kk = 0; kk < kCPT; ++kk) p = fma(m[k][kk], v[kk], p);
     }
   }
   sm.red[q][i] = p;
@@ -135,7 +145,7 @@ LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
   if (tid < kTB) {
     const double* cbuf = kForward ? a.cf : a.cb;
     const double c = poll_value(cbuf + (size_t)I * kTB + tid, a.status);
-    const double v = c - ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
+    const double v = c - (red_sum(sm.red, tid));
     (kForward ? a.yf : a.xb)[(size_t)I * kTB + tid] = v;
     sm.ring[I % kLook][tid] = v;
   }
@@ -145,7 +155,7 @@ LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
 
 // ---------------- chain, forward: y_I = c_I - sum_k M_{I,k} y_{I-k} ----------
 LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
-  double mA[kLook][16], mB[kLook][16];
+  double mA[kLook][kCPT], mB[kLook][kCPT];
   auto nvalid = [&](int I) { return I < kLook ? I : kLook; };
   for (int I = 0; I < a.nb; I += 2) {
     if (I + 1 < a.nb) load_chain_tiles(a.mf, I + 1, nvalid(I + 1), mB);
@@ -159,7 +169,7 @@ LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
 
 // ---------------- chain, transposed: x_I = c_I - sum_k M'_{I,k} x_{I+k} ------
 LTB_DEV void chain_transposed(const SweepArgs& a, ChainSmem& sm) {
-  double mA[kLook][16], mB[kLook][16];
+  double mA[kLook][kCPT], mB[kLook][kCPT];
   const int nb = a.nb;
   auto nvalid = [&](int I) { return nb - 1 - I < kLook ? nb - 1 - I : kLook; };
   for (int I = nb - 1; I >= 0; I -= 2) {
@@ -193,7 +203,7 @@ LTB_DEV void ring_issue(TileRing& r, unsigned g, const double* src, uint64_t pol
 }
 
 // forward row I: thread (i = tid & 63, q = tid >> 6) owns row i, columns
-// [16q, 16q+16) of each tile L_IJ, J < I - kLook (contiguous in memory)
+// [8q, 8q+8) of each tile L_IJ, J < I - kLook (contiguous in memory)
 LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ring, int I,
                                 uint64_t policy) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
@@ -205,27 +215,27 @@ LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ri
   const double* D = a.dinv + (size_t)I * kTile;
   for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
   double acc = 0.0;
-  unsigned long long yraw[16];
+  unsigned long long yraw[kCPT];
   if (jmax > 0) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) yraw[k] = ld_relaxed_u64(a.yf + 16 * q + k);
+    for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(a.yf + kCPT * q + k);
   }
   for (int J = 0; J < jmax; ++J) {
     // resolve this tile's solution block (prefetched one tile ago)
-    double yv[16];
+    double yv[kCPT];
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < kCPT; ++k)
       yv[k] = yraw[k] != kSentinel ? __longlong_as_double((long long)yraw[k])
-                                   : poll_value(a.yf + (size_t)J * kTB + 16 * q + k, a.status);
+                                   : poll_value(a.yf + (size_t)J * kTB + kCPT * q + k, a.status);
     if (J + 1 < jmax) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) yraw[k] = ld_relaxed_u64(a.yf + (size_t)(J + 1) * kTB + 16 * q + k);
+      for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(a.yf + (size_t)(J + 1) * kTB + kCPT * q + k);
     }
     const unsigned g = g0 + J;
     mbar_wait(ring.full + g % kRing, (g / kRing) & 1);
     const double* T = ring.stage + (size_t)(g % kRing) * kTile;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) acc = fma(T[(16 * q + k) * kTB + i], yv[k], acc);
+    for (int k = 0; k < kCPT; ++k) acc = fma(T[(kCPT * q + k) * kTB + i], yv[k], acc);
     __syncthreads();  // stage consumed
     if (tid == 0 && J + kRing < jmax) ring_issue(ring, g + kRing, row + (size_t)(J + kRing) * kTile, policy);
   }
@@ -234,21 +244,21 @@ LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ri
   __syncthreads();
   if (tid < kTB)
     sm.rr[tid] = __ldg(a.b + (size_t)I * kTB + tid) -
-                 ((sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]));
+                 (red_sum(sm.red, tid));
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) s = fma(sm.sD[(16 * q + k) * kPad + i], sm.rr[16 * q + k], s);
+  for (int k = 0; k < kCPT; ++k) s = fma(sm.sD[(kCPT * q + k) * kPad + i], sm.rr[kCPT * q + k], s);
   sm.red[q][i] = s;
   __syncthreads();
   if (tid < kTB)
-    a.cf[(size_t)I * kTB + tid] = (sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]);
+    a.cf[(size_t)I * kTB + tid] = red_sum(sm.red, tid);
   __syncthreads();
   if (a.trace && tid == 0) a.trace[2 * a.nb + I] = globaltimer();
 }
 
 // transposed row I: thread (j = tid & 63, q = tid >> 6) reads row j of tile
-// L_JI (J descending, J > I + kLook), columns [16q, 16q+16), keeping 16
+// L_JI (J descending, J > I + kLook), columns [8q, 8q+8), keeping 8
 // partial sums of (L_JI^T x_J)
 LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ring, int I,
                                    uint64_t policy) {
@@ -261,9 +271,9 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
     for (int t = 0; t < ntile && t < kRing; ++t) ring_issue(ring, g0 + t, a.tiles + tile_off(nb - 1 - t, I), policy);
   const double* D = a.dinv + (size_t)I * kTile;
   for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
-  double acc[16];
+  double acc[kCPT];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+  for (int k = 0; k < kCPT; ++k) acc[k] = 0.0;
   unsigned long long xraw = ntile > 0 ? ld_relaxed_u64(a.xb + (size_t)(nb - 1) * kTB + j) : 0ull;
   for (int t = 0; t < ntile; ++t) {
     const int J = nb - 1 - t;
@@ -274,7 +284,7 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
     mbar_wait(ring.full + g % kRing, (g / kRing) & 1);
     const double* T = ring.stage + (size_t)(g % kRing) * kTile;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = fma(T[(16 * q + k) * kTB + j], xj, acc[k]);
+    for (int k = 0; k < kCPT; ++k) acc[k] = fma(T[(kCPT * q + k) * kTB + j], xj, acc[k]);
     __syncthreads();  // stage consumed
     if (tid == 0 && t + kRing < ntile) ring_issue(ring, g + kRing, a.tiles + tile_off(J - kRing, I), policy);
   }
@@ -282,7 +292,7 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
   // reduce over j: 32-lane shuffle tree per partial, then the two warps of
   // each column quarter meet in shared memory
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
+  for (int k = 0; k < kCPT; ++k) {
     double v = acc[k];
 #pragma unroll
     for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
@@ -290,7 +300,7 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
   }
   if ((j & 31) == 0) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) sm.sR[(j >> 5) * kTB + 16 * q + k] = acc[k];
+    for (int k = 0; k < kCPT; ++k) sm.sR[(j >> 5) * kTB + kCPT * q + k] = acc[k];
   }
   __syncthreads();
   // y_I is the forward result: final (polled, the forward chain wrote it)
@@ -302,12 +312,12 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
     double s = 0.0;
     // (Dinv^T)[ii][jj] = Dinv[jj][ii] = sD[ii * kPad + jj]
 #pragma unroll
-    for (int k = 0; k < 16; ++k) s = fma(sm.sD[ii * kPad + 16 * part + k], sm.rr[16 * part + k], s);
+    for (int k = 0; k < kCPT; ++k) s = fma(sm.sD[ii * kPad + kCPT * part + k], sm.rr[kCPT * part + k], s);
     sm.red[part][ii] = s;
   }
   __syncthreads();
   if (tid < kTB)
-    a.cb[(size_t)I * kTB + tid] = (sm.red[0][tid] + sm.red[1][tid]) + (sm.red[2][tid] + sm.red[3][tid]);
+    a.cb[(size_t)I * kTB + tid] = red_sum(sm.red, tid);
   __syncthreads();
   if (a.trace && tid == 0) a.trace[3 * a.nb + I] = globaltimer();
 }

@@ -9,7 +9,7 @@
 namespace ltb {
 
 constexpr int kTB = 64;    // factor tile edge
-constexpr int kLook = 2;   // diagonal-chain lookahead depth (tiles per chain step)
+constexpr int kLook = 3;   // diagonal-chain lookahead depth (tiles per chain step)
 
 // Lower factor packed as 64x64 tiles (I, J), J <= I, tile index
 // I (I+1)/2 + J, each tile column-major (row fastest).  The last tile row /
