@@ -128,8 +128,14 @@ LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double
 // one chain step: out_I = c_I - sum_{k < nvalid} M_{I,k} ring[slot_k]
 template <bool kForward>
 LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
-                        const double (&m)[kLook][kCPT]) {
+                        const double (&m)[kLook][kCPT], unsigned long long cur,
+                        unsigned long long& nxt) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  const double* cbuf = kForward ? a.cf : a.cb;
+  // speculative prefetch of the next step's hand-off (workers usually run
+  // ahead); a sentinel just means "poll it then"
+  const int In = kForward ? I + 1 : I - 1;
+  if (tid < kTB && In >= 0 && In < a.nb) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
   double p = 0.0;
 #pragma unroll
   for (int k = 0; k < kLook; ++k) {
@@ -143,8 +149,8 @@ LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
   sm.red[q][i] = p;
   __syncthreads();
   if (tid < kTB) {
-    const double* cbuf = kForward ? a.cf : a.cb;
-    const double c = poll_value(cbuf + (size_t)I * kTB + tid, a.status);
+    const double c = cur != kSentinel ? __longlong_as_double((long long)cur)
+                                      : poll_value(cbuf + (size_t)I * kTB + tid, a.status);
     const double v = c - (red_sum(sm.red, tid));
     (kForward ? a.yf : a.xb)[(size_t)I * kTB + tid] = v;
     sm.ring[I % kLook][tid] = v;
@@ -156,13 +162,14 @@ LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
 // ---------------- chain, forward: y_I = c_I - sum_k M_{I,k} y_{I-k} ----------
 LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
   double mA[kLook][kCPT], mB[kLook][kCPT];
+  unsigned long long cA = kSentinel, cB = kSentinel;
   auto nvalid = [&](int I) { return I < kLook ? I : kLook; };
   for (int I = 0; I < a.nb; I += 2) {
     if (I + 1 < a.nb) load_chain_tiles(a.mf, I + 1, nvalid(I + 1), mB);
-    chain_step<true>(a, sm, I, nvalid(I), mA);
+    chain_step<true>(a, sm, I, nvalid(I), mA, cA, cB);
     if (I + 1 < a.nb) {
       if (I + 2 < a.nb) load_chain_tiles(a.mf, I + 2, nvalid(I + 2), mA);
-      chain_step<true>(a, sm, I + 1, nvalid(I + 1), mB);
+      chain_step<true>(a, sm, I + 1, nvalid(I + 1), mB, cB, cA);
     }
   }
 }
@@ -172,12 +179,13 @@ LTB_DEV void chain_transposed(const SweepArgs& a, ChainSmem& sm) {
   double mA[kLook][kCPT], mB[kLook][kCPT];
   const int nb = a.nb;
   auto nvalid = [&](int I) { return nb - 1 - I < kLook ? nb - 1 - I : kLook; };
+  unsigned long long cA = kSentinel, cB = kSentinel;
   for (int I = nb - 1; I >= 0; I -= 2) {
     if (I - 1 >= 0) load_chain_tiles(a.mb, I - 1, nvalid(I - 1), mB);
-    chain_step<false>(a, sm, I, nvalid(I), mA);
+    chain_step<false>(a, sm, I, nvalid(I), mA, cA, cB);
     if (I - 1 >= 0) {
       if (I - 2 >= 0) load_chain_tiles(a.mb, I - 2, nvalid(I - 2), mA);
-      chain_step<false>(a, sm, I - 1, nvalid(I - 1), mB);
+      chain_step<false>(a, sm, I - 1, nvalid(I - 1), mB, cB, cA);
     }
   }
 }
