@@ -186,6 +186,13 @@ ltb_status ltb_engine_forecast(const ltb_engine* e, ltb_scratch* s, const double
  * stops recording. */
 ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned long long* host_out, int n);
 
+/* diagnostics: the distributed K^{-1} apply emulated on ONE GPU -- P ranks'
+ * row-cyclic shards of the synthetic factor (seed) and one cooperative
+ * launch playing all P ranks; x_host = rank 0's K^{-1} b, max_rank_diff =
+ * largest deviation of the other ranks' replicated results. */
+ltb_status ltb_debug_dtrsv_emulated(int n, int P, uint64_t seed, const double* b_host,
+                                    double* x_host, double* max_rank_diff, double* seconds);
+
 /* infer_map + forecast in one call: m_map and q (either nullable) */
 ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e, ltb_scratch* s,
                                          const double* d, double* m_map, double* q,

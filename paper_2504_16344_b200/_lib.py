@@ -47,6 +47,7 @@ SIGNATURES = {
     "ltb_engine_infer_map": ([_vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
     "ltb_engine_forecast": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_engine_trsv_trace": ([_vp, C.c_int, C.POINTER(C.c_ulonglong), C.c_int], C.c_int),
+    "ltb_debug_dtrsv_emulated": ([C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp], C.c_int),
     "ltb_engine_infer_and_forecast": ([_vp, _vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
 }
 

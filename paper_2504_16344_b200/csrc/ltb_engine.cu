@@ -5,6 +5,7 @@
 // adjoint apply; the forecast is F_q m (acceptance_main.cpp:243-264).
 #include <cstdarg>
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <string>
 
@@ -144,8 +145,7 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
   return LTB_OK;
 }
 
-ltb_status factor_finish(ltb_engine* e) {
-  cudaError_t err = trsv_prepare(e->factor, 0);
+ltb_status factor_finish(ltb_engine* e, cudaError_t err) {
   count_launches(2);
   if (err == cudaErrorInvalidValue)
     return efail(LTB_NUMERICAL, "set_factor: zero or non-finite diagonal in the Cholesky factor");
@@ -234,7 +234,7 @@ ltb_status ltb_engine_set_factor(ltb_engine* e, const double* L, int n, size_t l
   cudaFree(tmp);
   if (err != cudaSuccess) return efail(LTB_CUDA, "set_factor: pack: %s", cudaGetErrorString(err));
   count_launches(1);
-  return factor_finish(e);
+  return factor_finish(e, trsv_prepare_packed(e->factor, 0));
 }
 
 ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed) {
@@ -242,11 +242,8 @@ ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed) 
   Guard gd(e->device);
   ltb_status st = factor_prepare(e, n);
   if (st != LTB_OK) return st;
-  cudaError_t err = trsv_pack_generated(e->factor, seed, 0);
-  if (err == cudaSuccess) err = cudaDeviceSynchronize();
-  if (err != cudaSuccess) return efail(LTB_CUDA, "set_factor_generated: %s", cudaGetErrorString(err));
   count_launches(1);
-  return factor_finish(e);
+  return factor_finish(e, trsv_setup_generated(e->factor, seed, 0));
 }
 
 ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, int ptr_kind) {
@@ -354,4 +351,65 @@ extern "C" ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned 
     e->factor.trace = nullptr;
   }
   return LTB_OK;
+}
+
+// ---- diagnostics: the distributed TRSV emulated on one GPU ----
+// Builds P row-cyclic shards of the synthetic factor (seed) on the current
+// device, runs ONE cooperative launch emulating all P ranks (peer buffers on
+// the same device), and returns rank 0's x = K^{-1} b.  *max_rank_diff gets
+// the largest |x_rank - x_0| over the other ranks' replicated copies.
+extern "C" ltb_status ltb_debug_dtrsv_emulated(int n, int P, uint64_t seed, const double* b_host,
+                                               double* x_host, double* max_rank_diff,
+                                               double* seconds) {
+  if (P < 1 || P > kMaxRanks || n < 1 || !b_host || !x_host)
+    return efail(LTB_INVALID, "dtrsv_emulated: bad arguments");
+  TriFactor ts[kMaxRanks];
+  TriFactor* tp[kMaxRanks];
+  const double* bp[kMaxRanks];
+  double* b = nullptr;
+  const int nb = (n + kTB - 1) / kTB;
+  auto cleanup = [&](ltb_status s) {
+    for (int r = 0; r < P; ++r) trsv_free(ts[r]);
+    cudaFree(b);
+    return s;
+  };
+  if (cudaMalloc(&b, (size_t)nb * kTB * sizeof(double)) != cudaSuccess)
+    return cleanup(efail(LTB_CUDA, "dtrsv_emulated: alloc"));
+  cudaMemset(b, 0, (size_t)nb * kTB * sizeof(double));
+  cudaMemcpy(b, b_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice);
+  for (int r = 0; r < P; ++r) {
+    cudaError_t e = trsv_alloc(ts[r], n, P, r);
+    if (e == cudaSuccess) e = trsv_setup_generated(ts[r], seed, 0);
+    if (e != cudaSuccess) return cleanup(efail(LTB_CUDA, "dtrsv_emulated: setup: %s", cudaGetErrorString(e)));
+    tp[r] = &ts[r];
+    bp[r] = b;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, 0);
+  cudaError_t e = trsv_solve_emulated(tp, bp, P, 0);
+  cudaEventRecord(e1, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (e != cudaSuccess) return cleanup(efail(LTB_CUDA, "dtrsv_emulated: %s", cudaGetErrorString(e)));
+  int h = 0;
+  cudaMemcpy(&h, ts[0].status, sizeof(int), cudaMemcpyDeviceToHost);
+  if (h) return cleanup(efail(LTB_CUDA, "dtrsv_emulated: dependency wait timed out"));
+  cudaMemcpy(x_host, trsv_result(ts[0]), (size_t)n * sizeof(double), cudaMemcpyDeviceToHost);
+  double worst = 0.0;
+  std::string scratch;
+  double* other = new double[n];
+  for (int r = 1; r < P; ++r) {
+    cudaMemcpy(other, trsv_result(ts[r]), (size_t)n * sizeof(double), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < n; ++i) worst = std::max(worst, std::abs(other[i] - x_host[i]));
+  }
+  delete[] other;
+  if (max_rank_diff) *max_rank_diff = worst;
+  if (seconds) *seconds = ms * 1e-3;
+  count_launches(1);
+  return cleanup(LTB_OK);
 }

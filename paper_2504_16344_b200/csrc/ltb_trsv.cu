@@ -1,30 +1,41 @@
 // ltb_trsv.cu -- blocked triangular solves for K^{-1} = L^{-T} L^{-1}
-// (bayes_engine.cpp:236-240) on sm_100a.
+// (bayes_engine.cpp:236-240) on sm_100a, one GPU or P GPUs.
 //
 // Single-RHS TRSV is a GEMV over the packed factor (HBM bound, ~0.25
 // flop/byte) plus a sequential dependency chain over the nb = n/64 diagonal
-// blocks.  Design (one cooperative persistent launch for BOTH sweeps):
+// blocks.  Design (one cooperative persistent launch per rank for BOTH
+// sweeps):
 //
-//   * CTA 0 is the CHAIN CTA, CTAs 1..G-1 are WORKERS;
-//   * worker rows (round robin) stream their panel tiles as soon as the
-//     needed solution blocks exist, but stop kLook tiles short of the
-//     diagonal and hand the chain c_I = L_II^{-1} (b_I - sum_{J<I-kLook}
-//     L_IJ y_J);
-//   * the chain finishes y_I = c_I - sum_{k=1..kLook} M_{I,k} y_{I-k} with the
-//     precomputed M_{I,k} = L_II^{-1} L_{I,I-k} (prefetched into registers a
-//     step ahead) and the last kLook blocks of y kept in shared memory, so
-//     the critical path per 64-block is one 64 x (64 kLook) GEMV plus one
-//     L2 round trip;
-//   * no flags: every hand-off buffer (c_I, y, x) is pre-filled with a NaN
-//     sentinel (all ones, never produced by arithmetic, which yields the
-//     canonical NaN) and consumers poll the VALUES themselves with
-//     gpu-scope relaxed loads -- one L2 round trip per hand-off instead of
-//     flag + data;
-//   * the transposed sweep is the mirror image (rows descending, panel tiles
-//     down the block column, M'_{I,k} = L_II^{-T} L_{I+k,I}^T) and follows in
-//     the same launch: a worker moves on to its transposed rows as soon as its
-//     forward rows are done.
+//   * the factor is distributed row-cyclically (block row I on rank I mod P;
+//     P = 1 is the single-GPU packed triangle);
+//   * rank 0's CTA 0 is the CHAIN; every other CTA is a WORKER of its rank;
+//   * forward sweep: a worker owns whole block rows of its rank, streams the
+//     row's panel tiles through a TMA ring as soon as the needed y blocks
+//     exist, stops kLook tiles short of the diagonal and hands the chain
+//     c_I = L_II^{-1} (b_I - sum_{J<I-kLook} L_IJ y_J);
+//   * the chain finishes y_I = c_I - sum_{k<=kLook} M_{I,k} y_{I-k}
+//     (M_{I,k} = L_II^{-1} L_{I,I-k} precomputed, prefetched into registers a
+//     step ahead, last kLook blocks of y kept in shared memory) and pushes
+//     y_I to every rank;
+//   * transposed sweep: block column I is spread over the ranks, so every
+//     rank's workers reduce their share s_h = sum_{J=h mod P, J>I+kLook}
+//     L_JI^T x_J and push q_h = L_II^{-T} (delta y_I - s_h) to the chain, which
+//     sums the P hand-offs and finishes x_I with M'_{I,k} = L_II^{-T}
+//     L_{I+k,I}^T; x_I is pushed to every rank;
+//   * no flags: every hand-off slot is pre-filled with a NaN sentinel (all
+//     ones; arithmetic only ever produces the canonical NaN) and consumers
+//     poll the VALUES with system-scope relaxed loads -- one memory round
+//     trip per hand-off.  Across GPUs the pushes are plain stores through
+//     CUDA-IPC-mapped peer memory (NVLink); a ready-flag barrier at launch
+//     start guarantees no rank pushes before the receiver re-armed its
+//     sentinels.
+//
+// All P ranks can also be emulated by ONE launch on one GPU (the CTAs split
+// into P groups, the "peer" buffers live on the same device), which is how
+// the distributed algorithm is validated without P GPUs.
 #include <math.h>
+
+#include <algorithm>
 
 #include "ltb_common.cuh"
 #include "ltb_gen.cuh"
@@ -35,16 +46,34 @@ namespace ltb {
 namespace {
 
 constexpr int kQ = 8;                // column groups per 64-row tile
-constexpr int kThreads = 64 * kQ;   // 512: thread (row, group)
-constexpr int kCPT = kTB / kQ;      // 8 tile columns per thread
-constexpr int kPad = 65;                               // padded smem tile stride
+constexpr int kThreads = 64 * kQ;    // 512: thread (row, group)
+constexpr int kCPT = kTB / kQ;       // 8 tile columns per thread
+constexpr int kPad = 65;             // padded smem tile stride
 constexpr int kTile = kTB * kTB;
+constexpr int kRing = 4;             // worker TMA ring depth (32 KB stages)
 constexpr unsigned long long kSentinel = ~0ull;        // all-ones NaN
 constexpr unsigned long long kSpinNs = 4000000000ull;  // 4 s dependency-wait timeout
 
+// recv layout (in doubles)
+__host__ __device__ inline size_t off_yf(int) { return 0; }
+__host__ __device__ inline size_t off_xb(int nb) { return (size_t)nb * kTB; }
+__host__ __device__ inline size_t off_ready(int nb) { return 2 * (size_t)nb * kTB; }
+__host__ __device__ inline size_t off_cf(int nb) { return 2 * (size_t)nb * kTB + kMaxRanks; }
+__host__ __device__ inline size_t off_cb(int nb) { return 3 * (size_t)nb * kTB + kMaxRanks; }
+__host__ __device__ inline size_t recv_len(int nb, int P) { return off_cb(nb) + (size_t)P * nb * kTB; }
+
+// tile offset (in tiles) of local row li on rank r of P
+__host__ __device__ inline size_t row_off(long long li, int r, int P) {
+  return (size_t)(li * (r + 1) + (long long)P * li * (li - 1) / 2);
+}
+__host__ inline size_t rank_tiles(int nb, int r, int P) {
+  const long long rows = r < nb ? (nb - 1 - r) / P + 1 : 0;
+  return row_off(rows, r, P);
+}
+
 LTB_DEV unsigned long long ld_relaxed_u64(const double* p) {
   unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 LTB_DEV unsigned long long globaltimer() {
@@ -72,21 +101,23 @@ LTB_DEV double poll_value(const double* p, int* status) {
   }
 }
 
-LTB_DEV size_t tile_off(int I, int J) { return ((size_t)I * (I + 1) / 2 + J) * kTile; }
+struct RankView {
+  const double* tiles;  // this rank's packed rows
+  const double* dinv;   // all nb diagonal inverses
+  const double* b;      // right-hand side (padded, replicated)
+  double* recv;         // this rank's receive buffers
+};
 
-struct SweepArgs {
-  const double* tiles;
-  const double* dinv;
-  const double* mf;
+struct DistArgs {
+  int P, r0, nloc, nb, gper;      // ranks, first local rank, local ranks, blocks, CTAs per rank
+  RankView loc[kMaxRanks];        // local ranks (index rank - r0)
+  double* peer[kMaxRanks];        // recv of EVERY rank, addressable from this launch
+  const double* mf;               // chain tiles (rank 0 local)
   const double* mb;
-  const double* b;  // right-hand side (padded)
-  double* yf;       // forward result   (sentinel on entry)
-  double* xb;       // transposed result (sentinel on entry) = the solution
-  double* cf;       // forward worker hand-offs  (sentinel on entry)
-  double* cb;       // transposed worker hand-offs (sentinel on entry)
-  int nb;
+  unsigned epoch;
+  unsigned* gsync;                // local grid barrier {count, generation}
   int* status;
-  unsigned long long* trace;  // optional: per-step timestamps (ltb_trsv_trace)
+  unsigned long long* trace;
 };
 
 // fixed-order sum of the kQ column-group partials of row r
@@ -109,10 +140,26 @@ struct WorkerSmem {
   double sR[2 * kTB];
 };
 
-// The chain tiles of step I are loaded into registers one step ahead.  The
-// two register sets alternate (manual 2x unroll) so a prefetch is first
-// consumed one full step after it was issued -- its HBM latency overlaps
-// the poll of the previous step instead of stalling a register copy.
+// grid-wide barrier of this launch (all CTAs co-resident: cooperative launch)
+LTB_DEV void grid_barrier(unsigned* gsync) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = gsync + 1;
+    const unsigned g = *gen;
+    __threadfence_system();
+    if (atomicAdd(gsync, 1u) == gridDim.x - 1) {
+      gsync[0] = 0;
+      __threadfence();
+      atomicAdd(gsync + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------- chain ------------------------------------------------------
 LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double (&m)[kLook][kCPT]) {
   const int i = threadIdx.x & 63, q = threadIdx.x >> 6;
 #pragma unroll
@@ -125,17 +172,22 @@ LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double
   }
 }
 
-// one chain step: out_I = c_I - sum_{k < nvalid} M_{I,k} ring[slot_k]
+// The chain tiles of step I are loaded into registers one step ahead; the two
+// register sets (and the prefetched hand-offs) alternate through a manual 2x
+// unroll so a prefetch is first consumed one full step after it was issued.
+// Hand-off of step I: forward = cf[I] (one worker); transposed = sum over the
+// P ranks' cb[h][I].
 template <bool kForward>
-LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
+LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, int I, int nvalid,
                         const double (&m)[kLook][kCPT], unsigned long long cur,
                         unsigned long long& nxt) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
-  const double* cbuf = kForward ? a.cf : a.cb;
-  // speculative prefetch of the next step's hand-off (workers usually run
-  // ahead); a sentinel just means "poll it then"
+  const int nb = a.nb, P = kForward ? 1 : a.P;
+  double* recv0 = a.loc[0].recv;  // the chain runs on rank 0 = local rank 0
+  const double* cbuf = recv0 + (kForward ? off_cf(nb) : off_cb(nb));
   const int In = kForward ? I + 1 : I - 1;
-  if (tid < kTB && In >= 0 && In < a.nb) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
+  // prefetch rank 0's hand-off of the next step (the others are polled)
+  if (tid < kTB && In >= 0 && In < nb) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
   double p = 0.0;
 #pragma unroll
   for (int k = 0; k < kLook; ++k) {
@@ -149,18 +201,23 @@ LTB_DEV void chain_step(const SweepArgs& a, ChainSmem& sm, int I, int nvalid,
   sm.red[q][i] = p;
   __syncthreads();
   if (tid < kTB) {
-    const double c = cur != kSentinel ? __longlong_as_double((long long)cur)
-                                      : poll_value(cbuf + (size_t)I * kTB + tid, a.status);
-    const double v = c - (red_sum(sm.red, tid));
-    (kForward ? a.yf : a.xb)[(size_t)I * kTB + tid] = v;
+    unsigned long long raw[kMaxRanks];
+    for (int h = 1; h < P; ++h) raw[h] = ld_relaxed_u64(cbuf + ((size_t)h * nb + I) * kTB + tid);
+    double c = cur != kSentinel ? __longlong_as_double((long long)cur)
+                                : poll_value(cbuf + (size_t)I * kTB + tid, a.status);
+    for (int h = 1; h < P; ++h)  // fixed order h = 0, 1, ..., P-1
+      c += raw[h] != kSentinel ? __longlong_as_double((long long)raw[h])
+                               : poll_value(cbuf + ((size_t)h * nb + I) * kTB + tid, a.status);
+    const double v = c - red_sum(sm.red, tid);
+    const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + tid;
+    for (int r = 0; r < a.P; ++r) a.peer[r][o] = v;  // push to every rank
     sm.ring[I % kLook][tid] = v;
   }
   __syncthreads();
-  if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : a.nb) + I] = globaltimer();
+  if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
 }
 
-// ---------------- chain, forward: y_I = c_I - sum_k M_{I,k} y_{I-k} ----------
-LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
+LTB_DEV void chain_forward(const DistArgs& a, ChainSmem& sm) {
   double mA[kLook][kCPT], mB[kLook][kCPT];
   unsigned long long cA = kSentinel, cB = kSentinel;
   auto nvalid = [&](int I) { return I < kLook ? I : kLook; };
@@ -174,12 +231,11 @@ LTB_DEV void chain_forward(const SweepArgs& a, ChainSmem& sm) {
   }
 }
 
-// ---------------- chain, transposed: x_I = c_I - sum_k M'_{I,k} x_{I+k} ------
-LTB_DEV void chain_transposed(const SweepArgs& a, ChainSmem& sm) {
+LTB_DEV void chain_transposed(const DistArgs& a, ChainSmem& sm) {
   double mA[kLook][kCPT], mB[kLook][kCPT];
+  unsigned long long cA = kSentinel, cB = kSentinel;
   const int nb = a.nb;
   auto nvalid = [&](int I) { return nb - 1 - I < kLook ? nb - 1 - I : kLook; };
-  unsigned long long cA = kSentinel, cB = kSentinel;
   for (int I = nb - 1; I >= 0; I -= 2) {
     if (I - 1 >= 0) load_chain_tiles(a.mb, I - 1, nvalid(I - 1), mB);
     chain_step<false>(a, sm, I, nvalid(I), mA, cA, cB);
@@ -196,12 +252,10 @@ LTB_DEV void chain_transposed(const SweepArgs& a, ChainSmem& sm) {
 // stage), so a worker keeps ~96 KB of the factor in flight without holding
 // it in registers.  A running tile counter carries the stage / phase across
 // rows and sweeps.
-constexpr int kRing = 4;
-
 struct TileRing {
-  double* stage;  // kRing * kTile doubles (dynamic shared memory)
-  uint64_t* full; // kRing mbarriers
-  unsigned next;  // tiles consumed so far by this CTA
+  double* stage;   // kRing * kTile doubles (dynamic shared memory)
+  uint64_t* full;  // kRing mbarriers
+  unsigned next;   // tiles consumed so far by this CTA
 };
 
 LTB_DEV void ring_issue(TileRing& r, unsigned g, const double* src, uint64_t policy) {
@@ -210,23 +264,24 @@ LTB_DEV void ring_issue(TileRing& r, unsigned g, const double* src, uint64_t pol
   bulk_g2s(r.stage + (size_t)s * kTile, src, kTile * sizeof(double), r.full + s, policy);
 }
 
-// forward row I: thread (i = tid & 63, q = tid >> 6) owns row i, columns
-// [8q, 8q+8) of each tile L_IJ, J < I - kLook (contiguous in memory)
-LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ring, int I,
-                                uint64_t policy) {
+// forward row I of rank r: thread (i = tid & 63, q = tid >> 6) owns row i,
+// columns [8q, 8q+8) of each tile L_IJ, J < I - kLook (contiguous in memory)
+LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSmem& sm,
+                                TileRing& ring, int I, const double* row, uint64_t policy) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  const int nb = a.nb;
+  const double* yf = rv.recv + off_yf(nb);
   const int jmax = I - kLook;  // panel tiles J < jmax; the chain does the rest
-  const double* row = a.tiles + tile_off(I, 0);
   const unsigned g0 = ring.next;
   if (tid == 0)
     for (int J = 0; J < jmax && J < kRing; ++J) ring_issue(ring, g0 + J, row + (size_t)J * kTile, policy);
-  const double* D = a.dinv + (size_t)I * kTile;
+  const double* D = rv.dinv + (size_t)I * kTile;
   for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
   double acc = 0.0;
   unsigned long long yraw[kCPT];
   if (jmax > 0) {
 #pragma unroll
-    for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(a.yf + kCPT * q + k);
+    for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(yf + kCPT * q + k);
   }
   for (int J = 0; J < jmax; ++J) {
     // resolve this tile's solution block (prefetched one tile ago)
@@ -234,10 +289,10 @@ LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ri
 #pragma unroll
     for (int k = 0; k < kCPT; ++k)
       yv[k] = yraw[k] != kSentinel ? __longlong_as_double((long long)yraw[k])
-                                   : poll_value(a.yf + (size_t)J * kTB + kCPT * q + k, a.status);
+                                   : poll_value(yf + (size_t)J * kTB + kCPT * q + k, a.status);
     if (J + 1 < jmax) {
 #pragma unroll
-      for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(a.yf + (size_t)(J + 1) * kTB + kCPT * q + k);
+      for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(yf + (size_t)(J + 1) * kTB + kCPT * q + k);
     }
     const unsigned g = g0 + J;
     mbar_wait(ring.full + g % kRing, (g / kRing) & 1);
@@ -250,55 +305,60 @@ LTB_DEV void worker_forward_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ri
   ring.next = g0 + (jmax > 0 ? jmax : 0);
   sm.red[q][i] = acc;
   __syncthreads();
-  if (tid < kTB)
-    sm.rr[tid] = __ldg(a.b + (size_t)I * kTB + tid) -
-                 (red_sum(sm.red, tid));
+  if (tid < kTB) sm.rr[tid] = __ldg(rv.b + (size_t)I * kTB + tid) - red_sum(sm.red, tid);
   __syncthreads();
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < kCPT; ++k) s = fma(sm.sD[(kCPT * q + k) * kPad + i], sm.rr[kCPT * q + k], s);
   sm.red[q][i] = s;
   __syncthreads();
-  if (tid < kTB)
-    a.cf[(size_t)I * kTB + tid] = red_sum(sm.red, tid);
+  if (tid < kTB) a.peer[0][off_cf(nb) + (size_t)I * kTB + tid] = red_sum(sm.red, tid);
   __syncthreads();
-  if (a.trace && tid == 0) a.trace[2 * a.nb + I] = globaltimer();
+  if (a.trace && tid == 0 && a.r0 == 0) a.trace[2 * nb + I] = globaltimer();
 }
 
-// transposed row I: thread (j = tid & 63, q = tid >> 6) reads row j of tile
-// L_JI (J descending, J > I + kLook), columns [8q, 8q+8), keeping 8
-// partial sums of (L_JI^T x_J)
-LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing& ring, int I,
-                                   uint64_t policy) {
+// transposed column I, rank r's share: thread (j = tid & 63, q = tid >> 6)
+// reads row j of tile L_JI for J = r (mod P), J > I + kLook (descending),
+// columns [8q, 8q+8), keeping 8 partial sums of (L_JI^T x_J); hands the
+// chain q_r = L_II^{-T} (delta_{r, I mod P} y_I - s_r)
+LTB_DEV void worker_transposed_col(const DistArgs& a, const RankView& rv, int r, WorkerSmem& sm,
+                                   TileRing& ring, int I, uint64_t policy) {
   const int tid = threadIdx.x, j = tid & 63, q = tid >> 6;
-  const int nb = a.nb;
-  const int jmin = I + kLook;  // panel tiles J > jmin; the chain does the rest
-  const int ntile = nb - 1 - jmin > 0 ? nb - 1 - jmin : 0;
+  const int nb = a.nb, P = a.P;
+  const double* xb = rv.recv + off_xb(nb);
+  const double* yf = rv.recv + off_yf(nb);
+  // this rank's rows J > I + kLook, descending from the largest J = r (mod P)
+  const int jmin = I + kLook;
+  const int Jtop = nb - 1 - ((nb - 1 - r) % P + P) % P;
+  const int ntile = Jtop > jmin ? (Jtop - jmin - 1) / P + 1 : 0;
+  auto tile_of = [&](int J) {
+    return rv.tiles + (row_off((J - r) / P, r, P) + (size_t)I) * kTile;
+  };
   const unsigned g0 = ring.next;
   if (tid == 0)
-    for (int t = 0; t < ntile && t < kRing; ++t) ring_issue(ring, g0 + t, a.tiles + tile_off(nb - 1 - t, I), policy);
-  const double* D = a.dinv + (size_t)I * kTile;
+    for (int t = 0; t < ntile && t < kRing; ++t) ring_issue(ring, g0 + t, tile_of(Jtop - t * P), policy);
+  const double* D = rv.dinv + (size_t)I * kTile;
   for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
   double acc[kCPT];
 #pragma unroll
   for (int k = 0; k < kCPT; ++k) acc[k] = 0.0;
-  unsigned long long xraw = ntile > 0 ? ld_relaxed_u64(a.xb + (size_t)(nb - 1) * kTB + j) : 0ull;
+  unsigned long long xraw = ntile > 0 ? ld_relaxed_u64(xb + (size_t)Jtop * kTB + j) : 0ull;
   for (int t = 0; t < ntile; ++t) {
-    const int J = nb - 1 - t;
+    const int J = Jtop - t * P;
     const double xj = xraw != kSentinel ? __longlong_as_double((long long)xraw)
-                                        : poll_value(a.xb + (size_t)J * kTB + j, a.status);
-    if (t + 1 < ntile) xraw = ld_relaxed_u64(a.xb + (size_t)(J - 1) * kTB + j);
+                                        : poll_value(xb + (size_t)J * kTB + j, a.status);
+    if (t + 1 < ntile) xraw = ld_relaxed_u64(xb + (size_t)(J - P) * kTB + j);
     const unsigned g = g0 + t;
     mbar_wait(ring.full + g % kRing, (g / kRing) & 1);
     const double* T = ring.stage + (size_t)(g % kRing) * kTile;
 #pragma unroll
     for (int k = 0; k < kCPT; ++k) acc[k] = fma(T[(kCPT * q + k) * kTB + j], xj, acc[k]);
     __syncthreads();  // stage consumed
-    if (tid == 0 && t + kRing < ntile) ring_issue(ring, g + kRing, a.tiles + tile_off(J - kRing, I), policy);
+    if (tid == 0 && t + kRing < ntile) ring_issue(ring, g + kRing, tile_of(J - kRing * P), policy);
   }
   ring.next = g0 + ntile;
   // reduce over j: 32-lane shuffle tree per partial, then the two warps of
-  // each column quarter meet in shared memory
+  // each column group meet in shared memory
 #pragma unroll
   for (int k = 0; k < kCPT; ++k) {
     double v = acc[k];
@@ -311,9 +371,11 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
     for (int k = 0; k < kCPT; ++k) sm.sR[(j >> 5) * kTB + kCPT * q + k] = acc[k];
   }
   __syncthreads();
-  // y_I is the forward result: final (polled, the forward chain wrote it)
-  if (tid < kTB)
-    sm.rr[tid] = poll_value(a.yf + (size_t)I * kTB + tid, a.status) - (sm.sR[tid] + sm.sR[kTB + tid]);
+  if (tid < kTB) {
+    // y_I (the forward result) enters once, through the rank owning row I
+    const double yI = (I % P == r) ? poll_value(yf + (size_t)I * kTB + tid, a.status) : 0.0;
+    sm.rr[tid] = yI - (sm.sR[tid] + sm.sR[kTB + tid]);
+  }
   __syncthreads();
   {
     const int ii = tid & 63, part = tid >> 6;
@@ -324,89 +386,146 @@ LTB_DEV void worker_transposed_row(const SweepArgs& a, WorkerSmem& sm, TileRing&
     sm.red[part][ii] = s;
   }
   __syncthreads();
-  if (tid < kTB)
-    a.cb[(size_t)I * kTB + tid] = red_sum(sm.red, tid);
+  if (tid < kTB) a.peer[0][off_cb(nb) + ((size_t)r * nb + I) * kTB + tid] = red_sum(sm.red, tid);
   __syncthreads();
-  if (a.trace && tid == 0) a.trace[3 * a.nb + I] = globaltimer();
+  if (a.trace && tid == 0 && a.r0 == 0 && r == 0) a.trace[3 * nb + I] = globaltimer();
 }
 
-__global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
   __shared__ union {
     ChainSmem chain;
     WorkerSmem worker;
   } sm;
   extern __shared__ __align__(128) unsigned char ring_smem[];
-  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[4 * a.nb] = globaltimer();
-  if (blockIdx.x == 0) {
+  const int nb = a.nb;
+  const int grp = blockIdx.x / a.gper, lc = blockIdx.x % a.gper;
+  const int r = a.r0 + grp;
+  const RankView rv = a.loc[grp];
+
+  // (1) re-arm this rank's hand-off sentinels (everything but the ready flags)
+  {
+    const size_t n1 = off_ready(nb), n2 = recv_len(nb, a.P) - off_cf(nb);
+    unsigned long long* base = reinterpret_cast<unsigned long long*>(rv.recv);
+    for (size_t e = (size_t)lc * kThreads + threadIdx.x; e < n1 + n2; e += (size_t)a.gper * kThreads)
+      base[e < n1 ? e : off_cf(nb) + (e - n1)] = kSentinel;
+  }
+  grid_barrier(a.gsync);
+  // (2) real multi-GPU: no rank may push before every receiver has re-armed
+  if (a.nloc < a.P) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      for (int p = 0; p < a.P; ++p) {
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(a.peer[p] + off_ready(nb)) + r;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"((unsigned long long)a.epoch) : "memory");
+      }
+      const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(rv.recv + off_ready(nb));
+      const unsigned long long t0 = globaltimer();
+      for (int p = 0; p < a.P; ++p) {
+        while (true) {
+          unsigned long long v;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + p) : "memory");
+          if (v >= a.epoch) break;
+          if (globaltimer() - t0 > kSpinNs) {
+            atomicExch(a.status, 1);
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+    }
+    grid_barrier(a.gsync);
+  }
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && a.r0 == 0) a.trace[4 * nb] = globaltimer();
+
+  if (r == 0 && lc == 0) {
     chain_forward(a, sm.chain);
     chain_transposed(a, sm.chain);
-    return;
+  } else {
+    TileRing ring;
+    ring.stage = reinterpret_cast<double*>(ring_smem);
+    ring.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kRing * kTile * sizeof(double));
+    ring.next = 0;
+    uint64_t policy = 0;
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kRing; ++s) mbar_init(ring.full + s, 1);
+      fence_mbar_init();
+      policy = policy_evict_first();
+    }
+    __syncthreads();
+    const int w = r == 0 ? lc - 1 : lc, W = r == 0 ? a.gper - 1 : a.gper;
+    // forward: this rank's rows I = r + P li
+    const int nrows = r < nb ? (nb - 1 - r) / a.P + 1 : 0;
+    for (int li = w; li < nrows; li += W)
+      worker_forward_row(a, rv, sm.worker, ring, r + a.P * li, rv.tiles + row_off(li, r, a.P) * kTile, policy);
+    // transposed: every column, this rank's share
+    for (int I = nb - 1 - w; I >= 0; I -= W) worker_transposed_col(a, rv, r, sm.worker, ring, I, policy);
   }
-  TileRing ring;
-  ring.stage = reinterpret_cast<double*>(ring_smem);
-  ring.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kRing * kTile * sizeof(double));
-  ring.next = 0;
-  uint64_t policy = 0;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kRing; ++s) mbar_init(ring.full + s, 1);
-    fence_mbar_init();
-    policy = policy_evict_first();
+  // (3) leave only once this rank's copy of x is complete
+  {
+    const double* xb = rv.recv + off_xb(nb);
+    for (size_t e = (size_t)lc * kThreads + threadIdx.x; e < (size_t)nb * kTB; e += (size_t)a.gper * kThreads)
+      (void)poll_value(xb + e, a.status);
   }
-  __syncthreads();
-  const int W = gridDim.x - 1, w = blockIdx.x - 1;
-  for (int I = w; I < a.nb; I += W) worker_forward_row(a, sm.worker, ring, I, policy);
-  for (int I = a.nb - 1 - w; I >= 0; I -= W) worker_transposed_row(a, sm.worker, ring, I, policy);
 }
 
 constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
 
-// tile (I, J) for tile index t = I (I+1)/2 + J
-LTB_DEV void tile_ij(long long t, int* I, int* J) {
-  long long r = (long long)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while (r * (r + 1) / 2 > t) --r;
-  while ((r + 1) * (r + 2) / 2 <= t) ++r;
-  *I = (int)r;
-  *J = (int)(t - r * (r + 1) / 2);
+// ---------------- setup kernels ----------------------------------------------
+// local tile index t of rank r -> (I, J)
+LTB_DEV void local_tile_ij(long long t, int r, int P, int nrows, int* I, int* J) {
+  int lo = 0, hi = nrows - 1;  // largest li with row_off(li) <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if ((long long)row_off(mid, r, P) <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  *I = r + P * lo;
+  *J = (int)(t - (long long)row_off(lo, r, P));
 }
 
-__global__ void pack_colmajor_kernel(const double* __restrict__ L, size_t ld, int n,
-                                     double* __restrict__ tiles) {
+LTB_DEV double factor_value(bool gen, const double* L, size_t ld, uint64_t key, double scale, int n,
+                            int row, int col) {
+  if (row >= n || col >= n) return row == col ? 1.0 : 0.0;  // identity padding
+  if (col > row) return 0.0;
+  return gen ? gen_factor_entry(key, n, scale, row, col) : L[(size_t)col * ld + row];
+}
+
+// pack this rank's rows (from a device column-major L, or generated)
+__global__ void pack_rows_kernel(bool gen, const double* __restrict__ L, size_t ld, uint64_t key,
+                                 double scale, int n, int r, int P, int nrows,
+                                 double* __restrict__ tiles) {
   int I, J;
-  tile_ij(blockIdx.x, &I, &J);
+  local_tile_ij(blockIdx.x, r, P, nrows, &I, &J);
   double* dst = tiles + (size_t)blockIdx.x * kTile;
   for (int e = threadIdx.x; e < kTile; e += blockDim.x) {
     const int jj = e >> 6, ii = e & 63;
-    const int r = I * kTB + ii, c = J * kTB + jj;
-    double v;
-    if (r < n && c < n) v = (c <= r) ? L[(size_t)c * ld + r] : 0.0;
-    else v = (r == c) ? 1.0 : 0.0;
-    dst[e] = v;
+    dst[e] = factor_value(gen, L, ld, key, scale, n, I * kTB + ii, J * kTB + jj);
   }
 }
 
-__global__ void pack_generated_kernel(uint64_t key, int n, double scale, double* __restrict__ tiles) {
-  int I, J;
-  tile_ij(blockIdx.x, &I, &J);
-  double* dst = tiles + (size_t)blockIdx.x * kTile;
-  for (int e = threadIdx.x; e < kTile; e += blockDim.x) {
-    const int jj = e >> 6, ii = e & 63;
-    const int r = I * kTB + ii, c = J * kTB + jj;
-    double v;
-    if (r < n && c < n) v = gen_factor_entry(key, n, scale, r, c);
-    else v = (r == c) ? 1.0 : 0.0;
-    dst[e] = v;
+// tile (I, J) of the full factor staged into padded shared memory
+// s[col * kPad + row], from the packed single-rank layout or regenerated
+LTB_DEV void stage_tile(bool gen, const double* tiles, uint64_t key, double scale, int n, int I,
+                        int J, double* s) {
+  if (gen) {
+    for (int e = threadIdx.x; e < kTile; e += blockDim.x) {
+      const int jj = e >> 6, ii = e & 63;
+      s[jj * kPad + ii] = factor_value(true, nullptr, 0, key, scale, n, I * kTB + ii, J * kTB + jj);
+    }
+  } else {
+    const double* T = tiles + (row_off(I, 0, 1) + (size_t)J) * kTile;
+    for (int e = threadIdx.x; e < kTile; e += blockDim.x) s[(e >> 6) * kPad + (e & 63)] = T[e];
   }
 }
 
 // one CTA per diagonal tile, thread c solves L_II x = e_c
-__global__ void __launch_bounds__(64) invert_diag_kernel(const double* __restrict__ tiles,
+__global__ void __launch_bounds__(64) invert_diag_kernel(bool gen, const double* __restrict__ tiles,
+                                                         uint64_t key, double scale, int n,
                                                          double* __restrict__ dinv, int* status) {
   extern __shared__ double inv_smem[];
-  double* sL = inv_smem;              // kTB * kPad
+  double* sL = inv_smem;               // kTB * kPad
   double* sX = inv_smem + kTB * kPad;  // kTB * kPad
   const int I = blockIdx.x, c = threadIdx.x;
-  const double* T = tiles + tile_off(I, I);
-  for (int e = c; e < kTile; e += kTB) sL[(e >> 6) * kPad + (e & 63)] = T[e];
+  stage_tile(gen, tiles, key, scale, n, I, I, sL);
   __syncthreads();
   for (int i = 0; i < kTB; ++i) {
     double s = (i == c) ? 1.0 : 0.0;
@@ -428,7 +547,8 @@ __global__ void __launch_bounds__(64) invert_diag_kernel(const double* __restric
 // chain tiles: blockIdx = (I, k-1, dir)
 //   dir 0: mf[I][k-1] = Dinv_II L_{I,I-k}          C[i][j] = sum_l D[i][l] L[l][j]
 //   dir 1: mb[I][k-1] = Dinv_II^T L_{I+k,I}^T      C[i][j] = sum_l D[l][i] L[j][l]
-__global__ void __launch_bounds__(256) chain_tiles_kernel(const double* __restrict__ tiles,
+__global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double* __restrict__ tiles,
+                                                          uint64_t key, double scale, int n,
                                                           const double* __restrict__ dinv,
                                                           double* __restrict__ mf,
                                                           double* __restrict__ mb, int nb) {
@@ -444,11 +564,9 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(const double* __restri
     return;
   }
   const double* A = dinv + (size_t)I * kTile;
-  const double* B = dir == 0 ? tiles + tile_off(I, J) : tiles + tile_off(J, I);
-  for (int e = tid; e < kTile; e += blockDim.x) {
-    sA[(e >> 6) * kPad + (e & 63)] = A[e];
-    sB[(e >> 6) * kPad + (e & 63)] = B[e];
-  }
+  for (int e = tid; e < kTile; e += blockDim.x) sA[(e >> 6) * kPad + (e & 63)] = A[e];
+  if (dir == 0) stage_tile(gen, tiles, key, scale, n, I, J, sB);
+  else stage_tile(gen, tiles, key, scale, n, J, I, sB);
   __syncthreads();
   for (int jj = 16 * q; jj < 16 * q + 16; ++jj) {
     double s = 0.0;
@@ -461,60 +579,31 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(const double* __restri
   }
 }
 
-int g_coop_grid = -1;
+int g_coop_blocks = -1;  // co-resident CTAs of trsv_kernel on this device
 
-}  // namespace
-
-cudaError_t trsv_alloc(TriFactor& t, int n) {
-  trsv_free(t);
-  t.n = n;
-  t.nb = (n + kTB - 1) / kTB;
-  const size_t ntiles = (size_t)t.nb * (t.nb + 1) / 2;
-  const size_t chain = (size_t)t.nb * kLook * kTile;
-  const size_t vec = (size_t)t.nb * kTB;
-  t.bytes = (ntiles + t.nb + 2 * chain / kTile) * kTile * sizeof(double) + 5 * vec * sizeof(double);
-  cudaError_t e;
-  if ((e = cudaMalloc(&t.tiles, ntiles * kTile * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.dinv, (size_t)t.nb * kTile * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.mf, chain * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.mb, chain * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.work, 4 * vec * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.status, sizeof(int))) != cudaSuccess) return e;
-  cudaMemset(t.status, 0, sizeof(int));
+cudaError_t coop_blocks(int* out) {
+  if (g_coop_blocks < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kRingSmem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, kRingSmem);
+    g_coop_blocks = std::max(2, sms * per);
+  }
+  *out = g_coop_blocks;
   return cudaSuccess;
 }
 
-void trsv_free(TriFactor& t) {
-  cudaFree(t.tiles);
-  cudaFree(t.dinv);
-  cudaFree(t.mf);
-  cudaFree(t.mb);
-  cudaFree(t.work);
-  cudaFree(t.status);
-  cudaFree(t.trace);
-  t = TriFactor();
-}
-
-cudaError_t trsv_pack_colmajor(TriFactor& t, const double* L, size_t ld, cudaStream_t st) {
-  const size_t ntiles = (size_t)t.nb * (t.nb + 1) / 2;
-  pack_colmajor_kernel<<<(unsigned)ntiles, 256, 0, st>>>(L, ld, t.n, t.tiles);
-  return cudaGetLastError();
-}
-
-cudaError_t trsv_pack_generated(TriFactor& t, uint64_t seed, cudaStream_t st) {
-  const size_t ntiles = (size_t)t.nb * (t.nb + 1) / 2;
-  const double scale = 0.5 / sqrt((double)t.n);
-  pack_generated_kernel<<<(unsigned)ntiles, 256, 0, st>>>(gen_key(seed, kStreamFactor), t.n, scale,
-                                                          t.tiles);
-  return cudaGetLastError();
-}
-
-cudaError_t trsv_prepare(TriFactor& t, cudaStream_t st) {
+cudaError_t prepare(TriFactor& t, bool gen, uint64_t key, double scale, cudaStream_t st) {
   const int smem = 2 * kTB * kPad * (int)sizeof(double);
   cudaFuncSetAttribute(invert_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(chain_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  invert_diag_kernel<<<t.nb, kTB, smem, st>>>(t.tiles, t.dinv, t.status);
-  chain_tiles_kernel<<<dim3(t.nb, kLook, 2), 256, smem, st>>>(t.tiles, t.dinv, t.mf, t.mb, t.nb);
+  invert_diag_kernel<<<t.nb, kTB, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv, t.status);
+  if (t.rank == 0)
+    chain_tiles_kernel<<<dim3(t.nb, kLook, 2), 256, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv,
+                                                                  t.mf, t.mb, t.nb);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int h = 0;
@@ -528,39 +617,137 @@ cudaError_t trsv_prepare(TriFactor& t, cudaStream_t st) {
   return cudaSuccess;
 }
 
-double* trsv_result(TriFactor& t) { return t.work + (size_t)t.nb * kTB; }
+DistArgs make_args(TriFactor* const* ts, const double* const* bs, int nloc, int gper) {
+  TriFactor& t0 = *ts[0];
+  DistArgs a = {};
+  a.P = t0.P;
+  a.r0 = t0.rank;
+  a.nloc = nloc;
+  a.nb = t0.nb;
+  a.gper = gper;
+  for (int g = 0; g < nloc; ++g) a.loc[g] = RankView{ts[g]->tiles, ts[g]->dinv, bs[g], ts[g]->recv};
+  for (int p = 0; p < a.P; ++p) a.peer[p] = nloc == a.P ? ts[p]->recv : t0.peer_recv[p];
+  a.mf = t0.mf;
+  a.mb = t0.mb;
+  a.epoch = ++t0.epoch;
+  a.gsync = t0.gsync;
+  a.status = t0.status;
+  a.trace = t0.rank == 0 ? t0.trace : nullptr;
+  return a;
+}
+
+cudaError_t launch(const DistArgs& a, cudaStream_t st) {
+  void* args[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((const void*)trsv_kernel, a.nloc * a.gper, kThreads, args,
+                                     kRingSmem, st);
+}
+
+}  // namespace
+
+cudaError_t trsv_alloc(TriFactor& t, int n, int P, int rank) {
+  trsv_free(t);
+  if (P < 1 || P > kMaxRanks || rank < 0 || rank >= P) return cudaErrorInvalidValue;
+  t.n = n;
+  t.nb = (n + kTB - 1) / kTB;
+  t.P = P;
+  t.rank = rank;
+  const size_t ntiles = rank_tiles(t.nb, rank, P);
+  const size_t chain = rank == 0 ? (size_t)t.nb * kLook * kTile : 0;
+  const size_t rl = recv_len(t.nb, P);
+  t.bytes = (ntiles + t.nb) * kTile * sizeof(double) + 2 * chain * sizeof(double) + rl * sizeof(double);
+  cudaError_t e;
+  if ((e = cudaMalloc(&t.tiles, std::max<size_t>(1, ntiles) * kTile * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.dinv, (size_t)t.nb * kTile * sizeof(double))) != cudaSuccess) return e;
+  if (chain) {
+    if ((e = cudaMalloc(&t.mf, chain * sizeof(double))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&t.mb, chain * sizeof(double))) != cudaSuccess) return e;
+  }
+  if ((e = cudaMalloc(&t.recv, rl * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.gsync, 2 * sizeof(unsigned))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.status, sizeof(int))) != cudaSuccess) return e;
+  cudaMemset(t.recv, 0, rl * sizeof(double));  // ready flags = 0
+  cudaMemset(t.gsync, 0, 2 * sizeof(unsigned));
+  cudaMemset(t.status, 0, sizeof(int));
+  for (int p = 0; p < kMaxRanks; ++p) t.peer_recv[p] = nullptr;
+  t.peer_recv[rank] = t.recv;
+  return cudaSuccess;
+}
+
+void trsv_free(TriFactor& t) {
+  for (int p = 0; p < kMaxRanks; ++p)
+    if (t.peer_opened[p] && t.peer_recv[p]) cudaIpcCloseMemHandle(t.peer_recv[p]);
+  cudaFree(t.tiles);
+  cudaFree(t.dinv);
+  cudaFree(t.mf);
+  cudaFree(t.mb);
+  cudaFree(t.recv);
+  cudaFree(t.gsync);
+  cudaFree(t.status);
+  cudaFree(t.trace);
+  t = TriFactor();
+}
+
+cudaError_t trsv_pack_colmajor(TriFactor& t, const double* L, size_t ld, cudaStream_t st) {
+  if (t.P != 1) return cudaErrorInvalidValue;
+  const size_t ntiles = rank_tiles(t.nb, 0, 1);
+  pack_rows_kernel<<<(unsigned)ntiles, 256, 0, st>>>(false, L, ld, 0, 0.0, t.n, 0, 1, t.nb, t.tiles);
+  return cudaGetLastError();
+}
+
+cudaError_t trsv_prepare_packed(TriFactor& t, cudaStream_t st) { return prepare(t, false, 0, 0.0, st); }
+
+cudaError_t trsv_setup_generated(TriFactor& t, uint64_t seed, cudaStream_t st) {
+  const uint64_t key = gen_key(seed, kStreamFactor);
+  const double scale = 0.5 / sqrt((double)t.n);
+  const size_t ntiles = rank_tiles(t.nb, t.rank, t.P);
+  const int nrows = t.rank < t.nb ? (t.nb - 1 - t.rank) / t.P + 1 : 0;
+  if (ntiles)
+    pack_rows_kernel<<<(unsigned)ntiles, 256, 0, st>>>(true, nullptr, 0, key, scale, t.n, t.rank, t.P,
+                                                       nrows, t.tiles);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return prepare(t, true, key, scale, st);
+}
+
+cudaError_t trsv_ipc_handle(const TriFactor& t, cudaIpcMemHandle_t* out) {
+  return cudaIpcGetMemHandle(out, t.recv);
+}
+
+cudaError_t trsv_connect(TriFactor& t, const cudaIpcMemHandle_t* handles) {
+  for (int p = 0; p < t.P; ++p) {
+    if (p == t.rank) continue;
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, handles[p], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return e;
+    t.peer_recv[p] = static_cast<double*>(ptr);
+    t.peer_opened[p] = true;
+  }
+  return cudaSuccess;
+}
+
+double* trsv_result(TriFactor& t) { return t.recv + off_xb(t.nb); }
 
 cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
-  if (g_coop_grid < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, kRingSmem);
-    g_coop_grid = sms * per;
-    if (g_coop_grid < 2) g_coop_grid = 2;
-  }
-  // one chain CTA + up to one worker per block row
-  const int grid = t.nb + 1 < g_coop_grid ? t.nb + 1 : g_coop_grid;
-  const size_t vec = (size_t)t.nb * kTB;
-  // hand-off buffers [yf | xb | cf | cb] <- sentinel (all-ones bytes)
-  cudaError_t e = cudaMemsetAsync(t.work, 0xFF, 4 * vec * sizeof(double), st);
+  for (int p = 0; p < t.P; ++p)
+    if (!t.peer_recv[p]) return cudaErrorInvalidValue;  // not connected
+  int blocks = 0;
+  cudaError_t e = coop_blocks(&blocks);
   if (e != cudaSuccess) return e;
-  SweepArgs a;
-  a.tiles = t.tiles;
-  a.dinv = t.dinv;
-  a.mf = t.mf;
-  a.mb = t.mb;
-  a.b = b;
-  a.yf = t.work;
-  a.xb = t.work + vec;
-  a.cf = t.work + 2 * vec;
-  a.cb = t.work + 3 * vec;
-  a.nb = t.nb;
-  a.status = t.status;
-  a.trace = t.trace;
-  void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((const void*)trsv_kernel, grid, kThreads, args, kRingSmem, st);
+  // one chain CTA + up to one worker per block row
+  const int gper = std::min(blocks, t.nb + 1);
+  TriFactor* ts[1] = {&t};
+  const double* bs[1] = {b};
+  return launch(make_args(ts, bs, 1, gper), st);
+}
+
+cudaError_t trsv_solve_emulated(TriFactor* const* ts, const double* const* bs, int P, cudaStream_t st) {
+  if (P < 1 || P > kMaxRanks || ts[0]->P != P) return cudaErrorInvalidValue;
+  int blocks = 0;
+  cudaError_t e = coop_blocks(&blocks);
+  if (e != cudaSuccess) return e;
+  const int gper = blocks / P;
+  if (gper < 2) return cudaErrorInvalidValue;
+  return launch(make_args(ts, bs, P, gper), st);
 }
 
 }  // namespace ltb

@@ -1,6 +1,7 @@
 // ltb_trsv.h -- K^{-1} application through the dense lower Cholesky factor
 // (replaces InferenceEngine::solve_k_inplace, bayes_engine.cpp:236-240:
-// Eigen triangularView<Lower>().solveInPlace then its transpose).
+// Eigen triangularView<Lower>().solveInPlace then its transpose), on one GPU
+// or distributed over P GPUs.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -8,41 +9,59 @@
 
 namespace ltb {
 
-constexpr int kTB = 64;    // factor tile edge
-constexpr int kLook = 3;   // diagonal-chain lookahead depth (tiles per chain step)
+constexpr int kTB = 64;        // factor tile edge
+constexpr int kLook = 3;       // diagonal-chain lookahead depth (tiles per chain step)
+constexpr int kMaxRanks = 8;
 
-// Lower factor packed as 64x64 tiles (I, J), J <= I, tile index
-// I (I+1)/2 + J, each tile column-major (row fastest).  The last tile row /
-// column is padded with the identity.  Precomputed once at set_factor time:
-//   dinv[I]     = L_II^{-1}
-//   mf[I][k-1]  = L_II^{-1} L_{I,I-k}          (k = 1..kLook, forward chain)
-//   mb[I][k-1]  = L_II^{-T} L_{I+k,I}^T        (k = 1..kLook, transposed chain)
+// Row-cyclic block distribution over P ranks: rank r holds the 64-row block
+// rows I = r, r+P, r+2P, ... packed row after row (row I has I+1 tiles,
+// local row li = (I-r)/P starts at tile li (r+1) + P li (li-1)/2; tiles are
+// column-major 64x64).  P = 1 is the plain packed lower triangle.  The last
+// block row / column is padded with the identity.
+//
+// Precomputed at set_factor time (every rank): dinv[I] = L_II^{-1} for ALL
+// I; on rank 0 (the chain rank) the chain tiles
+//   mf[I][k-1] = L_II^{-1} L_{I,I-k},  mb[I][k-1] = L_II^{-T} L_{I+k,I}^T.
+//
+// `recv` is the one allocation other ranks write into (CUDA IPC exported):
+// [ yf | xb | ready (8 doubles) | cf | cb (P blocks) ], each vector nb*64.
 struct TriFactor {
-  int n = 0;
-  int nb = 0;
+  int n = 0, nb = 0, P = 1, rank = 0;
   double* tiles = nullptr;
   double* dinv = nullptr;
   double* mf = nullptr;
   double* mb = nullptr;
-  double* work = nullptr;  // 4 * nb * 64 hand-off buffers [yf | x | cf | cb]
-  int* status = nullptr;   // device error word (spin timeout / bad pivot)
+  double* recv = nullptr;
+  double* peer_recv[kMaxRanks] = {};  // every rank's recv as addressable here
+  bool peer_opened[kMaxRanks] = {};
+  unsigned* gsync = nullptr;  // local grid barrier words
+  int* status = nullptr;      // device error word (spin timeout / bad pivot)
   unsigned long long* trace = nullptr;  // diagnostic timestamps, 4 nb + 1 (optional)
+  unsigned epoch = 0;
   size_t bytes = 0;
 };
 
-cudaError_t trsv_alloc(TriFactor& t, int n);
+// n = N_d * N_t, P ranks, this rank
+cudaError_t trsv_alloc(TriFactor& t, int n, int P = 1, int rank = 0);
 void trsv_free(TriFactor& t);
-// pack from a device column-major matrix (only the lower triangle is read)
+// P == 1: pack from a device column-major matrix (only the lower triangle
+// is read), then trsv_prepare_packed
 cudaError_t trsv_pack_colmajor(TriFactor& t, const double* L, size_t ld, cudaStream_t st);
-// pack the synthetic factor (ltb_gen.cuh gen_factor_entry)
-cudaError_t trsv_pack_generated(TriFactor& t, uint64_t seed, cudaStream_t st);
-// invert the diagonal tiles and build the chain tiles; returns
-// cudaErrorInvalidValue on a zero / non-finite pivot
-cudaError_t trsv_prepare(TriFactor& t, cudaStream_t st);
-// x = L^{-T} L^{-1} b for a device vector b of length nb * 64 (zero padded);
-// the result is left in trsv_result(t).  One memset + one cooperative
-// launch; a dependency-wait timeout is reported through t.status.
+cudaError_t trsv_prepare_packed(TriFactor& t, cudaStream_t st);
+// any P: pack this rank's rows of the synthetic factor (ltb_gen.cuh
+// gen_factor_entry) and build dinv / chain tiles from regenerated tiles
+cudaError_t trsv_setup_generated(TriFactor& t, uint64_t seed, cudaStream_t st);
+// P > 1: exchange `recv` (CUDA IPC); handles[p] for every rank
+cudaError_t trsv_ipc_handle(const TriFactor& t, cudaIpcMemHandle_t* out);
+cudaError_t trsv_connect(TriFactor& t, const cudaIpcMemHandle_t* handles);
+// x = L^{-T} L^{-1} b for b of length nb*64 (zero padded, the same on every
+// rank); the result is left in trsv_result(t) on EVERY rank.  One
+// cooperative launch per rank; ranks must launch concurrently.
 cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st);
 double* trsv_result(TriFactor& t);
+// All P ranks emulated by ONE cooperative launch on the current GPU (test /
+// validation of the distributed algorithm without P GPUs).
+cudaError_t trsv_solve_emulated(TriFactor* const* ts, const double* const* bs, int P,
+                                cudaStream_t st);
 
 }  // namespace ltb
