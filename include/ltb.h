@@ -164,6 +164,20 @@ ltb_status ltb_engine_destroy(ltb_engine* e);
  * bayes_engine.cpp:180-193).  Repacked on the device into lower tiles. */
 ltb_status ltb_engine_set_factor(ltb_engine* e, const double* L, int n, size_t ld,
                                  int ptr_kind);
+/* Distributed K^{-1} over `world` ranks (one process per GPU; call before
+ * setting the factor).  The factor is split row-cyclically in 64-row blocks
+ * (rank r keeps block rows r, r+world, ...), built per rank by
+ * ltb_engine_set_factor_generated; the ranks then exchange the 64-byte CUDA
+ * IPC handles of their receive buffers (ltb_engine_ipc_handle, gathered in
+ * rank order and passed to ltb_engine_connect).  Every rank must call the
+ * solve / infer entry points concurrently.  With world > 1 the engine's G*
+ * and F_q plans are the rank's column shard: m_map is the rank's shard and
+ * q is the rank's partial forecast, to be summed over ranks by the caller
+ * (one small all-reduce). */
+ltb_status ltb_engine_set_world(ltb_engine* e, int world, int rank);
+ltb_status ltb_engine_ipc_handle(ltb_engine* e, void* out64);
+ltb_status ltb_engine_connect(ltb_engine* e, const void* handles);
+
 /* synthetic factor generated on the device (oracle orc_gen_factor) */
 ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed);
 

@@ -42,6 +42,9 @@ SIGNATURES = {
     "ltb_engine_create": ([_vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
     "ltb_engine_destroy": ([_vp], C.c_int),
     "ltb_engine_set_factor": ([_vp, _vp, C.c_int, C.c_size_t, C.c_int], C.c_int),
+    "ltb_engine_set_world": ([_vp, C.c_int, C.c_int], C.c_int),
+    "ltb_engine_ipc_handle": ([_vp, _vp], C.c_int),
+    "ltb_engine_connect": ([_vp, _vp], C.c_int),
     "ltb_engine_set_factor_generated": ([_vp, C.c_int, C.c_uint64], C.c_int),
     "ltb_engine_solve_k": ([_vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_engine_infer_map": ([_vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),

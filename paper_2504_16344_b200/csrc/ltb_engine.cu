@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "../../include/ltb.h"
@@ -63,6 +64,7 @@ struct ltb_engine {
   const ltb_plan* fq = nullptr;
   int device = 0;
   int nd = 0, nm = 0, nt = 0, nq = 0;
+  int world = 1, rank = 0;  // distributed K^{-1} (ltb_engine_set_world)
   TriFactor factor;
   bool factorized = false;
   double* ypad = nullptr;       // nb * 64
@@ -133,10 +135,12 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
   size_t free_b = 0, total_b = 0;
   ENG_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t nb = (size_t)(n + kTB - 1) / kTB;
-  const size_t need = (nb * (nb + 1) / 2 + nb + 2 * nb * kLook) * kTB * kTB * sizeof(double);
+  const size_t rows = e->rank < (int)nb ? (nb - 1 - e->rank) / e->world + 1 : 0;
+  const size_t mine = rows * (e->rank + 1) + (size_t)e->world * rows * (rows - 1) / 2;  // tiles
+  const size_t need = (mine + nb + (e->rank == 0 ? 2 * nb * kLook : 0)) * kTB * kTB * sizeof(double);
   if (need + (64u << 20) > free_b)
     return efail(LTB_CAPACITY, "set_factor: packed factor needs %zu bytes, %zu free", need, free_b);
-  ENG_CUDA(trsv_alloc(e->factor, n));
+  ENG_CUDA(trsv_alloc(e->factor, n, e->world, e->rank));
   cudaFree(e->ypad);
   e->ypad = nullptr;
   ENG_CUDA(cudaMalloc(&e->ypad, nb * kTB * sizeof(double)));
@@ -214,9 +218,41 @@ ltb_status fq_scratch_for(ltb_engine* e, cudaStream_t st, ltb_scratch** out) {
 
 extern "C" {
 
+ltb_status ltb_engine_set_world(ltb_engine* e, int world, int rank) {
+  if (!e) return efail(LTB_INVALID, "set_world: null engine");
+  if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+    return efail(LTB_INVALID, "set_world: world=%d rank=%d (1 <= world <= %d)", world, rank, kMaxRanks);
+  if (e->factorized) return efail(LTB_STATE, "set_world: must precede set_factor");
+  e->world = world;
+  e->rank = rank;
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_ipc_handle(ltb_engine* e, void* out) {
+  if (!e || !out) return efail(LTB_INVALID, "ipc_handle: null argument");
+  if (!e->factorized) return efail(LTB_STATE, "ipc_handle: set the factor first");
+  Guard gd(e->device);
+  cudaIpcMemHandle_t h;
+  ENG_CUDA(trsv_ipc_handle(e->factor, &h));
+  memcpy(out, &h, sizeof(h));
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_connect(ltb_engine* e, const void* handles) {
+  if (!e || !handles) return efail(LTB_INVALID, "connect: null argument");
+  if (!e->factorized) return efail(LTB_STATE, "connect: set the factor first");
+  Guard gd(e->device);
+  cudaIpcMemHandle_t h[kMaxRanks];
+  memcpy(h, handles, sizeof(cudaIpcMemHandle_t) * e->world);
+  ENG_CUDA(trsv_connect(e->factor, h));
+  return LTB_OK;
+}
+
 ltb_status ltb_engine_set_factor(ltb_engine* e, const double* L, int n, size_t ld, int ptr_kind) {
   if (!e || !L) return efail(LTB_INVALID, "set_factor: null argument");
   if (ld < (size_t)n) return efail(LTB_DIMENSION, "set_factor: ld < n");
+  if (e->world > 1)
+    return efail(LTB_STATE, "set_factor: a distributed factor is built per rank (set_factor_generated)");
   Guard gd(e->device);
   ltb_status st = factor_prepare(e, n);
   if (st != LTB_OK) return st;

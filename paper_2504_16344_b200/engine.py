@@ -27,15 +27,21 @@ class MapResult:
 class InferenceEngine:
     """Device-resident online engine: factor of K, G* plan, optional F_q plan."""
 
-    def __init__(self, plan_gstar, plan_fq=None, device=None):
+    def __init__(self, plan_gstar, plan_fq=None, device=None, world=1, rank=0, stream=None):
+        """``world`` > 1: distributed K^{-1} (one process per GPU, torch.distributed
+        initialised); the plans are then this rank's column shards and the
+        factor must be set with ``set_factor_generated`` (collective)."""
         self.plan_g = plan_gstar
         self.plan_fq = plan_fq
+        self.world, self.rank = int(world), int(rank)
         h = C.c_void_p()
         opts = _opts(device)
         check(_lib.load().ltb_engine_create(plan_gstar._h, plan_fq._h if plan_fq else None,
                                             C.byref(opts), C.byref(h)))
         self._h = h
-        self._scratch = MatvecPlan.Scratch(plan_gstar)
+        if self.world > 1:
+            check(_lib.load().ltb_engine_set_world(self._h, self.world, self.rank))
+        self._scratch = MatvecPlan.Scratch(plan_gstar, stream=stream)
         self.n_sensors = plan_gstar.rows_out()
         self.n_space = plan_gstar.n_cols()
         self.n_time = plan_gstar.n_time()
@@ -68,8 +74,21 @@ class InferenceEngine:
         Lf = np.asfortranarray(L)  # the ABI takes column-major (Eigen) storage
         check(_lib.load().ltb_engine_set_factor(self._h, C.c_void_p(Lf.ctypes.data), n, n, 0))
 
-    def set_factor_generated(self, seed):
-        check(_lib.load().ltb_engine_set_factor_generated(self._h, self.n_data(), seed))
+    def set_factor_generated(self, seed, group=None):
+        """Synthetic factor (oracle ``orc_gen_factor``) built on the device.
+        Distributed: every rank builds its block rows, then the ranks
+        exchange CUDA IPC handles of their receive buffers over
+        ``torch.distributed`` (collective)."""
+        L = _lib.load()
+        check(L.ltb_engine_set_factor_generated(self._h, self.n_data(), seed))
+        if self.world > 1:
+            import torch.distributed as dist
+            mine = (C.c_char * 64)()
+            check(L.ltb_engine_ipc_handle(self._h, mine))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(mine), group=group)
+            blob = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
+            check(L.ltb_engine_connect(self._h, blob))
 
     def solve_k_inplace(self, y, scratch=None):
         """bayes_engine.cpp:236-240: y <- K^{-1} y (numpy or CUDA tensor)."""

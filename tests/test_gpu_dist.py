@@ -1,0 +1,29 @@
+"""Multi-GPU online phase (distributed K^{-1} + sharded G* / F_q) against the
+oracle, through torchrun with one rank per visible GPU (skipped on a 1-GPU
+box; the single-GPU emulation in test_gpu_engine.py covers the algorithm)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_distributed_online_phase():
+    import torch
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", str(world), "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), os.path.join(HERE, "dist_online_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "PASS" in r.stdout
