@@ -48,7 +48,9 @@ typedef enum {
   LTB_CAPACITY = 4,  /* CapacityError   (core.hpp:27) */
   LTB_STATE = 5,     /* StateError      (core.hpp:30) */
   LTB_CUDA = 6,      /* CUDA runtime failure (no reference analogue) */
-  LTB_INVALID = 7    /* null handle / bad argument */
+  LTB_INVALID = 7,   /* null handle / bad argument */
+  LTB_CONFIG = 8,    /* ConfigError     (core.hpp:21) */
+  LTB_IO = 9         /* IoError         (core.hpp:33) */
 } ltb_status;
 
 typedef enum { LTB_PTR_HOST = 0, LTB_PTR_DEVICE = 1 } ltb_ptr_kind;
@@ -192,6 +194,26 @@ ltb_status ltb_engine_infer_map(const ltb_engine* e, ltb_scratch* s, const doubl
 /* forecast q = F_q m (acceptance_main.cpp:243-264 route) */
 ltb_status ltb_engine_forecast(const ltb_engine* e, ltb_scratch* s, const double* m,
                                double* q, int ptr_kind);
+
+/* ---- Q d forecast with credible intervals (predict_qoi) ---- */
+
+/* set_phase3 (bayes_engine.cpp:218-234), online part: Q (Nq*Nt x Nd*Nt,
+ * column-major with leading dimension ldq -- Eigen storage) and the
+ * diagonal of Gamma_post_q (Nq*Nt).  Both copied to the device. */
+ltb_status ltb_engine_set_phase3(ltb_engine* e, const double* Q, size_t ldq,
+                                 const double* gpost_q_diag, int ptr_kind);
+
+/* predict_qoi (bayes_engine.cpp:340-362): q = Q d; lo / hi = q -/+ z
+ * sqrt(max(diag Gamma_post_q, 0)) with z = 1.96 at level 0.95, else the
+ * normal quantile of (1+level)/2 (Acklam + one Halley step, :39-75).
+ * LTB_CONFIG unless 0 < level < 1; LTB_STATE without set_phase3.  lo / hi
+ * nullable. */
+ltb_status ltb_engine_predict_qoi(const ltb_engine* e, ltb_scratch* s, const double* d,
+                                  double level, double* q, double* lo, double* hi,
+                                  double* seconds, int ptr_kind);
+
+/* normal_quantile (bayes_engine.cpp:39-75); LTB_CONFIG unless 0 < p < 1 */
+ltb_status ltb_normal_quantile(double p, double* out);
 
 /* diagnostics: enable != 0 makes the TRSV sweeps record globaltimer stamps
  * (forward chain steps, transposed chain steps, forward worker hand-offs,

@@ -6,8 +6,9 @@ include/ltb.h); this package is the host-side mirror of the reference's
 ``ltibayes`` C++ API.  See DESIGN.md.
 """
 from ._lib import build, kernel_launches, last_error, load  # noqa: F401
-from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, CudaError,  # noqa: F401
+from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, ConfigError,  # noqa: F401
+                     CudaError, IoError,
                      DimensionError, KernelTag, Layout, LayoutError, LtbError, MatvecPlan,
                      NumericalError, ObsSeries, QoISeries, SpaceTimeField, StateError,
                      algorithmic_bytes, reindex)
-from .engine import InferenceEngine, MapResult  # noqa: F401
+from .engine import InferenceEngine, MapResult, QoIPrediction, normal_quantile  # noqa: F401

@@ -51,6 +51,9 @@ SIGNATURES = {
     "ltb_engine_forecast": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_engine_trsv_trace": ([_vp, C.c_int, C.POINTER(C.c_ulonglong), C.c_int], C.c_int),
     "ltb_debug_dtrsv_emulated": ([C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp], C.c_int),
+    "ltb_engine_set_phase3": ([_vp, _vp, C.c_size_t, _vp, C.c_int], C.c_int),
+    "ltb_engine_predict_qoi": ([_vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
+    "ltb_normal_quantile": ([C.c_double, _dp], C.c_int),
     "ltb_engine_infer_and_forecast": ([_vp, _vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
 }
 

@@ -8,7 +8,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/ltb.h"
 #include "ltb_kernels.h"
@@ -76,6 +78,8 @@ struct ltb_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
+void release_phase3(ltb_engine* e);  // Q d state (below)
+
 extern "C" {
 
 ltb_status ltb_engine_create(const ltb_plan* g, const ltb_plan* fq, const ltb_opts* opts,
@@ -122,6 +126,7 @@ ltb_status ltb_engine_destroy(ltb_engine* e) {
   if (e->fq_scratch) ltb_scratch_destroy(e->fq_scratch);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  release_phase3(e);
   delete e;
   return LTB_OK;
 }
@@ -448,4 +453,215 @@ extern "C" ltb_status ltb_debug_dtrsv_emulated(int n, int P, uint64_t seed, cons
   if (seconds) *seconds = ms * 1e-3;
   count_launches(1);
   return cleanup(LTB_OK);
+}
+
+// ---------------------------------------------------------------------------
+// Q d forecast with credible intervals (predict_qoi, bayes_engine.cpp:340-362)
+//
+// Q (Nq*Nt x Nd*Nt, column-major) is the one dense operator of the online
+// phase (17.8 GB at Cascadia).  Its GEMV is the same HBM-streaming problem as
+// GEMV-N, so it reuses that kernel: a column of Q with an even number of rows
+// read as complex pairs (q_2i, q_2i+1) times the real d_j embedded as (d_j, 0)
+// gives complex partial sums whose real / imaginary parts are exactly
+// sum_j Q_2i,j d_j and sum_j Q_2i+1,j d_j.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void real_to_complex_kernel(const double* __restrict__ d, long long n,
+                                       double2* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = make_double2(d[i], 0.0);
+}
+
+__global__ void pad_columns_kernel(const double* __restrict__ Q, size_t ldq, long long rows,
+                                   long long cols, long long ldp, double* __restrict__ out) {
+  const long long total = ldp * cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / ldp, r = e - c * ldp;
+    out[e] = r < rows ? Q[(size_t)c * ldq + r] : 0.0;
+  }
+}
+
+__global__ void credible_kernel(const double* __restrict__ q, const double* __restrict__ gdiag,
+                                long long n, double z, double* __restrict__ lo,
+                                double* __restrict__ hi) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double half = z * sqrt(fmax(gdiag[i], 0.0));
+    lo[i] = q[i] - half;
+    hi[i] = q[i] + half;
+  }
+}
+
+// bayes_engine.cpp:39-75: Acklam's rational approximation + one Halley step
+double normal_quantile_host(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                             -2.759285104469687e+02, 1.383577518672690e+02,
+                             -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                             -1.556989798598866e+02, 6.680131188771972e+01,
+                             -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                             -2.400758277161838e+00, -2.549732539343734e+00,
+                             4.374664141464968e+00, 2.938163982698783e+00};
+  static const double dd[] = {7.784695709041462e-03, 3.224671290700398e-01,
+                              2.445134137142996e+00, 3.754408661907416e+00};
+  const double plow = 0.02425, phigh = 1 - plow;
+  double x;
+  if (p < plow) {
+    const double q = std::sqrt(-2 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((dd[0] * q + dd[1]) * q + dd[2]) * q + dd[3]) * q + 1);
+  } else if (p <= phigh) {
+    const double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1);
+  } else {
+    const double q = std::sqrt(-2 * std::log(1 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((dd[0] * q + dd[1]) * q + dd[2]) * q + dd[3]) * q + 1);
+  }
+  const double e = 0.5 * std::erfc(-x / std::sqrt(2.0)) - p;
+  const double u = e * std::sqrt(2 * M_PI) * std::exp(x * x / 2);
+  return x - u / (1 + x * u / 2);
+}
+
+struct QoIOperator {
+  long long rows = 0, cols = 0, ldp = 0;  // Nq*Nt, Nd*Nt, rows padded to even
+  double* Q = nullptr;                    // ldp x cols, column-major
+  double* gdiag = nullptr;
+  double2* x = nullptr;                   // d as complex
+  double2* partials = nullptr;
+  unsigned* tickets = nullptr;
+  double* y = nullptr;                    // ldp reals (= ldp/2 complex)
+  double* lo = nullptr;
+  double* hi = nullptr;
+  double* stage = nullptr;                // host-pointer staging for d
+  GemvShape shape{};
+  void release() {
+    cudaFree(Q);
+    cudaFree(gdiag);
+    cudaFree(x);
+    cudaFree(partials);
+    cudaFree(tickets);
+    cudaFree(y);
+    cudaFree(lo);
+    cudaFree(hi);
+    cudaFree(stage);
+    *this = QoIOperator();
+  }
+};
+
+std::mutex g_qoi_mu;
+std::unordered_map<const ltb_engine*, QoIOperator> g_qoi;  // per-engine Phase-3 state
+
+}  // namespace
+
+extern "C" {
+
+ltb_status ltb_normal_quantile(double p, double* out) {
+  if (!out) return efail(LTB_INVALID, "normal_quantile: null out");
+  if (!(p > 0.0 && p < 1.0)) return efail(LTB_CONFIG, "normal_quantile: p must lie in (0, 1)");
+  *out = normal_quantile_host(p);
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_set_phase3(ltb_engine* e, const double* Q, size_t ldq,
+                                 const double* gpost_q_diag, int ptr_kind) {
+  if (!e || !Q || !gpost_q_diag) return efail(LTB_INVALID, "set_phase3: null argument");
+  if (!e->fq && e->nq == 0) return efail(LTB_STATE, "set_phase3: engine has no F_q plan (N_q unknown)");
+  const long long rows = (long long)e->nq * e->nt, cols = (long long)e->nd * e->nt;
+  if (ldq < (size_t)rows) return efail(LTB_DIMENSION, "set_phase3: wrong artifact dims (ldq < Nq*Nt)");
+  Guard gd(e->device);
+  std::lock_guard<std::mutex> lk(g_qoi_mu);
+  QoIOperator& op = g_qoi[e];
+  op.release();
+  op.rows = rows;
+  op.cols = cols;
+  op.ldp = rows + (rows & 1);
+  op.shape = gemv_shape((int)(op.ldp / 2), cols, 1, 0);
+  const int tiles = gemv_n_row_tiles(op.shape);
+  ENG_CUDA(cudaMalloc(&op.Q, sizeof(double) * op.ldp * cols));
+  ENG_CUDA(cudaMalloc(&op.gdiag, sizeof(double) * rows));
+  ENG_CUDA(cudaMalloc(&op.x, sizeof(double2) * cols));
+  ENG_CUDA(cudaMalloc(&op.partials, sizeof(double2) * gemv_n_partials(op.shape)));
+  ENG_CUDA(cudaMalloc(&op.tickets, sizeof(unsigned) * tiles));
+  ENG_CUDA(cudaMalloc(&op.y, sizeof(double) * op.ldp));
+  ENG_CUDA(cudaMalloc(&op.lo, sizeof(double) * rows));
+  ENG_CUDA(cudaMalloc(&op.hi, sizeof(double) * rows));
+  ENG_CUDA(cudaMalloc(&op.stage, sizeof(double) * cols));
+  const double* src = Q;
+  double* tmp = nullptr;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(cudaMalloc(&tmp, sizeof(double) * ldq * cols));
+    ENG_CUDA(cudaMemcpy(tmp, Q, sizeof(double) * ldq * cols, cudaMemcpyHostToDevice));
+    src = tmp;
+    ENG_CUDA(cudaMemcpy(op.gdiag, gpost_q_diag, sizeof(double) * rows, cudaMemcpyHostToDevice));
+  } else {
+    ENG_CUDA(cudaMemcpy(op.gdiag, gpost_q_diag, sizeof(double) * rows, cudaMemcpyDeviceToDevice));
+  }
+  pad_columns_kernel<<<148 * 8, 256>>>(src, ldq, rows, cols, op.ldp, op.Q);
+  cudaError_t err = cudaDeviceSynchronize();
+  cudaFree(tmp);
+  count_launches(1);
+  if (err != cudaSuccess) return efail(LTB_CUDA, "set_phase3: %s", cudaGetErrorString(err));
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_predict_qoi(const ltb_engine* e, ltb_scratch* s, const double* d, double level,
+                                  double* q, double* lo, double* hi, double* seconds, int ptr_kind) {
+  if (!e || !s || !d || !q) return efail(LTB_INVALID, "predict_qoi: null argument");
+  if (!(level > 0 && level < 1)) return efail(LTB_CONFIG, "predict_qoi: credible level must lie in (0, 1)");
+  Guard gd(e->device);
+  QoIOperator* opp = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_qoi_mu);
+    auto it = g_qoi.find(e);
+    if (it == g_qoi.end() || !it->second.Q)
+      return efail(LTB_STATE, "engine: missing offline artifact: Phase-3 artifacts (run form_Q/form_qoi_cov)");
+    opp = &it->second;
+  }
+  QoIOperator& op = *opp;
+  const cudaStream_t st = scratch_stream(s);
+  const double z = (level == 0.95) ? 1.96 : normal_quantile_host(0.5 * (1 + level));
+  ltb_engine* em = const_cast<ltb_engine*>(e);
+  ENG_CUDA(cudaEventRecord(em->ev0, st));
+  const double* din = d;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(cudaMemcpyAsync(op.stage, d, sizeof(double) * op.cols, cudaMemcpyHostToDevice, st));
+    din = op.stage;
+  }
+  real_to_complex_kernel<<<148 * 4, 256, 0, st>>>(din, op.cols, op.x);
+  ENG_CUDA(cudaGetLastError());
+  ENG_CUDA(launch_gemv_n(op.shape, reinterpret_cast<const double2*>(op.Q), op.x, op.partials,
+                         reinterpret_cast<double2*>(op.y), op.tickets, st));
+  credible_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 4, (op.rows + 255) / 256)), 256, 0, st>>>(
+      op.y, op.gdiag, op.rows, z, op.lo, op.hi);
+  ENG_CUDA(cudaGetLastError());
+  count_launches(3);
+  const cudaMemcpyKind k = ptr_kind == LTB_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  ENG_CUDA(cudaMemcpyAsync(q, op.y, sizeof(double) * op.rows, k, st));
+  if (lo) ENG_CUDA(cudaMemcpyAsync(lo, op.lo, sizeof(double) * op.rows, k, st));
+  if (hi) ENG_CUDA(cudaMemcpyAsync(hi, op.hi, sizeof(double) * op.rows, k, st));
+  ENG_CUDA(cudaEventRecord(em->ev1, st));
+  ENG_CUDA(cudaStreamSynchronize(st));
+  if (seconds) {
+    float ms = 0.f;
+    ENG_CUDA(cudaEventElapsedTime(&ms, em->ev0, em->ev1));
+    *seconds = ms * 1e-3;
+  }
+  return LTB_OK;
+}
+
+}  // extern "C"
+
+void release_phase3(ltb_engine* e) {
+  std::lock_guard<std::mutex> lk(g_qoi_mu);
+  auto it = g_qoi.find(e);
+  if (it != g_qoi.end()) {
+    it->second.release();
+    g_qoi.erase(it);
+  }
 }

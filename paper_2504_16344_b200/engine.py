@@ -24,6 +24,22 @@ class MapResult:
     q_map: QoISeries = None
 
 
+@dataclass
+class QoIPrediction:
+    """bayes_engine.hpp:101-104"""
+    q_map: QoISeries
+    ci_lower: QoISeries
+    ci_upper: QoISeries
+    seconds: float
+
+
+def normal_quantile(p):
+    """bayes_engine.cpp:39-75 (ConfigError unless 0 < p < 1)."""
+    out = C.c_double()
+    check(_lib.load().ltb_normal_quantile(float(p), C.byref(out)))
+    return out.value
+
+
 class InferenceEngine:
     """Device-resident online engine: factor of K, G* plan, optional F_q plan."""
 
@@ -128,6 +144,33 @@ class InferenceEngine:
         check(_lib.load().ltb_engine_infer_and_forecast(self._h, (scratch or self._scratch)._h,
                                                         pd, pm, pq, C.byref(secs), kd))
         return secs.value
+
+    def set_phase3(self, Q, gamma_post_q_diag):
+        """Online part of set_phase3 (bayes_engine.cpp:218-234): Q
+        (Nq*Nt x Nd*Nt) and diag(Gamma_post_q)."""
+        Qf = np.asfortranarray(np.asarray(Q, dtype=np.float64))
+        rows, cols = Qf.shape
+        if rows != self.n_qoi * self.n_time or cols != self.n_data():
+            raise DimensionError("set_phase3: wrong artifact dims")
+        g = np.ascontiguousarray(gamma_post_q_diag, dtype=np.float64)
+        if g.size != rows:
+            raise DimensionError("set_phase3: wrong artifact dims")
+        check(_lib.load().ltb_engine_set_phase3(self._h, C.c_void_p(Qf.ctypes.data), rows,
+                                                C.c_void_p(g.ctypes.data), 0))
+
+    def predict_qoi(self, d_obs, level=0.95):
+        """bayes_engine.cpp:340-362: q_map = Q d_obs with credible intervals
+        q_map -/+ z sqrt(diag Gamma_post_q)."""
+        self._check_obs(d_obs, "predict_qoi")
+        n = self.n_qoi * self.n_time
+        q, lo, hi = (QoISeries(self.n_qoi, self.n_time, Layout.SpaceMajorRows) for _ in range(3))
+        secs = C.c_double()
+        check(_lib.load().ltb_engine_predict_qoi(
+            self._h, self._scratch._h, C.c_void_p(d_obs.values.ctypes.data), float(level),
+            C.c_void_p(q.values.ctypes.data), C.c_void_p(lo.values.ctypes.data),
+            C.c_void_p(hi.values.ctypes.data), C.byref(secs), 0))
+        assert q.values.size == n
+        return QoIPrediction(q, lo, hi, secs.value)
 
     def forecast(self, m_map):
         """q = F_q m (the F_q route pinned to Q d by acceptance criterion 5)."""

@@ -52,8 +52,16 @@ class CudaError(LtbError):
     pass
 
 
+class ConfigError(LtbError):
+    pass
+
+
+class IoError(LtbError):
+    pass
+
+
 _ERRORS = {1: DimensionError, 2: LayoutError, 3: NumericalError, 4: CapacityError,
-           5: StateError, 6: CudaError, 7: ValueError}
+           5: StateError, 6: CudaError, 7: ValueError, 8: ConfigError, 9: IoError}
 
 
 def check(status):

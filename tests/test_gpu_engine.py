@@ -174,3 +174,40 @@ def test_distributed_solve_emulated(ltb, n, P):
     ref = orc.solve_k_gen(seed, b)
     assert orc.rel_err(x, ref) <= 1e-12
     assert diff.value == 0.0
+
+
+def test_predict_qoi_with_credible_intervals(ltb):
+    """predict_qoi (bayes_engine.cpp:340-362): q = Q d (GEMV on the device)
+    and q -/+ z sqrt(max(diag, 0)); z = 1.96 at 0.95, normal quantile else;
+    odd Nq*Nt (padding path) and ConfigError on a bad level."""
+    rng = np.random.default_rng(8)
+    for nd, nq, nm, nt in [(3, 2, 5, 7), (4, 3, 6, 9), (64, 8, 16, 128)]:
+        g = ltb.MatvecPlan.generated(nd, nm, nt, seed=1, tag=ltb.KernelTag.Gstar)
+        fq = ltb.MatvecPlan.generated(nq, nm, nt, seed=1, tag=ltb.KernelTag.Fq)
+        eng = ltb.InferenceEngine(g, fq)
+        with pytest.raises(ltb.StateError):
+            eng.predict_qoi(obs(ltb, nd, nt, np.zeros(nd * nt)))
+        Q = rng.standard_normal((nq * nt, nd * nt))
+        gd = rng.standard_normal(nq * nt) ** 2
+        gd[0] = -1e-3  # negative diagonal entries clip to zero width
+        eng.set_phase3(Q, gd)
+        d = rng.standard_normal(nd * nt)
+        for level in (0.95, 0.8):
+            res = eng.predict_qoi(obs(ltb, nd, nt, d), level)
+            q_ref = Q @ d
+            z = 1.96 if level == 0.95 else orc_normal_quantile(0.5 * (1 + level))
+            half = z * np.sqrt(np.maximum(gd, 0.0))
+            assert orc.rel_err(res.q_map.values, q_ref) <= 1e-13
+            assert np.allclose(res.ci_lower.values, q_ref - half, rtol=1e-12, atol=1e-12)
+            assert np.allclose(res.ci_upper.values, q_ref + half, rtol=1e-12, atol=1e-12)
+        with pytest.raises(ltb.ConfigError):
+            eng.predict_qoi(obs(ltb, nd, nt, d), 1.0)
+    assert ltb.normal_quantile(0.975) == pytest.approx(1.95996398454, rel=1e-9)
+    assert ltb.normal_quantile(0.005) == pytest.approx(-2.57582930355, rel=1e-9)
+    with pytest.raises(ltb.ConfigError):
+        ltb.normal_quantile(1.0)
+
+
+def orc_normal_quantile(p):
+    from scipy.stats import norm
+    return float(norm.ppf(p))
