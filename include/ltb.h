@@ -92,6 +92,28 @@ ltb_status ltb_plan_create_generated(int rows, int cols, int nt, int tag, uint64
                                      uint64_t stream, long long nm_total, long long c0,
                                      const ltb_opts* opts, ltb_plan** out);
 
+/* G* plans built on the device from F: the kernel is premultiplied by the
+ * prior covariance Gamma_x = A_x^{-2}, A_x = delta I - gamma L (Neumann
+ * Laplacian on the n_cols nodes, spacing h_x), along its column axis before
+ * the transform -- PriorOp::premultiply_kernel (prior.cpp:108-134; A_x
+ * prior.cpp:9-39).  Tag F -> Gstar, Fq -> Gqstar; LTB_CONFIG for an already
+ * premultiplied tag or invalid prior parameters.  Built slab by slab (<= 16
+ * kernel rows at a time), so the time-domain kernel is never resident. */
+ltb_status ltb_plan_create_premultiplied(const double* kernel_rck, int rows, int cols, int nt,
+                                         int tag, int ptr_kind, double h_x, double gamma,
+                                         double delta, const ltb_opts* opts, ltb_plan** out);
+ltb_status ltb_plan_create_generated_premultiplied(int rows, int cols, int nt, int tag,
+                                                   uint64_t seed, uint64_t stream, double h_x,
+                                                   double gamma, double delta,
+                                                   const ltb_opts* opts, ltb_plan** out);
+
+/* Plan from a BTPZ1 kernel archive written by the reference (io.cpp:71-100:
+ * "BTPZ1", u64 rows, cols, N_t, tag, [row][col][lag] doubles), streamed
+ * slab by slab to the device (LTB_IO on a missing / bad / truncated file).
+ * prior3 = {h_x, gamma, delta} premultiplies on the way (NULL: as stored). */
+ltb_status ltb_plan_load_btpz(const char* path, const double* prior3, const ltb_opts* opts,
+                              ltb_plan** out);
+
 ltb_status ltb_plan_destroy(ltb_plan* plan);
 
 /* rows_out / n_cols / n_time / padded_len / n_freq / tag (fft_matvec.hpp:38-43) */

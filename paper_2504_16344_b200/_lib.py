@@ -22,6 +22,12 @@ SIGNATURES = {
     "ltb_plan_create": ([_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.POINTER(_vp)], C.c_int),
     "ltb_plan_create_generated": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                                    C.c_longlong, C.c_longlong, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_plan_create_premultiplied": ([_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                       C.c_double, C.c_double, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_plan_create_generated_premultiplied": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                                 C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                                 _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_plan_load_btpz": ([C.c_char_p, _dp, _vp, C.POINTER(_vp)], C.c_int),
     "ltb_plan_destroy": ([_vp], C.c_int),
     "ltb_plan_dims": ([_vp] + [C.POINTER(C.c_int)] * 6, C.c_int),
     "ltb_plan_bytes": ([_vp, C.POINTER(C.c_size_t)], C.c_int),

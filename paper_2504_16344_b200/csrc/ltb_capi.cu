@@ -651,3 +651,267 @@ extern "C" ltb_status ltb_dense_apply(const double* kernel, int rows, int cols, 
   if (e != cudaSuccess) return done(fail(LTB_CUDA, "dense_apply: %s", cudaGetErrorString(e)));
   return done(LTB_OK);
 }
+
+// ---------------------------------------------------------------------------
+// Device plan build from kernel slabs: the prior premultiply that turns F
+// into G* (prior.cpp:108-134) and the BTPZ1 kernel-archive loader
+// (io.cpp:71-100).  Kernel rows [r0, r0+R) are one contiguous slab
+// [R][cols][nt] of the kernel tensor (in the archive too), so plans of any
+// size are built slab by slab without holding the time-domain kernel.
+// ---------------------------------------------------------------------------
+namespace {
+
+// Cholesky of A_x = delta I - gamma L, L the Neumann Laplacian
+// (prior.cpp:9-39); SPD tridiagonal: diagonal ldiag, sub-diagonal lsub
+ltb_status prior_factor(int n, double h_x, double gamma, double delta, std::vector<double>& ldiag,
+                        std::vector<double>& lsub) {
+  if (n < 1) return fail(LTB_CONFIG, "prior: n_space must be >= 1");
+  if (!(h_x > 0)) return fail(LTB_CONFIG, "prior: h_x must be positive");
+  if (!(delta > 0)) return fail(LTB_CONFIG, "prior: delta must be positive");
+  if (gamma < 0) return fail(LTB_CONFIG, "prior: gamma must be >= 0");
+  const double w = gamma / (h_x * h_x);
+  ldiag.assign(n, 0.0);
+  lsub.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double diag = delta;
+    if (i > 0) diag += w;
+    if (i + 1 < n) diag += w;
+    if (i > 0) {
+      lsub[i] = -w / ldiag[i - 1];
+      diag -= lsub[i] * lsub[i];
+    }
+    if (!(diag > 0)) return fail(LTB_NUMERICAL, "prior: factorization of A_x failed");
+    ldiag[i] = std::sqrt(diag);
+  }
+  return LTB_OK;
+}
+
+// Gamma_x = A_x^{-2} applied along the column (space) axis of every
+// (row, lag) line of a slab [R][nm][nt]: thread per line, two forward /
+// backward substitution pairs; consecutive threads are consecutive lags, so
+// every step of the recurrence is one coalesced row of the slab.
+__global__ void prior_premultiply_kernel(double* __restrict__ slab, int R, int nm, int nt,
+                                         const double* __restrict__ ldiag,
+                                         const double* __restrict__ lsub) {
+  const long long lines = (long long)R * nt;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < lines;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long rr = t / nt, k = t - rr * nt;
+    double* x = slab + rr * (long long)nm * nt + k;
+    for (int pass = 0; pass < 2; ++pass) {
+      double prev = 0.0;
+      for (int i = 0; i < nm; ++i) {
+        double v = x[(size_t)i * nt];
+        if (i > 0) v -= lsub[i] * prev;
+        prev = v / ldiag[i];
+        x[(size_t)i * nt] = prev;
+      }
+      double next = 0.0;
+      for (int i = nm - 1; i >= 0; --i) {
+        double v = x[(size_t)i * nt];
+        if (i + 1 < nm) v -= lsub[i + 1] * next;
+        next = v / ldiag[i];
+        x[(size_t)i * nt] = next;
+      }
+    }
+  }
+}
+
+__global__ void count_nonfinite_slab(const double* x, long long n, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) ++local;
+  if (local) atomicAdd(bad, local);
+}
+
+// F-hat columns of kernel rows [r0, r0+R) from a device slab [R][cols][nt]
+cudaError_t slab_to_fhat(ltb_plan* p, const double* slab, int r0, int R, cudaStream_t st) {
+  RfftSrc src{slab, 0, R, (long long)p->cols, 0};
+  src.oP = R;           // logical row g = c R + rr ...
+  src.oQ = p->rows;     // ... lands in F-hat column c rows + r0 + rr
+  src.o0 = r0;
+  return launch_rfft_rows(p->fft, src, p->nt, (long long)R * p->cols, p->fhat,
+                          (long long)p->rows * p->cols, st);
+}
+
+struct PriorDev {
+  double* ldiag = nullptr;
+  double* lsub = nullptr;
+  ~PriorDev() {
+    cudaFree(ldiag);
+    cudaFree(lsub);
+  }
+};
+
+// Source of kernel slabs: host tensor, device tensor, generator, or archive.
+struct SlabSource {
+  int kind = 0;  // 0 host, 1 device, 2 generated, 3 file
+  const double* ptr = nullptr;
+  uint64_t key = 0;
+  FILE* fh = nullptr;
+};
+
+// Build p->fhat slab by slab, optionally premultiplying by Gamma_x first.
+ltb_status build_plan_slabs(ltb_plan* p, const SlabSource& src, const PriorDev* prior) {
+  const size_t row_elems = (size_t)p->cols * p->nt;
+  int R = (int)std::max<size_t>(1, std::min<size_t>(16, (size_t)(512u << 20) / (row_elems * 8)));
+  R = std::min(R, p->rows);
+  double* slab = nullptr;
+  unsigned long long* bad = nullptr;
+  std::vector<double> host;
+  auto done = [&](ltb_status s) {
+    cudaFree(slab);
+    cudaFree(bad);
+    return s;
+  };
+  if (cudaMalloc(&slab, sizeof(double) * row_elems * R) != cudaSuccess ||
+      cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess)
+    return done(fail(LTB_CUDA, "plan build: slab alloc failed"));
+  cudaMemset(bad, 0, sizeof(unsigned long long));
+  if (src.kind == 3) host.resize(row_elems * R);
+  for (int r0 = 0; r0 < p->rows; r0 += R) {
+    const int rr = std::min(R, p->rows - r0);
+    const size_t n = row_elems * rr;
+    cudaError_t e = cudaSuccess;
+    if (src.kind == 0) {
+      e = cudaMemcpy(slab, src.ptr + (size_t)r0 * row_elems, sizeof(double) * n, cudaMemcpyHostToDevice);
+    } else if (src.kind == 1) {
+      e = cudaMemcpy(slab, src.ptr + (size_t)r0 * row_elems, sizeof(double) * n, cudaMemcpyDeviceToDevice);
+    } else if (src.kind == 2) {
+      e = launch_gen_fill(src.key, (uint64_t)r0 * row_elems, (long long)n, slab, 0);
+      g_launches += 1;
+    } else {
+      if (fread(host.data(), sizeof(double), n, src.fh) != n)
+        return done(fail(LTB_IO, "truncated archive while reading kernel data"));
+      e = cudaMemcpy(slab, host.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) return done(fail(LTB_CUDA, "plan build: %s", cudaGetErrorString(e)));
+    if (src.kind != 2) {  // core.cpp:73-77: reject non-finite kernel entries
+      count_nonfinite_slab<<<148 * 4, 256>>>(slab, (long long)n, bad);
+      g_launches += 1;
+    }
+    if (prior) {
+      const long long lines = (long long)rr * p->nt;
+      prior_premultiply_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 16, (lines + 127) / 128)), 128>>>(
+          slab, rr, p->cols, p->nt, prior->ldiag, prior->lsub);
+      g_launches += 1;
+    }
+    e = slab_to_fhat(p, slab, r0, rr, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return done(fail(LTB_CUDA, "plan build: %s", cudaGetErrorString(e)));
+    g_launches += 1;
+  }
+  unsigned long long hb = 0;
+  cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+  if (hb) return done(fail(LTB_NUMERICAL, "MatvecPlan: non-finite kernel entry"));
+  return done(LTB_OK);
+}
+
+ltb_status make_prior(int nm, double h_x, double gamma, double delta, PriorDev& d) {
+  std::vector<double> ld, ls;
+  ltb_status st = prior_factor(nm, h_x, gamma, delta, ld, ls);
+  if (st != LTB_OK) return st;
+  LTB_CUDA_TRY(cudaMalloc(&d.ldiag, sizeof(double) * nm));
+  LTB_CUDA_TRY(cudaMalloc(&d.lsub, sizeof(double) * nm));
+  LTB_CUDA_TRY(cudaMemcpy(d.ldiag, ld.data(), sizeof(double) * nm, cudaMemcpyHostToDevice));
+  LTB_CUDA_TRY(cudaMemcpy(d.lsub, ls.data(), sizeof(double) * nm, cudaMemcpyHostToDevice));
+  return LTB_OK;
+}
+
+// premultiply_kernel tag rule (prior.cpp:114-120)
+ltb_status premultiplied_tag(int tag, int* out) {
+  if (tag == LTB_TAG_F) *out = LTB_TAG_GSTAR;
+  else if (tag == LTB_TAG_FQ) *out = LTB_TAG_GQSTAR;
+  else return fail(LTB_CONFIG, "premultiply_kernel: kernel already premultiplied");
+  return LTB_OK;
+}
+
+ltb_status plan_from_source(int rows, int cols, int nt, int tag, const SlabSource& src,
+                            const double* prior3, const ltb_opts* opts, ltb_plan** out) {
+  *out = nullptr;
+  int ptag = tag;
+  if (prior3) {
+    ltb_status st = premultiplied_tag(tag, &ptag);
+    if (st != LTB_OK) return st;
+  }
+  ltb_plan* p = new ltb_plan();
+  ltb_status st = plan_init(p, rows, cols, nt, ptag, opts);
+  if (st != LTB_OK) {
+    plan_free(p);
+    return st;
+  }
+  DeviceGuard g(p->device);
+  PriorDev prior;
+  if (prior3 && (st = make_prior(cols, prior3[0], prior3[1], prior3[2], prior)) != LTB_OK) {
+    plan_free(p);
+    return st;
+  }
+  st = build_plan_slabs(p, src, prior3 ? &prior : nullptr);
+  if (st != LTB_OK) {
+    plan_free(p);
+    return st;
+  }
+  *out = p;
+  return LTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ltb_status ltb_plan_create_premultiplied(const double* kernel, int rows, int cols, int nt, int tag,
+                                         int ptr_kind, double h_x, double gamma, double delta,
+                                         const ltb_opts* opts, ltb_plan** out) {
+  if (!out || !kernel) return fail(LTB_INVALID, "plan_create_premultiplied: null argument");
+  if (rows < 1 || cols < 1 || nt < 1)
+    return fail(LTB_DIMENSION, "premultiply_kernel: kernel tensor size does not match dims");
+  SlabSource src;
+  src.kind = ptr_kind == LTB_PTR_DEVICE ? 1 : 0;
+  src.ptr = kernel;
+  const double prior[3] = {h_x, gamma, delta};
+  return plan_from_source(rows, cols, nt, tag, src, prior, opts, out);
+}
+
+ltb_status ltb_plan_create_generated_premultiplied(int rows, int cols, int nt, int tag,
+                                                   uint64_t seed, uint64_t stream, double h_x,
+                                                   double gamma, double delta, const ltb_opts* opts,
+                                                   ltb_plan** out) {
+  if (!out) return fail(LTB_INVALID, "plan_create_generated_premultiplied: null out");
+  SlabSource src;
+  src.kind = 2;
+  src.key = gen_key(seed, stream);
+  const double prior[3] = {h_x, gamma, delta};
+  return plan_from_source(rows, cols, nt, tag, src, prior, opts, out);
+}
+
+// BTPZ1 (io.cpp:71-100): "BTPZ1", u64 rows, cols, N_t, tag, then the
+// [row][col][lag] doubles (little endian)
+ltb_status ltb_plan_load_btpz(const char* path, const double* prior3, const ltb_opts* opts,
+                              ltb_plan** out) {
+  if (!out || !path) return fail(LTB_INVALID, "plan_load_btpz: null argument");
+  *out = nullptr;
+  FILE* fh = fopen(path, "rb");
+  if (!fh) return fail(LTB_IO, "cannot open kernel archive %s", path);
+  char magic[5];
+  uint64_t hdr[4];
+  ltb_status st = LTB_OK;
+  if (fread(magic, 1, 5, fh) != 5 || memcmp(magic, "BTPZ1", 5) != 0) {
+    st = fail(LTB_IO, "bad magic in %s (expected BTPZ1)", path);
+  } else if (fread(hdr, sizeof(uint64_t), 4, fh) != 4) {
+    st = fail(LTB_IO, "truncated archive while reading header of %s", path);
+  } else if (hdr[0] == 0 || hdr[1] == 0 || hdr[2] == 0 || hdr[3] > 3 ||
+             hdr[0] * hdr[1] * hdr[2] > (1ull << 40) || hdr[0] > INT32_MAX || hdr[1] > INT32_MAX ||
+             hdr[2] > INT32_MAX) {
+    st = fail(LTB_IO, "implausible kernel header in %s", path);
+  } else {
+    SlabSource src;
+    src.kind = 3;
+    src.fh = fh;
+    st = plan_from_source((int)hdr[0], (int)hdr[1], (int)hdr[2], (int)hdr[3], src, prior3, opts, out);
+  }
+  fclose(fh);
+  return st;
+}
+
+}  // extern "C"

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(kFftThreads)
       const double dx = zk.x - zn.x, dy = zk.y + zn.y;
       v = make_double2(0.5 * dy, -0.5 * dx);
     }
-    out[(long long)k * ld + g] = v;
+    const long long col = src.oP ? (g / src.oP) * src.oQ + g % src.oP + src.o0 : g;
+    out[(long long)k * ld + col] = v;
   }
 }
 

@@ -18,6 +18,9 @@ struct RfftSrc {
   long long Q;
   long long c0;
   int bulk = 0;  // set by the launcher: contiguous, 16-byte aligned rows
+  // output column of logical row g: (g / oP) * oQ + g % oP + o0 (oP = 0: g);
+  // lets a slab of kernel rows land in its F-hat columns [f][c][r0 + rr]
+  long long oP = 0, oQ = 0, o0 = 0;
 };
 
 // Forward: rows [0, nrows) of real length nt, zero padded to N = 2 nt,

@@ -257,6 +257,50 @@ class MatvecPlan:
         self._dims()
         return self
 
+    @classmethod
+    def premultiplied(cls, kernel, prior, device=None, unit_cols=0):
+        """G* plan from an F kernel: PriorOp::premultiply_kernel
+        (prior.cpp:108-134) on the device, then the transform.
+        ``prior`` = (h_x, gamma, delta) of A_x = delta I - gamma L."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        opts = _opts(device, unit_cols)
+        hx, gamma, delta = (float(v) for v in prior)
+        check(_lib.load().ltb_plan_create_premultiplied(
+            C.c_void_p(kernel.data.ctypes.data), kernel.rows_out, kernel.n_cols, kernel.n_time,
+            int(kernel.tag), PTR_HOST, hx, gamma, delta, C.byref(opts), C.byref(h)))
+        self._h = h
+        self._dims()
+        return self
+
+    @classmethod
+    def generated_premultiplied(cls, rows, cols, nt, seed, prior, tag=KernelTag.F, stream=None,
+                                device=None, unit_cols=0):
+        """G* plan of the device-generated F kernel (all columns)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        opts = _opts(device, unit_cols)
+        stream = int(tag) + 1 if stream is None else stream
+        hx, gamma, delta = (float(v) for v in prior)
+        check(_lib.load().ltb_plan_create_generated_premultiplied(
+            rows, cols, nt, int(tag), seed, stream, hx, gamma, delta, C.byref(opts), C.byref(h)))
+        self._h = h
+        self._dims()
+        return self
+
+    @classmethod
+    def load(cls, path, prior=None, device=None, unit_cols=0):
+        """Plan from a BTPZ1 kernel archive (io.cpp:71-100), optionally
+        premultiplied by the prior on the way."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        opts = _opts(device, unit_cols)
+        p3 = (C.c_double * 3)(*[float(v) for v in prior]) if prior is not None else None
+        check(_lib.load().ltb_plan_load_btpz(str(path).encode(), p3, C.byref(opts), C.byref(h)))
+        self._h = h
+        self._dims()
+        return self
+
     def _dims(self):
         v = [C.c_int() for _ in range(6)]
         check(_lib.load().ltb_plan_dims(self._h, *[C.byref(x) for x in v]))

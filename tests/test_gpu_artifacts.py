@@ -1,0 +1,99 @@
+"""Device plan build from time-domain kernels with the prior premultiply
+(G* = Gamma_prior F*, prior.cpp:108-134) and the BTPZ1 kernel-archive
+loader (io.cpp:71-100), against the oracle."""
+import struct
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ltb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_16344_b200 as ltb
+    ltb.load()
+    return ltb
+
+
+def write_btpz(path, k, tag=0):
+    """io.cpp:71-82 byte layout."""
+    with open(path, "wb") as fh:
+        fh.write(b"BTPZ1")
+        fh.write(struct.pack("<4Q", k.shape[0], k.shape[1], k.shape[2], tag))
+        fh.write(np.ascontiguousarray(k, dtype="<f8").tobytes())
+
+
+@pytest.mark.parametrize("rows,cols,nt,prior", [(3, 12, 5, (1.0, 2.0, 1.0)), (20, 300, 24, (1000.0, 16e6, 1.0)),
+                                                (40, 64, 9, (0.5, 0.0, 3.0))])
+def test_premultiplied_plan_vs_oracle(ltb, rows, cols, nt, prior):
+    rng = np.random.default_rng(rows + cols)
+    f = rng.standard_normal((rows, cols, nt))
+    g = orc.prior_premultiply(f, *prior)
+    gp = ltb.MatvecPlan.premultiplied(ltb.BlockToeplitzKernel(rows, cols, nt, tag=ltb.KernelTag.F, data=f), prior)
+    assert gp.tag() == ltb.KernelTag.Gstar
+    ref = orc.OraclePlan(g)
+    assert orc.rel_err(gp.kernel_hat().view(np.float64), ref.khat().view(np.float64)) <= 1e-12
+    d = rng.standard_normal(rows * nt)
+    s = ltb.MatvecPlan.Scratch(gp)
+    out = np.empty(cols * nt)
+    gp.apply_adjoint_raw(d, out, s)
+    assert orc.rel_err(out, ref.apply_adjoint(d)) <= 1e-12
+
+
+def test_generated_premultiplied_vs_oracle(ltb):
+    rows, cols, nt, seed, prior = 6, 40, 16, 77, (1.0, 2.0, 1.0)
+    gp = ltb.MatvecPlan.generated_premultiplied(rows, cols, nt, seed, prior, tag=ltb.KernelTag.Fq)
+    assert gp.tag() == ltb.KernelTag.Gqstar
+    g = orc.prior_premultiply(orc.gen_kernel(seed, rows, cols, nt, stream=2), *prior)
+    assert orc.rel_err(gp.kernel_hat().view(np.float64), orc.OraclePlan(g).khat().view(np.float64)) <= 1e-12
+
+
+def test_premultiply_contract(ltb):
+    k = ltb.BlockToeplitzKernel(2, 5, 4, tag=ltb.KernelTag.Gstar, data=np.ones((2, 5, 4)))
+    with pytest.raises(ltb.ConfigError):
+        ltb.MatvecPlan.premultiplied(k, (1.0, 1.0, 1.0))
+    k = ltb.BlockToeplitzKernel(2, 5, 4, data=np.ones((2, 5, 4)))
+    for bad in [(0.0, 1.0, 1.0), (1.0, -1.0, 1.0), (1.0, 1.0, 0.0)]:
+        with pytest.raises(ltb.ConfigError):
+            ltb.MatvecPlan.premultiplied(k, bad)
+
+
+def test_btpz_loader_roundtrip(ltb, tmp_path):
+    rng = np.random.default_rng(4)
+    k = rng.standard_normal((7, 33, 11))
+    path = tmp_path / "f.btpz"
+    write_btpz(path, k, tag=1)
+    lp = ltb.MatvecPlan.load(path)
+    assert lp.tag() == ltb.KernelTag.Fq and (lp.rows_out(), lp.n_cols(), lp.n_time()) == (7, 33, 11)
+    ref = ltb.MatvecPlan(ltb.BlockToeplitzKernel(7, 33, 11, tag=1, data=k))
+    assert np.array_equal(lp.kernel_hat(), ref.kernel_hat())  # same bits in, same FFT
+    lg = ltb.MatvecPlan.load(path, prior=(1.0, 2.0, 1.0))
+    assert lg.tag() == ltb.KernelTag.Gqstar
+    g = orc.prior_premultiply(k, 1.0, 2.0, 1.0)
+    assert orc.rel_err(lg.kernel_hat().view(np.float64), orc.OraclePlan(g).khat().view(np.float64)) <= 1e-12
+
+
+def test_btpz_loader_errors(ltb, tmp_path):
+    bad = tmp_path / "bad.btpz"
+    bad.write_bytes(b"XXXXX" + b"\0" * 40)
+    with pytest.raises(ltb.IoError):
+        ltb.MatvecPlan.load(bad)
+    with pytest.raises(ltb.IoError):
+        ltb.MatvecPlan.load(tmp_path / "missing.btpz")
+    k = np.ones((2, 3, 4))
+    trunc = tmp_path / "trunc.btpz"
+    write_btpz(trunc, k)
+    trunc.write_bytes(trunc.read_bytes()[:-8])
+    with pytest.raises(ltb.IoError):
+        ltb.MatvecPlan.load(trunc)
+    nan = tmp_path / "nan.btpz"
+    k[1, 2, 3] = np.nan
+    write_btpz(nan, k)
+    with pytest.raises(ltb.NumericalError):
+        ltb.MatvecPlan.load(nan)
