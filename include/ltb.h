@@ -237,6 +237,17 @@ ltb_status ltb_engine_predict_qoi(const ltb_engine* e, ltb_scratch* s, const dou
 /* normal_quantile (bayes_engine.cpp:39-75); LTB_CONFIG unless 0 < p < 1 */
 ltb_status ltb_normal_quantile(double p, double* out);
 
+/* ---- artifact loaders (io.cpp) ---- */
+/* FNV-1a 64-bit hash of a file (io.cpp:198-219), for manifest checks */
+ltb_status ltb_fnv1a64_file(const char* path, uint64_t* out);
+/* set_factor from a DNSM1 archive (io.cpp:102-136; "DNSM1", u64 rows, cols,
+ * symmetric flag, row-major doubles), streamed in 64-row panels straight
+ * into the packed tiles; the strict upper part is ignored (chol.dnsm may
+ * hold K there, bayes_engine.cpp:180-193).  Single-GPU engines only. */
+ltb_status ltb_engine_load_factor_dnsm(ltb_engine* e, const char* path);
+/* set_phase3 from Q.dnsm and Gamma_post_q.dnsm (workflow.cpp:325-330) */
+ltb_status ltb_engine_load_phase3_dnsm(ltb_engine* e, const char* q_path, const char* gpost_path);
+
 /* diagnostics: enable != 0 makes the TRSV sweeps record globaltimer stamps
  * (forward chain steps, transposed chain steps, forward worker hand-offs,
  * transposed worker hand-offs: 4 nb values, then the launch start); with

@@ -60,6 +60,9 @@ SIGNATURES = {
     "ltb_engine_set_phase3": ([_vp, _vp, C.c_size_t, _vp, C.c_int], C.c_int),
     "ltb_engine_predict_qoi": ([_vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
     "ltb_normal_quantile": ([C.c_double, _dp], C.c_int),
+    "ltb_fnv1a64_file": ([C.c_char_p, C.POINTER(C.c_uint64)], C.c_int),
+    "ltb_engine_load_factor_dnsm": ([_vp, C.c_char_p], C.c_int),
+    "ltb_engine_load_phase3_dnsm": ([_vp, C.c_char_p, C.c_char_p], C.c_int),
     "ltb_engine_infer_and_forecast": ([_vp, _vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
 }
 

@@ -11,6 +11,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/ltb.h"
 #include "ltb_kernels.h"
@@ -664,4 +665,165 @@ void release_phase3(ltb_engine* e) {
     it->second.release();
     g_qoi.erase(it);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Artifact loaders (io.cpp): DNSM1 dense matrices -> device, FNV-1a hashes
+// (io.cpp:198-219) for manifest verification.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DnsmHeader {
+  uint64_t rows = 0, cols = 0, sym = 0;
+};
+
+// io.cpp:102-136: "DNSM1", u64 rows, cols, symmetric flag, row-major doubles
+ltb_status open_dnsm(const char* path, FILE** fh, DnsmHeader* h) {
+  *fh = fopen(path, "rb");
+  if (!*fh) return efail(LTB_IO, "cannot open dense archive %s", path);
+  char magic[5];
+  uint64_t v[3];
+  if (fread(magic, 1, 5, *fh) != 5 || memcmp(magic, "DNSM1", 5) != 0) {
+    fclose(*fh);
+    return efail(LTB_IO, "bad magic in %s (expected DNSM1)", path);
+  }
+  if (fread(v, sizeof(uint64_t), 3, *fh) != 3) {
+    fclose(*fh);
+    return efail(LTB_IO, "truncated archive while reading header of %s", path);
+  }
+  if (v[0] == 0 || v[1] == 0 || v[0] * v[1] > (1ull << 40)) {
+    fclose(*fh);
+    return efail(LTB_IO, "implausible dense header in %s", path);
+  }
+  h->rows = v[0];
+  h->cols = v[1];
+  h->sym = v[2];
+  return LTB_OK;
+}
+
+// pack block row I of the factor from a row-major panel of 64 rows
+// (panel[(r - 64 I) * n + c]); lower triangle only, identity padding
+__global__ void pack_panel_rowmajor_kernel(const double* __restrict__ panel, int n, int I,
+                                           double* __restrict__ row_tiles) {
+  const int J = blockIdx.x;  // tile (I, J), J <= I
+  double* dst = row_tiles + (size_t)J * kTB * kTB;
+  for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+    const int jj = e >> 6, ii = e & 63;
+    const int r = I * kTB + ii, c = J * kTB + jj;
+    double v;
+    if (r < n && c < n) v = c <= r ? panel[(size_t)ii * n + c] : 0.0;
+    else v = r == c ? 1.0 : 0.0;
+    dst[e] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" ltb_status ltb_fnv1a64_file(const char* path, uint64_t* out) {
+  if (!path || !out) return efail(LTB_INVALID, "fnv1a64_file: null argument");
+  FILE* fh = fopen(path, "rb");
+  if (!fh) return efail(LTB_IO, "cannot hash missing file %s", path);
+  uint64_t h = 0xcbf29ce484222325ull;
+  std::vector<unsigned char> buf(1 << 20);
+  size_t got;
+  while ((got = fread(buf.data(), 1, buf.size(), fh)) > 0) {
+    for (size_t i = 0; i < got; ++i) {
+      h ^= buf[i];
+      h *= 0x100000001b3ull;
+    }
+  }
+  fclose(fh);
+  *out = h;
+  return LTB_OK;
+}
+
+// set_factor from chol.dnsm (workflow.cpp:324 read_dense): the strict upper
+// part of the stored matrix is ignored (it may hold K, bayes_engine.cpp:180-193)
+extern "C" ltb_status ltb_engine_load_factor_dnsm(ltb_engine* e, const char* path) {
+  if (!e || !path) return efail(LTB_INVALID, "load_factor_dnsm: null argument");
+  if (e->world > 1)
+    return efail(LTB_STATE, "load_factor_dnsm: a distributed factor is built per rank (set_factor_generated)");
+  FILE* fh = nullptr;
+  DnsmHeader h;
+  ltb_status st = open_dnsm(path, &fh, &h);
+  if (st != LTB_OK) return st;
+  const int n = e->nd * e->nt;
+  if (h.rows != (uint64_t)n || h.cols != (uint64_t)n) {
+    fclose(fh);
+    return efail(LTB_DIMENSION, "set_factor: wrong factor dims");
+  }
+  Guard gd(e->device);
+  st = factor_prepare(e, n);
+  if (st != LTB_OK) {
+    fclose(fh);
+    return st;
+  }
+  std::vector<double> host((size_t)kTB * n);
+  double* panel = nullptr;
+  if (cudaMalloc(&panel, sizeof(double) * kTB * n) != cudaSuccess) {
+    fclose(fh);
+    return efail(LTB_CUDA, "load_factor_dnsm: alloc failed");
+  }
+  const int nb = (n + kTB - 1) / kTB;
+  for (int I = 0; I < nb && st == LTB_OK; ++I) {
+    const int r0 = I * kTB, rr = std::min(kTB, n - r0);
+    const size_t cnt = (size_t)rr * n;
+    if (fread(host.data(), sizeof(double), cnt, fh) != cnt) {
+      st = efail(LTB_IO, "truncated archive while reading dense row");
+      break;
+    }
+    cudaMemcpy(panel, host.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice);
+    const size_t row_off = (size_t)I * (I + 1) / 2;  // P = 1 packing
+    pack_panel_rowmajor_kernel<<<I + 1, 256>>>(panel, n, I, e->factor.tiles + row_off * kTB * kTB);
+    count_launches(1);
+    if (cudaGetLastError() != cudaSuccess) st = efail(LTB_CUDA, "load_factor_dnsm: pack failed");
+  }
+  fclose(fh);
+  cudaError_t err = cudaDeviceSynchronize();
+  cudaFree(panel);
+  if (st != LTB_OK) return st;
+  if (err != cudaSuccess) return efail(LTB_CUDA, "load_factor_dnsm: %s", cudaGetErrorString(err));
+  return factor_finish(e, trsv_prepare_packed(e->factor, 0));
+}
+
+// set_phase3 from Q.dnsm and Gamma_post_q.dnsm (workflow.cpp:325-330)
+extern "C" ltb_status ltb_engine_load_phase3_dnsm(ltb_engine* e, const char* q_path,
+                                                  const char* gpost_path) {
+  if (!e || !q_path || !gpost_path) return efail(LTB_INVALID, "load_phase3_dnsm: null argument");
+  const uint64_t rows = (uint64_t)e->nq * e->nt, cols = (uint64_t)e->nd * e->nt;
+  FILE* fq = nullptr;
+  DnsmHeader hq, hg;
+  ltb_status st = open_dnsm(q_path, &fq, &hq);
+  if (st != LTB_OK) return st;
+  if (hq.rows != rows || hq.cols != cols) {
+    fclose(fq);
+    return efail(LTB_DIMENSION, "set_phase3: wrong artifact dims");
+  }
+  // row-major on disk -> column-major (Eigen storage) for set_phase3
+  std::vector<double> qcm(rows * cols), row(cols);
+  for (uint64_t i = 0; i < rows; ++i) {
+    if (fread(row.data(), sizeof(double), cols, fq) != cols) {
+      fclose(fq);
+      return efail(LTB_IO, "truncated archive while reading dense row");
+    }
+    for (uint64_t j = 0; j < cols; ++j) qcm[j * rows + i] = row[j];
+  }
+  fclose(fq);
+  FILE* fg = nullptr;
+  st = open_dnsm(gpost_path, &fg, &hg);
+  if (st != LTB_OK) return st;
+  if (hg.rows != rows || hg.cols != rows) {
+    fclose(fg);
+    return efail(LTB_DIMENSION, "set_phase3: wrong artifact dims");
+  }
+  std::vector<double> diag(rows), grow(rows);
+  for (uint64_t i = 0; i < rows; ++i) {
+    if (fread(grow.data(), sizeof(double), rows, fg) != rows) {
+      fclose(fg);
+      return efail(LTB_IO, "truncated archive while reading dense row");
+    }
+    diag[i] = grow[i];
+  }
+  fclose(fg);
+  return ltb_engine_set_phase3(e, qcm.data(), rows, diag.data(), LTB_PTR_HOST);
 }

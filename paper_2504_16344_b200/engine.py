@@ -158,6 +158,15 @@ class InferenceEngine:
         check(_lib.load().ltb_engine_set_phase3(self._h, C.c_void_p(Qf.ctypes.data), rows,
                                                 C.c_void_p(g.ctypes.data), 0))
 
+    def load_factor(self, path):
+        """set_factor from a DNSM1 archive (chol.dnsm, io.cpp:102-136)."""
+        check(_lib.load().ltb_engine_load_factor_dnsm(self._h, str(path).encode()))
+
+    def load_phase3(self, q_path, gamma_post_q_path):
+        """set_phase3 from Q.dnsm / Gamma_post_q.dnsm (workflow.cpp:325-330)."""
+        check(_lib.load().ltb_engine_load_phase3_dnsm(self._h, str(q_path).encode(),
+                                                      str(gamma_post_q_path).encode()))
+
     def predict_qoi(self, d_obs, level=0.95):
         """bayes_engine.cpp:340-362: q_map = Q d_obs with credible intervals
         q_map -/+ z sqrt(diag Gamma_post_q)."""

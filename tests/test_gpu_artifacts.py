@@ -97,3 +97,57 @@ def test_btpz_loader_errors(ltb, tmp_path):
     write_btpz(nan, k)
     with pytest.raises(ltb.NumericalError):
         ltb.MatvecPlan.load(nan)
+
+
+def write_dnsm(path, m, symmetric=False):
+    """io.cpp:102-115 byte layout (row-major)."""
+    m = np.asarray(m, dtype="<f8")
+    with open(path, "wb") as fh:
+        fh.write(b"DNSM1")
+        fh.write(struct.pack("<3Q", m.shape[0], m.shape[1], int(symmetric)))
+        fh.write(np.ascontiguousarray(m).tobytes())
+
+
+def fnv1a64(data):
+    h = 0xCBF29CE484222325
+    for b in data:
+        h ^= b
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def test_dnsm_factor_and_phase3_loaders(ltb, tmp_path):
+    import ctypes as C
+    import scipy.linalg as sl
+    from paper_2504_16344_b200 import _lib
+    nd, nq, nm, nt = 3, 2, 5, 30  # n = 90: two 64-blocks, ragged
+    n = nd * nt
+    g = ltb.MatvecPlan.generated(nd, nm, nt, seed=2, tag=ltb.KernelTag.Gstar)
+    fq = ltb.MatvecPlan.generated(nq, nm, nt, seed=2, tag=ltb.KernelTag.Fq)
+    eng = ltb.InferenceEngine(g, fq)
+    rng = np.random.default_rng(0)
+    L = orc.gen_factor(5, n)
+    stored = L + np.triu(rng.standard_normal((n, n)), 1)  # upper part must be ignored
+    write_dnsm(tmp_path / "chol.dnsm", stored)
+    eng.load_factor(tmp_path / "chol.dnsm")
+    y = rng.standard_normal(n)
+    ref = sl.solve_triangular(L, sl.solve_triangular(L, y, lower=True), lower=True, trans="T")
+    assert orc.rel_err(eng.solve_k_inplace(y.copy()), ref) <= 1e-12
+    Q = rng.standard_normal((nq * nt, n))
+    G = rng.standard_normal((nq * nt, nq * nt))
+    G = G @ G.T
+    write_dnsm(tmp_path / "Q.dnsm", Q)
+    write_dnsm(tmp_path / "Gpost.dnsm", G, symmetric=True)
+    eng.load_phase3(tmp_path / "Q.dnsm", tmp_path / "Gpost.dnsm")
+    res = eng.predict_qoi(ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, y))
+    assert orc.rel_err(res.q_map.values, Q @ y) <= 1e-13
+    assert np.allclose(res.ci_upper.values - res.q_map.values, 1.96 * np.sqrt(np.diag(G)), rtol=1e-12)
+    # FNV-1a over the archive bytes (io.cpp:198-219)
+    h = C.c_uint64()
+    assert _lib.load().ltb_fnv1a64_file(str(tmp_path / "Q.dnsm").encode(), C.byref(h)) == 0
+    assert h.value == fnv1a64((tmp_path / "Q.dnsm").read_bytes())
+    with pytest.raises(ltb.DimensionError):
+        write_dnsm(tmp_path / "small.dnsm", np.eye(4))
+        eng.load_factor(tmp_path / "small.dnsm")
+    with pytest.raises(ltb.IoError):
+        eng.load_factor(tmp_path / "none.dnsm")
