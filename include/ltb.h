@@ -205,6 +205,34 @@ ltb_status ltb_engine_connect(ltb_engine* e, const void* handles);
 /* synthetic factor generated on the device (oracle orc_gen_factor) */
 ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed);
 
+/* ---- offline phase 2 on the device: form_K + factorize ----
+ * form_K (bayes_engine.cpp:136-172): K = F G* + sigma2 I over
+ * n = N_d N_t, from the time-domain kernels of F and G = F Gamma_x
+ * ([rows][cols][lag], host or device; rows = N_d, cols = N_m of the engine's
+ * G* plan).  g_kernel NULL: G is premultiplied from F on the device with
+ * prior3 = {h_x, gamma, delta} (bayes_engine.cpp:105, prior.cpp:108-134).
+ * Formed as the lag Gram contraction A = F_lag G_lag^T on FP64 tensor cores
+ * plus a diagonal recurrence (ltb_formk.h); only the lower triangle is
+ * formed (K is symmetric; the reference symmetrises, :154-171), straight
+ * into the packed tiles.  Single-GPU engines. */
+ltb_status ltb_engine_form_k(ltb_engine* e, const double* f_kernel, const double* g_kernel,
+                             const double* prior3, int rows, int cols, int nt, double sigma2,
+                             int ptr_kind);
+/* form_K of the generated kernel k(r, c, t) = U(seed, stream, (r N_m + c) N_t + t)
+ * (ltb_plan_create_generated with nm_total = N_m) and its premultiplied G */
+ltb_status ltb_engine_form_k_generated(ltb_engine* e, uint64_t seed, uint64_t stream, double h_x,
+                                       double gamma, double delta, double sigma2);
+/* factorize (bayes_engine.cpp:176-209): K = L L^T in place (tile Cholesky,
+ * DMMA trailing updates); LTB_NUMERICAL if K is not positive definite,
+ * LTB_STATE without form_K.  Afterwards the engine is ready to solve. */
+ltb_status ltb_engine_factorize(ltb_engine* e);
+/* device milliseconds of the last form_K / factorize (either nullable) */
+ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms);
+/* K (after form_K) or L (after factorize / set_factor) as an n x n
+ * column-major matrix with leading dimension ld: lower triangle, zeros
+ * above (the reference's K() / chol_lower() accessors) */
+ltb_status ltb_engine_export_lower(const ltb_engine* e, double* out, size_t ld, int ptr_kind);
+
 /* solve_k_inplace (bayes_engine.cpp:236-240): y <- L^{-T} L^{-1} y */
 ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, int ptr_kind);
 

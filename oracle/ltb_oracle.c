@@ -610,3 +610,88 @@ void orc_infer_map(const double* L, size_t ld, const orc_plan* plan_g,
   orc_apply_adjoint_raw(plan_g, y, m_map);
   free(y);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Offline phase 2: form_K (bayes_engine.cpp:136-172) and factorize
+ * (:176-209).  Test infrastructure only. */
+/* ------------------------------------------------------------------------ */
+
+/* read_gstar_column (bayes_engine.cpp:122-134): entry (x, t) = g[s][x][j-t]
+ * for t <= j, column col = s * nt + j */
+static void read_gstar_column(const double* g_rck, int nm, int nt, int col, double* out) {
+  const int s = col / nt, j = col % nt;
+  memset(out, 0, sizeof(double) * (size_t)nm * nt);
+  for (int x = 0; x < nm; ++x) {
+    const double* lag = g_rck + ((size_t)s * nm + x) * nt;
+    for (int t = 0; t <= j; ++t) out[(size_t)x * nt + t] = lag[j - t];
+  }
+}
+
+int orc_form_k(const double* f_rck, const double* g_rck, int rows, int nm, int nt,
+               double sigma2, int mode, double* K, double* asym) {
+  const int n = rows * nt;
+  orc_plan* pf = NULL;
+  orc_plan* pg = NULL;
+  if (orc_plan_create(f_rck, rows, nm, nt, &pf) != 0) return 1;
+  if (mode == 0 && orc_plan_create(g_rck, rows, nm, nt, &pg) != 0) {
+    orc_plan_destroy(pf);
+    return 1;
+  }
+  double* e = (double*)calloc((size_t)n, sizeof(double));
+  double* gcol = (double*)malloc(sizeof(double) * (size_t)nm * nt);
+  for (int i = 0; i < n; ++i) { /* :139-151 */
+    if (mode == 0) {
+      e[i] = 1.0;
+      orc_apply_adjoint_raw(pg, e, gcol);
+      e[i] = 0.0;
+    } else {
+      read_gstar_column(g_rck, nm, nt, i, gcol);
+    }
+    orc_apply_raw(pf, gcol, K + (size_t)i * n);
+    K[(size_t)i * n + i] += sigma2;
+  }
+  /* :153-171: asymmetry of the assembled K, then symmetrise */
+  double asym2 = 0, norm2 = 0;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < i; ++j) {
+      const double d = K[(size_t)j * n + i] - K[(size_t)i * n + j];
+      asym2 += 2 * d * d;
+      norm2 += K[(size_t)j * n + i] * K[(size_t)j * n + i] + K[(size_t)i * n + j] * K[(size_t)i * n + j];
+    }
+    norm2 += K[(size_t)i * n + i] * K[(size_t)i * n + i];
+  }
+  if (asym) *asym = sqrt(asym2) / fmax(sqrt(norm2), 1e-300);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j) {
+      const double v = 0.5 * (K[(size_t)j * n + i] + K[(size_t)i * n + j]);
+      K[(size_t)j * n + i] = v;
+      K[(size_t)i * n + j] = v;
+    }
+  free(e);
+  free(gcol);
+  orc_plan_destroy(pf);
+  if (pg) orc_plan_destroy(pg);
+  return 0;
+}
+
+/* Column-oriented (left-looking) Cholesky: L(j,j) = sqrt(A(j,j) - sum_k
+ * L(j,k)^2), L(i,j) = (A(i,j) - sum_k L(i,k) L(j,k)) / L(j,j) -- the
+ * textbook algorithm LLT / dpotrf block; rounding differs from both only in
+ * summation order. */
+int orc_cholesky(double* A, int n, size_t ld) {
+  for (int j = 0; j < n; ++j) {
+    double d = A[(size_t)j * ld + j];
+    for (int k = 0; k < j; ++k) d -= A[(size_t)k * ld + j] * A[(size_t)k * ld + j];
+    if (!(d > 0) || !isfinite(d)) return j + 1;
+    const double ljj = sqrt(d);
+    A[(size_t)j * ld + j] = ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double v = A[(size_t)j * ld + i];
+      for (int k = 0; k < j; ++k) v -= A[(size_t)k * ld + i] * A[(size_t)k * ld + j];
+      A[(size_t)j * ld + i] = v / ljj;
+    }
+  }
+  for (int j = 1; j < n; ++j)
+    for (int i = 0; i < j; ++i) A[(size_t)j * ld + i] = 0.0;
+  return 0;
+}

@@ -110,6 +110,19 @@ int orc_prior_premultiply(const double* f_rck, int rows, int nm, int nt,
 int orc_prior_apply_precision(const double* v_tm, int nm, int nt, double h_x,
                               double gamma, double delta, double* out_tm);
 
+/* ---- offline phase 2 (bayes_engine.cpp:122-209) ---- */
+/* form_K: column i of K (n = rows * nt, column-major, ld n) is
+ * plan_F.apply(G* e_i) with G* e_i from plan_G.apply_adjoint(e_i)
+ * (mode 0, ColumnByColumn) or read off the G kernel (mode 1, FusedBatched,
+ * read_gstar_column :122-134); K(i, i) += sigma2; then the asymmetry
+ * measure (*asym) and the symmetrisation (:153-171).  0 on success. */
+int orc_form_k(const double* f_rck, const double* g_rck, int rows, int nm, int nt,
+               double sigma2, int mode, double* K, double* asym);
+/* factorize: in-place lower Cholesky of the column-major n x n A (ld);
+ * the strict upper part is zeroed (Eigen LLT matrixL(), :195-208).
+ * Returns 0, or j + 1 for a non-positive pivot in column j. */
+int orc_cholesky(double* A, int n, size_t ld);
+
 /* ---- online phase (bayes_engine.cpp:307-338) ---- */
 /* m_map = G* K^{-1} d: y = copy(d); solve_k(y); m = plan_g.apply_adjoint(y) */
 void orc_infer_map(const double* L, size_t ld, const orc_plan* plan_g,

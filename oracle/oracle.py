@@ -68,6 +68,9 @@ def lib():
                                             C.c_double, C.c_double, _dp]
         L.orc_prior_apply_precision.argtypes = [_dp, C.c_int, C.c_int, C.c_double,
                                                 C.c_double, C.c_double, _dp]
+        L.orc_form_k.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                 _dp, _dp]
+        L.orc_cholesky.argtypes = [_dp, C.c_int, C.c_size_t]
         L.orc_fft_create.argtypes = [C.c_int]
         L.orc_fft_create.restype = C.c_void_p
         L.orc_fft_destroy.argtypes = [C.c_void_p]
@@ -275,6 +278,33 @@ def reindex(v, rows, nt, to_time_major):
     out = np.empty_like(v)
     lib().orc_reindex(_ptr(v), rows, nt, int(to_time_major), _ptr(out))
     return out
+
+
+def form_k(f_rck, g_rck, sigma2, mode=0):
+    """(K, asymmetry): bayes_engine.cpp:136-172 restated (mode 0
+    ColumnByColumn, 1 FusedBatched); K is an (n, n) array."""
+    f = np.ascontiguousarray(f_rck, dtype=np.float64)
+    g = np.ascontiguousarray(g_rck, dtype=np.float64)
+    rows, nm, nt = f.shape
+    n = rows * nt
+    K = np.empty(n * n)
+    asym = C.c_double()
+    st = lib().orc_form_k(_ptr(f), _ptr(g), rows, nm, nt, float(sigma2), int(mode), _ptr(K),
+                          C.byref(asym))
+    if st != 0:
+        raise RuntimeError("orc_form_k status %d" % st)
+    return K.reshape(n, n).T.copy(), asym.value
+
+
+def cholesky(A):
+    """Lower Cholesky factor (zeros above); raises ValueError on a
+    non-positive pivot (bayes_engine.cpp:195-206 NumericalError)."""
+    L = np.array(A, dtype=np.float64, order="F", copy=True)
+    n = L.shape[0]
+    st = lib().orc_cholesky(L.ctypes.data_as(_dp), n, n)
+    if st != 0:
+        raise ValueError("factorize: K not positive definite (column %d)" % (st - 1))
+    return np.ascontiguousarray(L)
 
 
 def rel_err(a, b):

@@ -858,6 +858,39 @@ ltb_status plan_from_source(int rows, int cols, int nt, int tag, const SlabSourc
 
 }  // namespace
 
+namespace ltb_internal {
+// Gamma_x premultiply of a whole device kernel [rows][cols][nt] in place
+// (form_K's G kernel, bayes_engine.cpp:105)
+ltb_status premultiply_device(double* kernel, int rows, int cols, int nt, double h_x, double gamma,
+                              double delta) {
+  PriorDev prior;
+  ltb_status st = make_prior(cols, h_x, gamma, delta, prior);
+  if (st != LTB_OK) return st;
+  const long long lines = (long long)rows * nt;
+  prior_premultiply_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 16, (lines + 127) / 128)), 128>>>(
+      kernel, rows, cols, nt, prior.ldiag, prior.lsub);
+  g_launches += 1;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(LTB_CUDA, "premultiply: %s", cudaGetErrorString(e));
+  return LTB_OK;
+}
+// non-finite scan of a device array (core.cpp:73-77)
+ltb_status check_finite_device(const double* x, long long n, const char* what) {
+  unsigned long long* bad = nullptr;
+  if (cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess) return fail(LTB_CUDA, "finite scan: alloc");
+  cudaMemset(bad, 0, sizeof(unsigned long long));
+  count_nonfinite_slab<<<148 * 4, 256>>>(x, n, bad);
+  g_launches += 1;
+  unsigned long long hb = 0;
+  cudaError_t e = cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  if (e != cudaSuccess) return fail(LTB_CUDA, "finite scan: %s", cudaGetErrorString(e));
+  if (hb) return fail(LTB_NUMERICAL, "%s: non-finite kernel entry", what);
+  return LTB_OK;
+}
+}  // namespace ltb_internal
+
 extern "C" {
 
 ltb_status ltb_plan_create_premultiplied(const double* kernel, int rows, int cols, int nt, int tag,

@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "../../include/ltb.h"
+#include "ltb_formk.h"
+#include "ltb_gen.cuh"
 #include "ltb_kernels.h"
 #include "ltb_trsv.h"
 
@@ -28,6 +30,9 @@ cudaStream_t scratch_stream(ltb_scratch* s);
 int plan_device(const ltb_plan* p);
 void plan_dims(const ltb_plan* p, int* rows, int* cols, int* nt);
 void count_launches(uint64_t n);
+ltb_status premultiply_device(double* kernel, int rows, int cols, int nt, double h_x, double gamma,
+                              double delta);
+ltb_status check_finite_device(const double* x, long long n, const char* what);
 }  // namespace ltb_internal
 
 using namespace ltb_internal;
@@ -70,6 +75,8 @@ struct ltb_engine {
   int world = 1, rank = 0;  // distributed K^{-1} (ltb_engine_set_world)
   TriFactor factor;
   bool factorized = false;
+  bool kformed = false;          // factor.tiles hold K (form_K), not yet factorized
+  double formk_ms = 0.0, factorize_ms = 0.0;
   double* ypad = nullptr;       // nb * 64
   double* stage_in = nullptr;   // host-pointer staging: d (nd*nt)
   double* stage_m = nullptr;    // m_map (nm*nt)
@@ -152,6 +159,7 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
   ENG_CUDA(cudaMalloc(&e->ypad, nb * kTB * sizeof(double)));
   ENG_CUDA(cudaMemset(e->ypad, 0, nb * kTB * sizeof(double)));
   e->factorized = false;
+  e->kformed = false;
   return LTB_OK;
 }
 
@@ -286,6 +294,148 @@ ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed) 
   if (st != LTB_OK) return st;
   count_launches(1);
   return factor_finish(e, trsv_setup_generated(e->factor, seed, 0));
+}
+
+}  // extern "C"
+
+// ---- offline phase 2 on the device: form_K / factorize (ltb_formk.h) ----
+namespace {
+
+struct DevBuf {
+  double* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+};
+
+// K from device kernels f, g (both [nd][nm][nt]) into the packed tiles
+ltb_status form_k_dev(ltb_engine* e, const double* f, const double* g, int nm, double sigma2) {
+  ltb_status st = factor_prepare(e, e->nd * e->nt);
+  if (st != LTB_OK) return st;
+  ENG_CUDA(cudaEventRecord(e->ev0, 0));
+  cudaError_t err = formk_device(e->factor, f, g, e->nd, nm, e->nt, sigma2, 0);
+  count_launches(formk_last_launches());
+  if (err != cudaSuccess) return efail(LTB_CUDA, "form_K: %s", cudaGetErrorString(err));
+  ENG_CUDA(cudaEventRecord(e->ev1, 0));
+  ENG_CUDA(cudaEventSynchronize(e->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  e->formk_ms = ms;
+  e->kformed = true;
+  return LTB_OK;
+}
+
+ltb_status form_k_check(ltb_engine* e, const char* what) {
+  if (e->world > 1) return efail(LTB_STATE, "%s: a distributed engine takes a per-rank factor", what);
+  if ((long long)e->nd * e->nt > INT32_MAX / 2) return efail(LTB_CAPACITY, "%s: n_data too large", what);
+  return LTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ltb_status ltb_engine_form_k(ltb_engine* e, const double* f_kernel, const double* g_kernel,
+                             const double* prior3, int rows, int cols, int nt, double sigma2,
+                             int ptr_kind) {
+  if (!e || !f_kernel) return efail(LTB_INVALID, "form_K: null argument");
+  if (!g_kernel && !prior3) return efail(LTB_INVALID, "form_K: need the G kernel or the prior (prior3)");
+  ltb_status st = form_k_check(e, "form_K");
+  if (st != LTB_OK) return st;
+  if (rows != e->nd || nt != e->nt || cols != e->nm)
+    return efail(LTB_DIMENSION, "form_K: kernel dims (%d, %d, %d) do not match the engine (%d, %d, %d)",
+                 rows, cols, nt, e->nd, e->nm, e->nt);
+  Guard gd(e->device);
+  const size_t cnt = (size_t)rows * cols * nt;
+  DevBuf df, dg;
+  const double* f = f_kernel;
+  const double* g = g_kernel;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(cudaMalloc(&df.p, cnt * sizeof(double)));
+    ENG_CUDA(cudaMemcpy(df.p, f_kernel, cnt * sizeof(double), cudaMemcpyHostToDevice));
+    f = df.p;
+  }
+  if ((st = check_finite_device(f, (long long)cnt, "engine F")) != LTB_OK) return st;
+  if (!g_kernel) {
+    ENG_CUDA(cudaMalloc(&dg.p, cnt * sizeof(double)));
+    ENG_CUDA(cudaMemcpy(dg.p, f, cnt * sizeof(double), cudaMemcpyDeviceToDevice));
+    if ((st = premultiply_device(dg.p, rows, cols, nt, prior3[0], prior3[1], prior3[2])) != LTB_OK) return st;
+    g = dg.p;
+  } else {
+    if (ptr_kind == LTB_PTR_HOST) {
+      ENG_CUDA(cudaMalloc(&dg.p, cnt * sizeof(double)));
+      ENG_CUDA(cudaMemcpy(dg.p, g_kernel, cnt * sizeof(double), cudaMemcpyHostToDevice));
+      g = dg.p;
+    }
+    if ((st = check_finite_device(g, (long long)cnt, "engine G")) != LTB_OK) return st;
+  }
+  return form_k_dev(e, f, g, cols, sigma2);
+}
+
+ltb_status ltb_engine_form_k_generated(ltb_engine* e, uint64_t seed, uint64_t stream, double h_x,
+                                       double gamma, double delta, double sigma2) {
+  if (!e) return efail(LTB_INVALID, "form_K: null engine");
+  ltb_status st = form_k_check(e, "form_K");
+  if (st != LTB_OK) return st;
+  Guard gd(e->device);
+  const size_t cnt = (size_t)e->nd * e->nm * e->nt;
+  DevBuf df, dg;
+  ENG_CUDA(cudaMalloc(&df.p, cnt * sizeof(double)));
+  ENG_CUDA(cudaMalloc(&dg.p, cnt * sizeof(double)));
+  ENG_CUDA(launch_gen_fill(gen_key(seed, stream), 0, (long long)cnt, df.p, 0));
+  count_launches(1);
+  ENG_CUDA(cudaMemcpy(dg.p, df.p, cnt * sizeof(double), cudaMemcpyDeviceToDevice));
+  if ((st = premultiply_device(dg.p, e->nd, e->nm, e->nt, h_x, gamma, delta)) != LTB_OK) return st;
+  return form_k_dev(e, df.p, dg.p, e->nm, sigma2);
+}
+
+ltb_status ltb_engine_factorize(ltb_engine* e) {
+  if (!e) return efail(LTB_INVALID, "factorize: null engine");
+  if (!e->kformed) return efail(LTB_STATE, "engine: missing offline artifact: K (run form_K)");
+  Guard gd(e->device);
+  ENG_CUDA(cudaEventRecord(e->ev0, 0));
+  int bad = -1;
+  cudaError_t err = cholesky_packed(e->factor, 0, &bad);
+  count_launches(formk_last_launches());
+  e->kformed = false;  // overwritten in place (bayes_engine.cpp:180-193)
+  if (err == cudaErrorInvalidValue)
+    return efail(LTB_NUMERICAL, "factorize: K not positive definite (pivot failure in block column %d)", bad);
+  if (err != cudaSuccess) return efail(LTB_CUDA, "factorize: %s", cudaGetErrorString(err));
+  ENG_CUDA(cudaEventRecord(e->ev1, 0));
+  ENG_CUDA(cudaEventSynchronize(e->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  e->factorize_ms = ms;
+  return factor_finish(e, trsv_prepare_packed(e->factor, 0));
+}
+
+ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms) {
+  if (!e) return efail(LTB_INVALID, "offline_ms: null engine");
+  if (formk_ms) *formk_ms = e->formk_ms;
+  if (factorize_ms) *factorize_ms = e->factorize_ms;
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_export_lower(const ltb_engine* e_, double* out, size_t ld, int ptr_kind) {
+  ltb_engine* e = const_cast<ltb_engine*>(e_);
+  if (!e || !out) return efail(LTB_INVALID, "export_lower: null argument");
+  if (!e->kformed && !e->factorized) return efail(LTB_STATE, "engine: missing offline artifact: K or its factor");
+  if (e->world > 1) return efail(LTB_STATE, "export_lower: distributed factor");
+  const int n = e->factor.n;
+  if (ld < (size_t)n) return efail(LTB_DIMENSION, "export_lower: ld < n");
+  Guard gd(e->device);
+  DevBuf tmp;
+  double* dst = out;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(cudaMalloc(&tmp.p, ld * (size_t)n * sizeof(double)));
+    dst = tmp.p;
+  }
+  ENG_CUDA(cudaMemset2D(dst, ld * sizeof(double), 0, (size_t)n * sizeof(double), n));
+  ENG_CUDA(export_lower(e->factor, dst, ld, 0));
+  count_launches(1);
+  if (ptr_kind == LTB_PTR_HOST)
+    ENG_CUDA(cudaMemcpy(out, tmp.p, ld * (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
+  else
+    ENG_CUDA(cudaDeviceSynchronize());
+  return LTB_OK;
 }
 
 ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, int ptr_kind) {

@@ -1,0 +1,454 @@
+// ltb_formk.cu -- form_K and the tile Cholesky on FP64 tensor cores (DMMA,
+// mma.sync m16n8k4 f64 -> SASS DMMA.8x8x4 on sm_100a).  See ltb_formk.h for
+// the algebra.  Packed tile layout as in ltb_trsv.h (P = 1): block row I
+// starts at tile I (I+1) / 2, tile (I, J) is column-major 64x64.
+#include <math.h>
+
+#include <algorithm>
+
+#include "ltb_common.cuh"
+#include "ltb_formk.h"
+
+namespace ltb {
+
+namespace {
+
+constexpr int kT = kTB;          // 64
+constexpr int kTile = kT * kT;   // 4096 doubles
+int g_last_launches = 0;
+
+__host__ __device__ inline size_t tile_at(int I, int J) { return ((size_t)I * (I + 1) / 2 + J) * kTile; }
+
+// lower-triangular pair (i >= j) of linear index b
+LTB_DEV void tri_pair(long long b, int* i, int* j) {
+  long long r = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while ((r + 1) * (r + 2) / 2 <= b) ++r;
+  while (r * (r + 1) / 2 > b) --r;
+  *i = (int)r;
+  *j = (int)(b - r * (r + 1) / 2);
+}
+
+// D += A B for one m16n8k4 FP64 tile.  Fragments (g = lane / 4, q = lane % 4):
+// a0 = A[g][q], a1 = A[g+8][q], b0 = B[q][g];
+// d = {D[g][2q], D[g][2q+1], D[g+8][2q], D[g+8][2q+1]}
+LTB_DEV void dmma(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+LTB_DEV void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+LTB_DEV void cp_async8(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+LTB_DEV void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+LTB_DEV void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// (1) lag Gram A = F_lag G_lag^T, lower 128x128 CTA tiles, into the packed
+// tiles.  Operand row i = (r, a) = divmod(i, nt) reads f[(r nm + x) nt + a]:
+// for a fixed x a run of rows is contiguous, so a stage (kBK values of x,
+// 128 rows) is kBK contiguous 1 KB runs.  Shared stages are k-major
+// [x][row] with a row stride of 132 doubles (== 4 mod 16: the DMMA fragment
+// loads of a half-warp hit 32 distinct banks).
+// ---------------------------------------------------------------------------
+constexpr int kBM = 128;
+constexpr int kBK = 16;
+constexpr int kStages = 4;
+constexpr int kSS = kBM + 4;
+constexpr int kGemmThreads = 256;
+constexpr size_t kStageDoubles = (size_t)2 * kBK * kSS;
+constexpr size_t kGemmSmem = kStages * kStageDoubles * sizeof(double);
+
+template <bool kPair>
+LTB_DEV void gram_load_stage(double* sA, double* sB, const double* f, const double* g,
+                             const double* pa, const double* pb, int x0, int nm, int nt) {
+  const int tid = threadIdx.x;
+  if (kPair) {
+    // thread: row pair m = 2 (tid & 63), x rows kr + 4 q
+    const int m = 2 * (tid & 63), kr = tid >> 6;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = kr + 4 * q, x = x0 + k;
+      const bool okx = x < nm;
+      cp_async16(sA + k * kSS + m, (pa && okx) ? pa + (size_t)x * nt : f, (pa && okx) ? 16 : 0);
+      cp_async16(sB + k * kSS + m, (pb && okx) ? pb + (size_t)x * nt : g, (pb && okx) ? 16 : 0);
+    }
+  } else {
+    // thread: row m = tid & 127, x rows kr + 2 q
+    const int m = tid & 127, kr = tid >> 7;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = kr + 2 * q, x = x0 + k;
+      const bool okx = x < nm;
+      cp_async8(sA + k * kSS + m, (pa && okx) ? pa + (size_t)x * nt : f, (pa && okx) ? 8 : 0);
+      cp_async8(sB + k * kSS + m, (pb && okx) ? pb + (size_t)x * nt : g, (pb && okx) ? 8 : 0);
+    }
+  }
+}
+
+template <bool kPair>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    lag_gram_kernel(const double* __restrict__ f, const double* __restrict__ g, int nm, int nt,
+                    int n, int nb, double* __restrict__ tiles) {
+  extern __shared__ __align__(16) double gsm[];
+  int bi, bj;
+  tri_pair(blockIdx.x, &bi, &bj);
+  const int i0 = bi * kBM, j0 = bj * kBM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;  // warp tile 64 (rows) x 32 (cols)
+
+  // this thread's operand row base pointers (nullptr = padding row >= n)
+  const double* rowA;
+  const double* rowB;
+  {
+    const int m = kPair ? 2 * (tid & 63) : (tid & 127);
+    const int ia = i0 + m, ib = j0 + m;
+    rowA = ia < n ? f + (size_t)(ia / nt) * nm * nt + ia % nt : nullptr;
+    rowB = ib < n ? g + (size_t)(ib / nt) * nm * nt + ib % nt : nullptr;
+  }
+
+  double acc[4][4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+
+  const int nk = (nm + kBK - 1) / kBK;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nk) {
+      double* st = gsm + s * kStageDoubles;
+      gram_load_stage<kPair>(st, st + kBK * kSS, f, g, rowA, rowB, s * kBK, nm, nt);
+    }
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nx = kt + kStages - 1;
+      if (nx < nk) {
+        double* st = gsm + (nx % kStages) * kStageDoubles;
+        gram_load_stage<kPair>(st, st + kBK * kSS, f, g, rowA, rowB, nx * kBK, nm, nt);
+      }
+      cp_commit();
+    }
+    const double* sA = gsm + (kt % kStages) * kStageDoubles;
+    const double* sB = sA + kBK * kSS;
+#pragma unroll
+    for (int kk = 0; kk < kBK / 4; ++kk) {
+      const int kr = (kk * 4 + tq) * kSS;
+      double a[4][2], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        a[mt][0] = sA[kr + wm * 64 + mt * 16 + gq];
+        a[mt][1] = sA[kr + wm * 64 + mt * 16 + gq + 8];
+      }
+#pragma unroll
+      for (int nt8 = 0; nt8 < 4; ++nt8) b[nt8] = sB[kr + wn * 32 + nt8 * 8 + gq];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt8 = 0; nt8 < 4; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], b[nt8]);
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue: scatter into the packed 64x64 tiles (skip J > I and I >= nb)
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 4; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int i = i0 + wm * 64 + mt * 16 + gq + 8 * h;
+          const int j = j0 + wn * 32 + nt8 * 8 + 2 * tq + c;
+          const int I = i >> 6, J = j >> 6;
+          if (I < nb && J <= I) tiles[tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63)] = acc[mt][nt8][2 * h + c];
+        }
+}
+
+// ---------------------------------------------------------------------------
+// (2) K(t, j) = A(t, j) + K(t-1, j-1) inside each (r, s) block (r >= s), plus
+// sigma2 on the diagonal.  One thread per diagonal; consecutive threads take
+// consecutive diagonal starts (coalesced on the left-edge diagonals).  Loads
+// of a diagonal are batched 8 at a time so the walk is not latency-serial.
+// ---------------------------------------------------------------------------
+LTB_DEV double* elem(double* tiles, int i, int j) {
+  return tiles + tile_at(i >> 6, j >> 6) + (size_t)(j & 63) * kT + (i & 63);
+}
+
+__global__ void diag_prefix_kernel(double* __restrict__ tiles, int nd, int nt, double sigma2) {
+  const long long per = 2ll * nt - 1;
+  const long long total = (long long)nd * (nd + 1) / 2 * per;
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
+       id += (long long)gridDim.x * blockDim.x) {
+    const long long p = id / per;
+    const int d = (int)(id - p * per);
+    int r, s;
+    tri_pair(p, &r, &s);
+    int t0, j0;
+    if (d < nt) {
+      t0 = d;
+      j0 = 0;
+    } else {
+      if (r == s) continue;  // strict upper of a diagonal block: not stored
+      t0 = 0;
+      j0 = d - nt + 1;
+    }
+    const int len = nt - max(t0, j0);
+    const int ib = r * nt + t0, jb = s * nt + j0;
+    double run = 0.0;
+    for (int k0 = 0; k0 < len; k0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q < len) v[q] = *elem(tiles, ib + k0 + q, jb + k0 + q);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q < len) {
+          run += v[q];
+          const bool diag = (r == s) && (t0 == 0);
+          *elem(tiles, ib + k0 + q, jb + k0 + q) = diag ? run + sigma2 : run;
+        }
+    }
+  }
+}
+
+// identity on the padding diagonal (rows / columns >= n of the last block)
+__global__ void pad_identity_kernel(double* tiles, int n, int nb) {
+  const int i = n + threadIdx.x;
+  if (i < nb * kT) *elem(tiles, i, i) = 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// (3) tile Cholesky.  Panel step k: each CTA holds [A_kk; A_ik] (128 x 64,
+// column-major, ld 129) in shared memory and runs the unscaled right-looking
+// elimination a_ij -= a_ic a_jc / d_c (d_c = a_cc), one barrier per column;
+// then L = a_ij / sqrt(d_j).  CTA 0 writes L_kk (strict upper zeroed), every
+// CTA writes its panel tile L_ik = A_ik L_kk^{-T}.
+// ---------------------------------------------------------------------------
+constexpr int kPL = 129;
+constexpr int kPanelThreads = 256;
+
+constexpr size_t kPanelSmem = (size_t)(kT * kPL + kT) * sizeof(double);
+
+__global__ void __launch_bounds__(kPanelThreads)
+    chol_panel_kernel(double* __restrict__ tiles, int nb, int k, int* status) {
+  extern __shared__ double psm[];
+  double* sp = psm;          // [64 columns][129]: rows 0..63 = A_kk, 64..127 = A_ik
+  double* piv = psm + kT * kPL;
+  const int tid = threadIdx.x;
+  const int ip = k + 1 + blockIdx.x;  // panel tile row (none when ip >= nb)
+  const bool has_panel = ip < nb;
+  const double* Dk = tiles + tile_at(k, k);
+  const double* Pk = has_panel ? tiles + tile_at(ip, k) : nullptr;
+  for (int e = tid; e < kTile; e += kPanelThreads) {
+    const int j = e >> 6, i = e & 63;
+    sp[j * kPL + i] = Dk[e];
+    sp[j * kPL + 64 + i] = has_panel ? Pk[e] : 0.0;
+  }
+  __syncthreads();
+  const int row = tid & 127, cg = tid >> 7;  // this thread: row `row`, columns c+1+cg, c+3+cg, ...
+  bool bad = false;
+  for (int c = 0; c < kT; ++c) {
+    double d = sp[c * kPL + c];
+    if (!(d > 0.0) || !isfinite(d)) {
+      bad = true;
+      d = 1.0;
+    }
+    if (tid == 0) piv[c] = d;
+    if (row > c) {
+      const double lic = sp[c * kPL + row] / d;
+      for (int j = c + 1 + cg; j < kT; j += 2) {
+        if (row < 64 && j > row) break;
+        sp[j * kPL + row] -= lic * sp[c * kPL + j];
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && blockIdx.x == 0 && tid == 0) atomicCAS(status, 0, k + 1);
+  // scale: L_ij = a_ij / sqrt(d_j)
+  double* Lk = tiles + tile_at(k, k);
+  double* Lp = has_panel ? tiles + tile_at(ip, k) : nullptr;
+  for (int e = tid; e < kTile; e += kPanelThreads) {
+    const int j = e >> 6, i = e & 63;
+    const double rs = 1.0 / sqrt(piv[j]);
+    if (blockIdx.x == 0) Lk[e] = i > j ? sp[j * kPL + i] * rs : (i == j ? sqrt(piv[j]) : 0.0);
+    if (has_panel) Lp[e] = sp[j * kPL + 64 + i] * rs;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// (4) trailing update A_ij -= L_ik L_jk^T for k < j <= i < nb: one CTA per
+// tile, L_ik and L_jk staged by cp.async (k-major = the column-major tile),
+// A_ij fragments loaded into the DMMA accumulators and stored back.
+// 8 warps, warp tile 32 x 16.
+// ---------------------------------------------------------------------------
+constexpr int kUS = kT + 4;  // 68 == 4 mod 16
+constexpr int kUpdThreads = 256;
+constexpr size_t kUpdSmem = (size_t)2 * kT * kUS * sizeof(double);
+
+__global__ void __launch_bounds__(kUpdThreads)
+    chol_update_kernel(double* __restrict__ tiles, int nb, int k) {
+  extern __shared__ __align__(16) double usm[];
+  double* sA = usm;
+  double* sB = usm + kT * kUS;
+  int li, lj;
+  tri_pair(blockIdx.x, &li, &lj);
+  const int i = k + 1 + li, j = k + 1 + lj;
+  const double* Lik = tiles + tile_at(i, k);
+  const double* Ljk = tiles + tile_at(j, k);
+  double* Aij = tiles + tile_at(i, j);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  for (int c = tid; c < kTile / 2; c += kUpdThreads) {
+    const int l = c >> 5, m = 2 * (c & 31);
+    cp_async16(sA + l * kUS + m, Lik + l * kT + m, 16);
+    cp_async16(sB + l * kUS + m, Ljk + l * kT + m, 16);
+  }
+  cp_commit();
+  double acc[2][2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
+          acc[mt][nt8][2 * h + c] = Aij[col * kT + r];
+        }
+  cp_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int kk = 0; kk < kT / 4; ++kk) {
+    const int kr = (kk * 4 + tq) * kUS;
+    double a[2][2], b[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      a[mt][0] = -sA[kr + wm * 32 + mt * 16 + gq];
+      a[mt][1] = -sA[kr + wm * 32 + mt * 16 + gq + 8];
+    }
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8) b[nt8] = sB[kr + wn * 16 + nt8 * 8 + gq];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt8 = 0; nt8 < 2; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], b[nt8]);
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
+          Aij[col * kT + r] = acc[mt][nt8][2 * h + c];
+        }
+}
+
+// packed lower tiles -> column-major lower triangle
+__global__ void export_lower_kernel(const double* __restrict__ tiles, int n, double* __restrict__ out,
+                                    size_t ld) {
+  int I, J;
+  tri_pair(blockIdx.x, &I, &J);
+  const double* T = tiles + tile_at(I, J);
+  for (int e = threadIdx.x; e < kTile; e += blockDim.x) {
+    const int jj = e >> 6, ii = e & 63;
+    const int i = I * kT + ii, j = J * kT + jj;
+    if (i < n && j < n && i >= j) out[(size_t)j * ld + i] = T[e];
+  }
+}
+
+}  // namespace
+
+int formk_last_launches() { return g_last_launches; }
+
+cudaError_t formk_device(TriFactor& t, const double* f, const double* g, int nd, int nm, int nt,
+                         double sigma2, cudaStream_t st) {
+  if (t.P != 1 || t.n != nd * nt || nm < 1) return cudaErrorInvalidValue;
+  const int n = t.n, nb = t.nb;
+  const long long nbm = (n + kBM - 1) / kBM;
+  const long long ctas = nbm * (nbm + 1) / 2;
+  const bool pair = (nt % 2 == 0) && ((uintptr_t)f % 16 == 0) && ((uintptr_t)g % 16 == 0);
+  cudaError_t e;
+  if (pair) {
+    e = cudaFuncSetAttribute(lag_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    if (e != cudaSuccess) return e;
+    lag_gram_kernel<true><<<(unsigned)ctas, kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles);
+  } else {
+    e = cudaFuncSetAttribute(lag_gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    if (e != cudaSuccess) return e;
+    lag_gram_kernel<false><<<(unsigned)ctas, kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles);
+  }
+  const long long diags = (long long)nd * (nd + 1) / 2 * (2ll * nt - 1);
+  const unsigned pblocks = (unsigned)std::max(1ll, std::min(148ll * 32, (diags + 255) / 256));
+  diag_prefix_kernel<<<pblocks, 256, 0, st>>>(t.tiles, nd, nt, sigma2);
+  pad_identity_kernel<<<1, kT, 0, st>>>(t.tiles, n, nb);
+  g_last_launches = 3;
+  return cudaGetLastError();
+}
+
+cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
+  if (t.P != 1) return cudaErrorInvalidValue;
+  const int nb = t.nb;
+  cudaError_t e = cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kUpdSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmem);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(t.status, 0, sizeof(int), st);
+  int launches = 0;
+  for (int k = 0; k < nb; ++k) {
+    const int m = nb - k - 1;
+    chol_panel_kernel<<<std::max(1, m), kPanelThreads, kPanelSmem, st>>>(t.tiles, nb, k, t.status);
+    ++launches;
+    if (m > 0) {
+      chol_update_kernel<<<(unsigned)((long long)m * (m + 1) / 2), kUpdThreads, kUpdSmem, st>>>(t.tiles, nb, k);
+      ++launches;
+    }
+  }
+  g_last_launches = launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int h = 0;
+  e = cudaMemcpyAsync(&h, t.status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  if (h) {
+    cudaMemset(t.status, 0, sizeof(int));
+    if (bad_block) *bad_block = h - 1;
+    return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t export_lower(const TriFactor& t, double* out, size_t ld, cudaStream_t st) {
+  const long long ntiles = (long long)t.nb * (t.nb + 1) / 2;
+  export_lower_kernel<<<(unsigned)ntiles, 256, 0, st>>>(t.tiles, t.n, out, ld);
+  return cudaGetLastError();
+}
+
+}  // namespace ltb

@@ -1,0 +1,42 @@
+// ltb_formk.h -- offline phase 2 on the device: form_K (bayes_engine.cpp:
+// 136-172) and the in-place Cholesky factorize (:176-209), writing straight
+// into the packed 64x64 lower tiles the K^{-1} apply reads (ltb_trsv.h).
+//
+// form_K.  Column (s, j) of K is F G* e_(s,j) + sigma2 e_(s,j).  With
+// G* e_(s,j) read off the G kernel (read_gstar_column, :122-134) and F
+// causal, entry (r, t; s, j) is
+//     K = sum_x sum_{tau <= min(t, j)} f[r][x][t - tau] g[s][x][j - tau]
+// which satisfies the diagonal recurrence K(t, j) = A(t, j) + K(t-1, j-1)
+// inside every (r, s) block, with the lag Gram matrix
+//     A[(r, a), (s, b)] = sum_x f[r][x][a] g[s][x][b]       (n x n x N_m).
+// A is one dense FP64 contraction -- DMMA (FP64 tensor core) tiles fed by a
+// cp.async multi-stage pipeline -- and the recurrence is one O(n^2) pass.
+// Only the lower triangle is formed: G = F Gamma_x with Gamma_x symmetric
+// makes K symmetric, which is what the reference's symmetrisation restores.
+//
+// factorize.  Right-looking tile Cholesky on the packed tiles: per block
+// column k, one launch factors L_kk (and L_kk^{-1}) in shared memory and
+// forms the panel L_ik = A_ik L_kk^{-T} with DMMA; one launch applies the
+// trailing update A_ij -= L_ik L_jk^T with DMMA.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "ltb_trsv.h"
+
+namespace ltb {
+
+// t allocated by trsv_alloc(t, n = nd * nt, 1, 0).  f, g: device kernels
+// [nd][nm][nt].  Writes the lower tiles of K (identity padding included).
+cudaError_t formk_device(TriFactor& t, const double* f, const double* g, int nd, int nm, int nt,
+                         double sigma2, cudaStream_t st);
+// In place K -> L.  Returns cudaErrorInvalidValue (and leaves *bad_block the
+// first failing block column) when K is not positive definite.
+cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block);
+// Packed lower tiles -> column-major n x n device matrix (lower triangle
+// incl. the diagonal written; the strict upper part is left untouched).
+cudaError_t export_lower(const TriFactor& t, double* out, size_t ld, cudaStream_t st);
+// launches issued by the last formk_device / cholesky_packed call
+int formk_last_launches();
+
+}  // namespace ltb

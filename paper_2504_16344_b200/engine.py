@@ -17,6 +17,19 @@ from .matvec import (Layout, MatvecPlan, ObsSeries, QoISeries, SpaceTimeField, S
                      DimensionError, LayoutError, _buffer, _opts, check)
 
 
+def _kernel_data(k, what):
+    """(data, (rows, cols, nt)) of a BlockToeplitzKernel, a 3-D numpy array or
+    a 3-D CUDA tensor."""
+    if hasattr(k, "data") and hasattr(k, "n_time") and not hasattr(k, "dtype"):
+        return np.ascontiguousarray(k.data, dtype=np.float64).ravel(), (k.rows_out, k.n_cols, k.n_time)
+    if len(k.shape) != 3:
+        raise DimensionError("%s: kernel must be [rows][cols][nt]" % what)
+    shape = tuple(int(s) for s in k.shape)
+    if type(k).__module__.startswith("torch"):
+        return k.contiguous().view(-1), shape
+    return np.ascontiguousarray(k, dtype=np.float64).ravel(), shape
+
+
 @dataclass
 class MapResult:
     m_map: SpaceTimeField
@@ -105,6 +118,64 @@ class InferenceEngine:
             dist.all_gather_object(handles, bytes(mine), group=group)
             blob = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
             check(L.ltb_engine_connect(self._h, blob))
+
+    # ---- offline phase 2 on the device (bayes_engine.cpp:136-209) ----
+    def form_K(self, f_kernel, g_kernel=None, prior=None, sigma2=0.0):
+        """K = F G* + sigma2 I from the time-domain kernels (BlockToeplitzKernel,
+        numpy [rows][cols][nt] or CUDA tensor).  ``g_kernel`` None: G is the
+        Gamma_x premultiplied F, ``prior`` = (h_x, gamma, delta)."""
+        f, shape = _kernel_data(f_kernel, "form_K f")
+        g = None
+        if g_kernel is not None:
+            g, gshape = _kernel_data(g_kernel, "form_K g")
+            if gshape != shape:
+                raise DimensionError("form_K: F and G kernel dims differ")
+        elif prior is None:
+            raise ValueError("form_K: need g_kernel or prior=(h_x, gamma, delta)")
+        rows, cols, nt = shape
+        pf, kind, _a = _buffer(f, rows * cols * nt, "form_K f")
+        pg = None
+        if g is not None:
+            pg, kind_g, _b = _buffer(g, rows * cols * nt, "form_K g")
+            if kind_g != kind:
+                raise ValueError("form_K: f and g must both be host or both be device arrays")
+        p3 = (C.c_double * 3)(*prior) if prior is not None else None
+        check(_lib.load().ltb_engine_form_k(self._h, pf, pg, p3, rows, cols, nt, float(sigma2), kind))
+
+    def form_K_generated(self, seed, stream, prior, sigma2):
+        """form_K of the generated kernel (ltb_plan_create_generated's) and its
+        premultiplied G; prior = (h_x, gamma, delta)."""
+        h_x, gamma, delta = prior
+        check(_lib.load().ltb_engine_form_k_generated(self._h, int(seed), int(stream), float(h_x),
+                                                      float(gamma), float(delta), float(sigma2)))
+
+    def factorize(self):
+        """In-place Cholesky of K (bayes_engine.cpp:176-209)."""
+        check(_lib.load().ltb_engine_factorize(self._h))
+
+    def offline_ms(self):
+        a, b = C.c_double(), C.c_double()
+        check(_lib.load().ltb_engine_offline_ms(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def _export(self):
+        n = self.n_data()
+        out = np.empty((n, n), dtype=np.float64, order="F")
+        check(_lib.load().ltb_engine_export_lower(self._h, C.c_void_p(out.ctypes.data), n, 0))
+        return out
+
+    def K_lower(self):
+        """Lower triangle of K after form_K (zeros above)."""
+        return self._export()
+
+    def K(self):
+        """Symmetric K (bayes_engine.hpp K() accessor)."""
+        L = self._export()
+        return L + np.tril(L, -1).T
+
+    def chol_lower(self):
+        """The Cholesky factor (after factorize / set_factor)."""
+        return self._export()
 
     def solve_k_inplace(self, y, scratch=None):
         """bayes_engine.cpp:236-240: y <- K^{-1} y (numpy or CUDA tensor)."""
