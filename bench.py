@@ -14,7 +14,9 @@ value  = algorithmic bytes of the step over all ranks / max-over-ranks
 e2e    = same metric with pinned-host inputs copied in and results copied
          out inside the timed region (the user-facing API call);
 online = BASELINE config 2 (Nd=64, Nm=16384, Nt=128, Nq=8, n=8192):
-         posterior mean + forecast latency through InferenceEngine;
+         K formed (FP64 tensor cores) and factorized on the device
+         ("offline" sub-object), then posterior mean + forecast latency
+         through InferenceEngine;
 roofline = the GEMV kernels (the dominant stage) against the measured HBM
          copy bandwidth in MEASURED_PEAKS.json;
 cpu_baseline = the reference's own apply_raw / apply_adjoint_raw
@@ -193,10 +195,18 @@ def bench_online(ltb, torch, reps=20):
     """BASELINE config 2: posterior mean + forecast latency (device time)."""
     nd, nm, nt, seed = WORKLOADS["small"]
     nq = 8
-    g = ltb.MatvecPlan.generated(nd, nm, nt, seed=seed, tag=ltb.KernelTag.Gstar)
+    prior, sigma2 = (1.0, 2.0, 1.0), 1.0
+    # the whole model on the device: G* = Gamma_x-premultiplied generated F,
+    # then offline phase 2 (form_K on the FP64 tensor cores + tile Cholesky)
+    g = ltb.MatvecPlan.generated_premultiplied(nd, nm, nt, seed, prior, tag=ltb.KernelTag.F)
     fq = ltb.MatvecPlan.generated(nq, nm, nt, seed=seed, tag=ltb.KernelTag.Fq)
     eng = ltb.InferenceEngine(g, fq)
-    eng.set_factor_generated(seed)
+    offline = []
+    for _ in range(2):  # the second run is the reported one (first pays module / allocation setup)
+        eng.form_K_generated(seed, 1, prior, sigma2)
+        eng.factorize()
+        offline.append(eng.offline_ms())
+    fk_ms, fz_ms = offline[-1]
     d = torch.rand(nd * nt, dtype=torch.float64, device="cuda")
     m = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
     q = torch.empty(nq * nt, dtype=torch.float64, device="cuda")
@@ -232,13 +242,20 @@ def bench_online(ltb, torch, reps=20):
     n = nd * nt
     byts = 2 * 8 * (n * (n + 1) // 2) + algorithmic_bytes(nd, nm, nt) + algorithmic_bytes(nq, nm, nt)
     med = dev[len(dev) // 2]
-    out = {"config": "small inversion (Nd=64, Nm=16384, Nt=128, Nq=8, n=8192, synthetic factor)",
+    out = {"config": "small inversion (Nd=64, Nm=16384, Nt=128, Nq=8, n=8192; K formed and "
+                     "factorized on the device from the generated F and its prior-premultiplied G)",
            "latency_ms": med * 1e3, "latency_min_ms": dev[0] * 1e3,
            "e2e_ms": e2e[len(e2e) // 2] * 1e3,
            "bytes": byts, "achieved_gbs": byts / med / 1e9,
            "solve_k_ms": solve[len(solve) // 2] * 1e3,
            "gstar_ms": sum(gst["Fstar"]) / reps, "fq_ms": sum(fqt["F"]) / reps,
-           "paper_online_s": 0.2}
+           "paper_online_s": 0.2,
+           "offline": {"form_k_ms": fk_ms, "form_k_tflops": n * n * nm / (fk_ms * 1e-3) / 1e12,
+                       "form_k_flops": n * n * nm,
+                       "factorize_ms": fz_ms, "factorize_tflops": n ** 3 / 3 / (fz_ms * 1e-3) / 1e12,
+                       "unit": "FP64 (DMMA) TFLOP/s",
+                       "note": "lag-Gram contraction n^2 N_m (lower half, 2 flop/FMA) + diagonal recurrence; "
+                               "tile Cholesky n^3/3"}}
     eng.close()
     return out
 

@@ -239,60 +239,75 @@ __global__ void pad_identity_kernel(double* tiles, int n, int nb) {
 }
 
 // ---------------------------------------------------------------------------
-// (3) tile Cholesky.  Panel step k: each CTA holds [A_kk; A_ik] (128 x 64,
-// column-major, ld 129) in shared memory and runs the unscaled right-looking
-// elimination a_ij -= a_ic a_jc / d_c (d_c = a_cc), one barrier per column;
-// then L = a_ij / sqrt(d_j).  CTA 0 writes L_kk (strict upper zeroed), every
-// CTA writes its panel tile L_ik = A_ik L_kk^{-T}.
+// (3) tile Cholesky.  Panel step k: one CTA per panel tile row holds
+// [A_kk; A_ik] (128 rows x 64); thread (row, q) keeps the row's 16 entries
+// j = 4 t + q in registers.  Column c: the owners of column c publish a_rc
+// to shared memory, one barrier, then every row r > c eliminates
+// a_rj -= (a_rc / d_c) a_jc (c < j, j <= r on the diagonal block) from the
+// broadcast column (d_c = a_cc).  Finally L_rj = a_rj / sqrt(d_j),
+// L_jj = sqrt(d_j).  CTA 0 writes L_kk (strict upper zeroed), every CTA its
+// panel tile L_ik = A_ik L_kk^{-T}.
 // ---------------------------------------------------------------------------
-constexpr int kPL = 129;
-constexpr int kPanelThreads = 256;
-
-constexpr size_t kPanelSmem = (size_t)(kT * kPL + kT) * sizeof(double);
+constexpr int kPanelRows = 2 * kT;
+constexpr int kPanelSplit = 4;                 // threads per row
+constexpr int kPerThread = kT / kPanelSplit;   // 16 register entries
+constexpr int kPanelThreads = kPanelRows * kPanelSplit;
 
 __global__ void __launch_bounds__(kPanelThreads)
     chol_panel_kernel(double* __restrict__ tiles, int nb, int k, int* status) {
-  extern __shared__ double psm[];
-  double* sp = psm;          // [64 columns][129]: rows 0..63 = A_kk, 64..127 = A_ik
-  double* piv = psm + kT * kPL;
-  const int tid = threadIdx.x;
+  __shared__ double col[2][kPanelRows];
+  __shared__ double rsq[kT];
+  const int row = threadIdx.x % kPanelRows, q = threadIdx.x / kPanelRows;
   const int ip = k + 1 + blockIdx.x;  // panel tile row (none when ip >= nb)
+  const bool diag_row = row < kT;
   const bool has_panel = ip < nb;
-  const double* Dk = tiles + tile_at(k, k);
-  const double* Pk = has_panel ? tiles + tile_at(ip, k) : nullptr;
-  for (int e = tid; e < kTile; e += kPanelThreads) {
-    const int j = e >> 6, i = e & 63;
-    sp[j * kPL + i] = Dk[e];
-    sp[j * kPL + 64 + i] = has_panel ? Pk[e] : 0.0;
-  }
-  __syncthreads();
-  const int row = tid & 127, cg = tid >> 7;  // this thread: row `row`, columns c+1+cg, c+3+cg, ...
+  double* src = diag_row ? tiles + tile_at(k, k) + row
+                         : (has_panel ? tiles + tile_at(ip, k) + (row - kT) : nullptr);
+  double a[kPerThread];
+#pragma unroll
+  for (int t = 0; t < kPerThread; ++t) a[t] = src ? src[(kPanelSplit * t + q) * kT] : 0.0;
   bool bad = false;
+  const int jmax = diag_row ? row : kT - 1;
   for (int c = 0; c < kT; ++c) {
-    double d = sp[c * kPL + c];
+    if (q == (c & (kPanelSplit - 1))) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < kPerThread; ++t)
+        if (kPanelSplit * t + q == c) v = a[t];
+      col[c & 1][row] = v;
+    }
+    __syncthreads();
+    double d = col[c & 1][c];
     if (!(d > 0.0) || !isfinite(d)) {
       bad = true;
       d = 1.0;
     }
-    if (tid == 0) piv[c] = d;
     if (row > c) {
-      const double lic = sp[c * kPL + row] / d;
-      for (int j = c + 1 + cg; j < kT; j += 2) {
-        if (row < 64 && j > row) break;
-        sp[j * kPL + row] -= lic * sp[c * kPL + j];
+      const double lic = col[c & 1][row] / d;
+#pragma unroll
+      for (int t = 0; t < kPerThread; ++t) {
+        const int j = kPanelSplit * t + q;
+        if (j > c && j <= jmax) a[t] = fma(-lic, col[c & 1][j], a[t]);
       }
     }
-    __syncthreads();
   }
-  if (bad && blockIdx.x == 0 && tid == 0) atomicCAS(status, 0, k + 1);
-  // scale: L_ij = a_ij / sqrt(d_j)
-  double* Lk = tiles + tile_at(k, k);
-  double* Lp = has_panel ? tiles + tile_at(ip, k) : nullptr;
-  for (int e = tid; e < kTile; e += kPanelThreads) {
-    const int j = e >> 6, i = e & 63;
-    const double rs = 1.0 / sqrt(piv[j]);
-    if (blockIdx.x == 0) Lk[e] = i > j ? sp[j * kPL + i] * rs : (i == j ? sqrt(piv[j]) : 0.0);
-    if (has_panel) Lp[e] = sp[j * kPL + 64 + i] * rs;
+  // publish the pivots: owner (j, j % 4) of a_jj
+  if (diag_row && q == (row & (kPanelSplit - 1))) {
+    double v = 1.0;
+#pragma unroll
+    for (int t = 0; t < kPerThread; ++t)
+      if (kPanelSplit * t + q == row) v = a[t];
+    if (!(v > 0.0) || !isfinite(v)) v = 1.0;
+    rsq[row] = 1.0 / sqrt(v);
+  }
+  __syncthreads();
+  if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(status, 0, k + 1);
+  if (diag_row ? blockIdx.x == 0 : has_panel) {
+#pragma unroll
+    for (int t = 0; t < kPerThread; ++t) {
+      const int j = kPanelSplit * t + q;
+      src[j * kT] = !diag_row || j < row ? a[t] * rsq[j] : (j == row ? 1.0 / rsq[j] : 0.0);
+    }
   }
 }
 
@@ -416,14 +431,12 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   const int nb = t.nb;
   cudaError_t e = cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kUpdSmem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmem);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(t.status, 0, sizeof(int), st);
   int launches = 0;
   for (int k = 0; k < nb; ++k) {
     const int m = nb - k - 1;
-    chol_panel_kernel<<<std::max(1, m), kPanelThreads, kPanelSmem, st>>>(t.tiles, nb, k, t.status);
+    chol_panel_kernel<<<std::max(1, m), kPanelThreads, 0, st>>>(t.tiles, nb, k, t.status);
     ++launches;
     if (m > 0) {
       chol_update_kernel<<<(unsigned)((long long)m * (m + 1) / 2), kUpdThreads, kUpdSmem, st>>>(t.tiles, nb, k);
