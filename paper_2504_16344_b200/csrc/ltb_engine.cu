@@ -528,7 +528,7 @@ extern "C" ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned 
   if (!e) return efail(LTB_INVALID, "trsv_trace: null engine");
   Guard gd(e->device);
   if (!e->factorized) return efail(LTB_STATE, "trsv_trace: no factor");
-  const size_t need = 4 * (size_t)e->factor.nb + 1;
+  const size_t need = 8 * (size_t)e->factor.nb + 1;
   if (enable && !e->factor.trace) {
     ENG_CUDA(cudaMalloc(&e->factor.trace, need * sizeof(unsigned long long)));
     ENG_CUDA(cudaMemset(e->factor.trace, 0, need * sizeof(unsigned long long)));

@@ -14,8 +14,9 @@
 //     exist, stops kLook tiles short of the diagonal and hands the chain
 //     c_I = L_II^{-1} (b_I - sum_{J<I-kLook} L_IJ y_J);
 //   * the chain finishes y_I = c_I - sum_{k<=kLook} M_{I,k} y_{I-k}
-//     (M_{I,k} = L_II^{-1} L_{I,I-k} precomputed, prefetched into registers a
-//     step ahead, last kLook blocks of y kept in shared memory) and pushes
+//     (M_{I,k} = L_II^{-1} L_{I,I-k} precomputed, streamed by bulk async
+//     copies into a two-stage shared buffer, last kLook blocks of y kept in
+//     shared memory) and pushes
 //     y_I to every rank;
 //   * transposed sweep: block column I is spread over the ranks, so every
 //     rank's workers reduce their share s_h = sum_{J=h mod P, J>I+kLook}
@@ -101,6 +102,37 @@ LTB_DEV double poll_value(const double* p, int* status) {
   }
 }
 
+// Resolve N prefetched hand-off values at p[0], p[stride], ...: every
+// still-sentinel slot is re-loaded in the same round trip (the loads are
+// independent), so a block of values published together costs one memory
+// latency, not N.
+template <int N>
+LTB_DEV void poll_block(unsigned long long (&raw)[N], const double* p, int stride, int* status) {
+  bool miss = false;
+#pragma unroll
+  for (int k = 0; k < N; ++k) miss |= raw[k] == kSentinel;
+  if (!miss) return;
+  const unsigned long long t0 = globaltimer();
+  while (true) {
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      if (raw[k] == kSentinel) raw[k] = ld_relaxed_u64(p + (size_t)k * stride);
+    miss = false;
+#pragma unroll
+    for (int k = 0; k < N; ++k) miss |= raw[k] == kSentinel;
+    if (!miss) return;
+    if (*(volatile int*)status) break;
+    if (globaltimer() - t0 > kSpinNs) {
+      atomicExch(status, 1);
+      break;
+    }
+    __nanosleep(20);
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    if (raw[k] == kSentinel) raw[k] = 0ull;  // timed out: finish with zeros, host reports
+}
+
 struct RankView {
   const double* tiles;  // this rank's packed rows
   const double* dinv;   // all nb diagonal inverses
@@ -160,46 +192,63 @@ LTB_DEV void grid_barrier(unsigned* gsync) {
 }
 
 // ---------------- chain ------------------------------------------------------
-LTB_DEV void load_chain_tiles(const double* mtiles, int step, int nvalid, double (&m)[kLook][kCPT]) {
-  const int i = threadIdx.x & 63, q = threadIdx.x >> 6;
-#pragma unroll
-  for (int k = 0; k < kLook; ++k) {
-    if (k < nvalid) {
-      const double* M = mtiles + ((size_t)step * kLook + k) * kTile;
-#pragma unroll
-      for (int kk = 0; kk < kCPT; ++kk) m[k][kk] = __ldg(M + (kCPT * q + kk) * kTB + i);
-    }
+// The chain tiles of a step (kLook contiguous 32 KB tiles) arrive by ONE bulk
+// async copy (TMA 1-D) into a two-stage shared-memory buffer, issued a full
+// step ahead: register prefetches of the same data made every step wait on
+// the scoreboard of the NEXT step's loads (measured: ~1100 cycles per step
+// stalled in the FMA phase), async copies into shared memory do not.
+struct ChainRing {
+  double* stage;   // 2 stages x kLook tiles (dynamic shared memory)
+  uint64_t* full;  // 2 mbarriers
+};
+
+LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int step) {
+  if (threadIdx.x == 0) {
+    const int s = step & 1;
+    constexpr unsigned kBytes = kLook * kTile * sizeof(double);
+    mbar_arrive_expect_tx(cr.full + s, kBytes);
+    bulk_g2s(cr.stage + (size_t)s * kLook * kTile, mtiles + (size_t)step * kLook * kTile, kBytes,
+             cr.full + s, policy_evict_first());
   }
 }
 
-// The chain tiles of step I are loaded into registers one step ahead; the two
-// register sets (and the prefetched hand-offs) alternate through a manual 2x
-// unroll so a prefetch is first consumed one full step after it was issued.
 // Hand-off of step I: forward = cf[I] (one worker); transposed = sum over the
-// P ranks' cb[h][I].
+// P ranks' cb[h][I].  `cur` is this step's hand-off prefetched one step ago;
+// `nxt` receives the next one.
 template <bool kForward>
-LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, int I, int nvalid,
-                        const double (&m)[kLook][kCPT], unsigned long long cur,
-                        unsigned long long& nxt) {
+LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, int I, int nvalid,
+                        unsigned long long cur, unsigned long long& nxt) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
   const int nb = a.nb, P = kForward ? 1 : a.P;
   double* recv0 = a.loc[0].recv;  // the chain runs on rank 0 = local rank 0
   const double* cbuf = recv0 + (kForward ? off_cf(nb) : off_cb(nb));
   const int In = kForward ? I + 1 : I - 1;
+  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I] = clock64();
   // prefetch rank 0's hand-off of the next step (the others are polled)
   if (tid < kTB && In >= 0 && In < nb) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
+  // the step's tiles: stage I & 1, its (I >> 1)-th use
+  mbar_wait(cr.full + (I & 1), (unsigned)((kForward ? I : nb - 1 - I) >> 1) & 1);
+  const double* ms = cr.stage + (size_t)(I & 1) * kLook * kTile;
   double p = 0.0;
 #pragma unroll
   for (int k = 0; k < kLook; ++k) {
     if (k < nvalid) {
       const int src = kForward ? I - k - 1 : I + k + 1;
       const double* v = sm.ring[src % kLook] + kCPT * q;
+      const double* M = ms + (size_t)k * kTile + (size_t)kCPT * q * kTB + i;
 #pragma unroll
-      for (int kk = 0; kk < kCPT; ++kk) p = fma(m[k][kk], v[kk], p);
+      for (int kk = 0; kk < kCPT; ++kk) p = fma(M[kk * kTB], v[kk], p);
     }
   }
+  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
   sm.red[q][i] = p;
-  __syncthreads();
+  __syncthreads();  // also: every thread is done with stage I & 1
+  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
+  // refill the stage just consumed with the tiles of step I +- 2
+  {
+    const int I2 = kForward ? I + 2 : I - 2;
+    if (I2 >= 0 && I2 < nb) chain_issue(cr, kForward ? a.mf : a.mb, I2);
+  }
   if (tid < kTB) {
     unsigned long long raw[kMaxRanks];
     for (int h = 1; h < P; ++h) raw[h] = ld_relaxed_u64(cbuf + ((size_t)h * nb + I) * kTB + tid);
@@ -208,6 +257,7 @@ LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, int I, int nvalid,
     for (int h = 1; h < P; ++h)  // fixed order h = 0, 1, ..., P-1
       c += raw[h] != kSentinel ? __longlong_as_double((long long)raw[h])
                                : poll_value(cbuf + ((size_t)h * nb + I) * kTB + tid, a.status);
+    if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
     const double v = c - red_sum(sm.red, tid);
     const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + tid;
     for (int r = 0; r < a.P; ++r) a.peer[r][o] = v;  // push to every rank
@@ -217,32 +267,47 @@ LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, int I, int nvalid,
   if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
 }
 
-LTB_DEV void chain_forward(const DistArgs& a, ChainSmem& sm) {
-  double mA[kLook][kCPT], mB[kLook][kCPT];
-  unsigned long long cA = kSentinel, cB = kSentinel;
+// Both sweeps use the same two stages; every stage's mbarrier completes once
+// per use, so the forward sweep's uses (steps 0..nb-1) and the transposed
+// sweep's (nb-1..0) each start from parity 0 on a freshly initialised pair.
+LTB_DEV void chain_init(const ChainRing& cr) {
+  if (threadIdx.x == 0) {
+    mbar_init(cr.full, 1);
+    mbar_init(cr.full + 1, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+LTB_DEV void chain_forward(const DistArgs& a, ChainSmem& sm, const ChainRing& cr) {
+  chain_init(cr);
   auto nvalid = [&](int I) { return I < kLook ? I : kLook; };
+  chain_issue(cr, a.mf, 0);
+  if (a.nb > 1) chain_issue(cr, a.mf, 1);
+  unsigned long long cA = kSentinel, cB = kSentinel;
   for (int I = 0; I < a.nb; I += 2) {
-    if (I + 1 < a.nb) load_chain_tiles(a.mf, I + 1, nvalid(I + 1), mB);
-    chain_step<true>(a, sm, I, nvalid(I), mA, cA, cB);
-    if (I + 1 < a.nb) {
-      if (I + 2 < a.nb) load_chain_tiles(a.mf, I + 2, nvalid(I + 2), mA);
-      chain_step<true>(a, sm, I + 1, nvalid(I + 1), mB, cB, cA);
-    }
+    chain_step<true>(a, sm, cr, I, nvalid(I), cA, cB);
+    if (I + 1 < a.nb) chain_step<true>(a, sm, cr, I + 1, nvalid(I + 1), cB, cA);
   }
 }
 
-LTB_DEV void chain_transposed(const DistArgs& a, ChainSmem& sm) {
-  double mA[kLook][kCPT], mB[kLook][kCPT];
-  unsigned long long cA = kSentinel, cB = kSentinel;
+LTB_DEV void chain_transposed(const DistArgs& a, ChainSmem& sm, const ChainRing& cr) {
   const int nb = a.nb;
+  // fresh barriers for the second sweep (all forward copies were consumed)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(cr.full)) : "memory");
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(cr.full + 1)) : "memory");
+  }
+  chain_init(cr);
   auto nvalid = [&](int I) { return nb - 1 - I < kLook ? nb - 1 - I : kLook; };
+  // stage of step I is I & 1; use index (nb - 1 - I) >> 1 of that stage
+  chain_issue(cr, a.mb, nb - 1);
+  if (nb > 1) chain_issue(cr, a.mb, nb - 2);
+  unsigned long long cA = kSentinel, cB = kSentinel;
   for (int I = nb - 1; I >= 0; I -= 2) {
-    if (I - 1 >= 0) load_chain_tiles(a.mb, I - 1, nvalid(I - 1), mB);
-    chain_step<false>(a, sm, I, nvalid(I), mA, cA, cB);
-    if (I - 1 >= 0) {
-      if (I - 2 >= 0) load_chain_tiles(a.mb, I - 2, nvalid(I - 2), mA);
-      chain_step<false>(a, sm, I - 1, nvalid(I - 1), mB, cB, cA);
-    }
+    chain_step<false>(a, sm, cr, I, nvalid(I), cA, cB);
+    if (I - 1 >= 0) chain_step<false>(a, sm, cr, I - 1, nvalid(I - 1), cB, cA);
   }
 }
 
@@ -277,6 +342,7 @@ LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSme
     for (int J = 0; J < jmax && J < kRing; ++J) ring_issue(ring, g0 + J, row + (size_t)J * kTile, policy);
   const double* D = rv.dinv + (size_t)I * kTile;
   for (int e = tid; e < kTile; e += kThreads) sm.sD[(e >> 6) * kPad + (e & 63)] = __ldg(D + e);
+  const double bI = tid < kTB ? __ldg(rv.b + (size_t)I * kTB + tid) : 0.0;  // off the tail
   double acc = 0.0;
   unsigned long long yraw[kCPT];
   if (jmax > 0) {
@@ -285,11 +351,10 @@ LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSme
   }
   for (int J = 0; J < jmax; ++J) {
     // resolve this tile's solution block (prefetched one tile ago)
+    poll_block<kCPT>(yraw, yf + (size_t)J * kTB + kCPT * q, 1, a.status);
     double yv[kCPT];
 #pragma unroll
-    for (int k = 0; k < kCPT; ++k)
-      yv[k] = yraw[k] != kSentinel ? __longlong_as_double((long long)yraw[k])
-                                   : poll_value(yf + (size_t)J * kTB + kCPT * q + k, a.status);
+    for (int k = 0; k < kCPT; ++k) yv[k] = __longlong_as_double((long long)yraw[k]);
     if (J + 1 < jmax) {
 #pragma unroll
       for (int k = 0; k < kCPT; ++k) yraw[k] = ld_relaxed_u64(yf + (size_t)(J + 1) * kTB + kCPT * q + k);
@@ -305,7 +370,7 @@ LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSme
   ring.next = g0 + (jmax > 0 ? jmax : 0);
   sm.red[q][i] = acc;
   __syncthreads();
-  if (tid < kTB) sm.rr[tid] = __ldg(rv.b + (size_t)I * kTB + tid) - red_sum(sm.red, tid);
+  if (tid < kTB) sm.rr[tid] = bI - red_sum(sm.red, tid);
   __syncthreads();
   double s = 0.0;
 #pragma unroll
@@ -437,8 +502,11 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && a.r0 == 0) a.trace[4 * nb] = globaltimer();
 
   if (r == 0 && lc == 0) {
-    chain_forward(a, sm.chain);
-    chain_transposed(a, sm.chain);
+    ChainRing cr;
+    cr.stage = reinterpret_cast<double*>(ring_smem);
+    cr.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kRing * kTile * sizeof(double));
+    chain_forward(a, sm.chain, cr);
+    chain_transposed(a, sm.chain, cr);
   } else {
     TileRing ring;
     ring.stage = reinterpret_cast<double*>(ring_smem);
@@ -468,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
 }
 
 constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
+static_assert(2 * kLook <= kRing, "the chain's two tile stages live in the worker ring's space");
 
 // ---------------- setup kernels ----------------------------------------------
 // local tile index t of rank r -> (I, J)
