@@ -98,13 +98,21 @@ LTB_DEV void gram_load_stage(double* sA, double* sB, const double* f, const doub
   }
 }
 
+// split == 1: CTA b computes lower 128-tile tile0 + b over all of N_m and
+// writes it into the packed tiles.  split > 1 (the last, partial wave): CTA b
+// computes k-slice b % split of tile tile0 + b / split into `partial`
+// ([tile][slice][128 x 128]); reduce_partials_kernel sums the slices in
+// order (deterministic) and scatters them.
 template <bool kPair>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     lag_gram_kernel(const double* __restrict__ f, const double* __restrict__ g, int nm, int nt,
-                    int n, int nb, double* __restrict__ tiles) {
+                    int n, int nb, double* __restrict__ tiles, long long tile0, int split,
+                    double* __restrict__ partial) {
   extern __shared__ __align__(16) double gsm[];
+  const long long tile = tile0 + blockIdx.x / split;
+  const int slice = blockIdx.x % split;
   int bi, bj;
-  tri_pair(blockIdx.x, &bi, &bj);
+  tri_pair(tile, &bi, &bj);
   const int i0 = bi * kBM, j0 = bj * kBM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
@@ -128,12 +136,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
 
-  const int nk = (nm + kBK - 1) / kBK;
+  const int nk_all = (nm + kBK - 1) / kBK;
+  const int kb = (int)((long long)slice * nk_all / split);
+  const int nk = (int)((long long)(slice + 1) * nk_all / split) - kb;  // this CTA's k-chunks
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
     if (s < nk) {
       double* st = gsm + s * kStageDoubles;
-      gram_load_stage<kPair>(st, st + kBK * kSS, f, g, rowA, rowB, s * kBK, nm, nt);
+      gram_load_stage<kPair>(st, st + kBK * kSS, f, g, rowA, rowB, (kb + s) * kBK, nm, nt);
     }
     cp_commit();
   }
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int nx = kt + kStages - 1;
       if (nx < nk) {
         double* st = gsm + (nx % kStages) * kStageDoubles;
-        gram_load_stage<kPair>(st, st + kBK * kSS, f, g, rowA, rowB, nx * kBK, nm, nt);
+        gram_load_stage<kPair>(st, st + kBK * kSS, f, g, rowA, rowB, (kb + nx) * kBK, nm, nt);
       }
       cp_commit();
     }
@@ -169,6 +179,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   cp_wait<0>();
 
+  if (split > 1) {
+    // partial 128x128 block, row-major [m][n]
+    double* P = partial + ((size_t)(blockIdx.x / split) * split + slice) * kBM * kBM;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt8 = 0; nt8 < 4; ++nt8)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int m = wm * 64 + mt * 16 + gq + 8 * h, c = wn * 32 + nt8 * 8 + 2 * tq;
+          *reinterpret_cast<double2*>(P + (size_t)m * kBM + c) =
+              make_double2(acc[mt][nt8][2 * h], acc[mt][nt8][2 * h + 1]);
+        }
+    return;
+  }
   // epilogue: scatter into the packed 64x64 tiles (skip J > I and I >= nb)
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
@@ -183,6 +208,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int I = i >> 6, J = j >> 6;
           if (I < nb && J <= I) tiles[tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63)] = acc[mt][nt8][2 * h + c];
         }
+}
+
+// sum the k-slices of the split tiles in slice order, scatter like the
+// data-parallel epilogue
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, long long tile0, int split,
+                                       int nb, double* __restrict__ tiles) {
+  const long long t = blockIdx.y;
+  int bi, bj;
+  tri_pair(tile0 + t, &bi, &bj);
+  const double* P = partial + (size_t)t * split * kBM * kBM;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kBM * kBM; e += gridDim.x * blockDim.x) {
+    const int m = e / kBM, c = e % kBM;
+    double v = 0.0;
+    for (int s = 0; s < split; ++s) v += P[(size_t)s * kBM * kBM + e];
+    const int i = bi * kBM + m, j = bj * kBM + c;
+    const int I = i >> 6, J = j >> 6;
+    if (I < nb && J <= I) tiles[tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63)] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -408,21 +451,39 @@ cudaError_t formk_device(TriFactor& t, const double* f, const double* g, int nd,
   const long long nbm = (n + kBM - 1) / kBM;
   const long long ctas = nbm * (nbm + 1) / 2;
   const bool pair = (nt % 2 == 0) && ((uintptr_t)f % 16 == 0) && ((uintptr_t)g % 16 == 0);
-  cudaError_t e;
-  if (pair) {
-    e = cudaFuncSetAttribute(lag_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+  auto kern = pair ? lag_gram_kernel<true> : lag_gram_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+  if (e != cudaSuccess) return e;
+  // one CTA per SM: full waves data-parallel; a short last wave (<= half the
+  // SMs) is split along N_m instead so it does not cost a whole wave
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long rem = ctas % sms;
+  int split = rem > 0 && rem <= sms / 2 && ctas > sms ? (int)std::min<long long>(sms / rem, (nm + kBK - 1) / kBK) : 1;
+  if (split < 2) rem = 0;
+  double* partial = nullptr;
+  if (rem) {
+    e = cudaMallocAsync(&partial, (size_t)rem * split * kBM * kBM * sizeof(double), st);
     if (e != cudaSuccess) return e;
-    lag_gram_kernel<true><<<(unsigned)ctas, kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles);
-  } else {
-    e = cudaFuncSetAttribute(lag_gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-    if (e != cudaSuccess) return e;
-    lag_gram_kernel<false><<<(unsigned)ctas, kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles);
+  }
+  g_last_launches = 0;
+  if (ctas - rem > 0) {
+    kern<<<(unsigned)(ctas - rem), kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles, 0, 1, nullptr);
+    ++g_last_launches;
+  }
+  if (rem) {
+    kern<<<(unsigned)(rem * split), kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles, ctas - rem,
+                                                                    split, partial);
+    reduce_partials_kernel<<<dim3(16, (unsigned)rem), 256, 0, st>>>(partial, ctas - rem, split, nb, t.tiles);
+    cudaFreeAsync(partial, st);
+    g_last_launches += 2;
   }
   const long long diags = (long long)nd * (nd + 1) / 2 * (2ll * nt - 1);
   const unsigned pblocks = (unsigned)std::max(1ll, std::min(148ll * 32, (diags + 255) / 256));
   diag_prefix_kernel<<<pblocks, 256, 0, st>>>(t.tiles, nd, nt, sigma2);
   pad_identity_kernel<<<1, kT, 0, st>>>(t.tiles, n, nb);
-  g_last_launches = 3;
+  g_last_launches += 2;
   return cudaGetLastError();
 }
 

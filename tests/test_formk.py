@@ -132,11 +132,12 @@ def test_factorize_diagonal_and_state(ltb):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("nd,nm,nt", [(3, 4, 6), (8, 300, 50), (5, 64, 33), (16, 1024, 64),
-                                      (2, 40, 129)])
+                                      (2, 40, 129), (20, 64, 128)])
 def test_form_k_factorize_vs_oracle(ltb, nd, nm, nt):
     """K (DMMA lag Gram + diagonal recurrence) vs the oracle's column-by-
     column FFT assembly; L vs the oracle Cholesky; ragged n, odd N_t (8-byte
-    operand path), N_m not a multiple of the 16-wide k-stage."""
+    operand path), N_m not a multiple of the 16-wide k-stage, and (n = 2560:
+    210 CTA tiles) the split-k last wave."""
     rng = np.random.default_rng(nd * 1000 + nm + nt)
     s2 = 0.3
     f = lti_like(rng, nd, nm, nt)
