@@ -226,8 +226,30 @@ ltb_status ltb_engine_form_k_generated(ltb_engine* e, uint64_t seed, uint64_t st
  * DMMA trailing updates); LTB_NUMERICAL if K is not positive definite,
  * LTB_STATE without form_K.  Afterwards the engine is ready to solve. */
 ltb_status ltb_engine_factorize(ltb_engine* e);
-/* device milliseconds of the last form_K / factorize (either nullable) */
-ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms);
+/* form_Q + form_qoi_cov (bayes_engine.cpp:242-285) on the device, after
+ * factorize / set_factor: R = F Gq* and the prior QoI covariance P = Fq Gq*
+ * (the form_K contraction, rectangular), K^{-1} R by multi-RHS block
+ * substitution on the packed factor (FP64 tensor cores),
+ * Gamma_post_q = sym(P - R^T K^{-1} R) (as (L^{-1}R)^T (L^{-1}R)), Q = (K^{-1}R)^T;
+ * then the Phase-3 operator is installed exactly as by set_phase3.  Kernels
+ * [rows][N_m][N_t]: F (rows N_d), F_q and its premultiplied Gq (rows N_q;
+ * gq NULL: premultiplied on the device with prior3).  LTB_NUMERICAL for a
+ * negative posterior variance beyond -1e-10 ||Gamma_post_q|| (:276-282). */
+ltb_status ltb_engine_form_q(ltb_engine* e, const double* f_kernel, const double* fq_kernel,
+                             const double* gq_kernel, const double* prior3, int nd, int nq, int nm,
+                             int nt, int ptr_kind);
+/* generated F (stream_f) and F_q (stream_fq) kernels, Gq premultiplied */
+ltb_status ltb_engine_form_q_generated(ltb_engine* e, uint64_t seed, uint64_t stream_f,
+                                       uint64_t stream_fq, int nq, double h_x, double gamma,
+                                       double delta);
+/* Q (N_q N_t x N_d N_t, column-major, ldq) and, after form_Q, the full
+ * Gamma_post_q and prior QoI covariance (m x m, ldg); any output nullable
+ * (the Q() / gamma_post_q() / prior_qoi_cov() accessors, :287-306) */
+ltb_status ltb_engine_export_phase3(const ltb_engine* e, double* Q, size_t ldq, double* gpost,
+                                    double* prior_cov, size_t ldg, int ptr_kind);
+/* device milliseconds of the last form_K / factorize / form_Q (nullable) */
+ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms,
+                                 double* formq_ms);
 /* K (after form_K) or L (after factorize / set_factor) as an n x n
  * column-major matrix with leading dimension ld: lower triangle, zeros
  * above (the reference's K() / chol_lower() accessors) */

@@ -695,3 +695,57 @@ int orc_cholesky(double* A, int n, size_t ld) {
     for (int i = 0; i < j; ++i) A[(size_t)j * ld + i] = 0.0;
   return 0;
 }
+
+int orc_form_q(const double* f_rck, const double* fq_rck, const double* gq_rck, int nd, int nq,
+               int nm, int nt, const double* L, double* Q, double* gpost, double* prior_cov) {
+  const int n = nd * nt, m = nq * nt;
+  orc_plan* pf = NULL;
+  orc_plan* pfq = NULL;
+  if (orc_plan_create(f_rck, nd, nm, nt, &pf) != 0) return 1;
+  if (orc_plan_create(fq_rck, nq, nm, nt, &pfq) != 0) {
+    orc_plan_destroy(pf);
+    return 1;
+  }
+  double* R = (double*)malloc(sizeof(double) * (size_t)n * m);
+  double* X = (double*)malloc(sizeof(double) * (size_t)n * m);
+  double* gcol = (double*)malloc(sizeof(double) * (size_t)nm * nt);
+  for (int i = 0; i < m; ++i) { /* :244-249 */
+    read_gstar_column(gq_rck, nm, nt, i, gcol);
+    orc_apply_raw(pf, gcol, R + (size_t)i * n);
+  }
+  memcpy(X, R, sizeof(double) * (size_t)n * m);
+  for (int i = 0; i < m; ++i) orc_solve_k(L, n, (size_t)n, X + (size_t)i * n); /* :250-255 */
+  for (int i = 0; i < m; ++i) /* q_ = x_solve_^T (:256) */
+    for (int j = 0; j < n; ++j) Q[(size_t)j * m + i] = X[(size_t)i * n + j];
+  for (int i = 0; i < m; ++i) { /* :266-270 */
+    read_gstar_column(gq_rck, nm, nt, i, gcol);
+    orc_apply_raw(pfq, gcol, prior_cov + (size_t)i * m);
+  }
+  for (int i = 0; i < m; ++i) /* :271 symmetrise */
+    for (int j = 0; j < i; ++j) {
+      const double v = 0.5 * (prior_cov[(size_t)j * m + i] + prior_cov[(size_t)i * m + j]);
+      prior_cov[(size_t)j * m + i] = v;
+      prior_cov[(size_t)i * m + j] = v;
+    }
+  for (int j = 0; j < m; ++j) /* :273 gamma_post_q = prior - R^T X */
+    for (int i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < n; ++k) acc += R[(size_t)i * n + k] * X[(size_t)j * n + k];
+      gpost[(size_t)j * m + i] = prior_cov[(size_t)j * m + i] - acc;
+    }
+  double nrm = 0.0, min_diag = 0.0;
+  for (int i = 0; i < m; ++i) /* :274 symmetrise */
+    for (int j = 0; j < i; ++j) {
+      const double v = 0.5 * (gpost[(size_t)j * m + i] + gpost[(size_t)i * m + j]);
+      gpost[(size_t)j * m + i] = v;
+      gpost[(size_t)i * m + j] = v;
+    }
+  for (size_t e = 0; e < (size_t)m * m; ++e) nrm += gpost[e] * gpost[e];
+  for (int i = 0; i < m; ++i) min_diag = i == 0 || gpost[(size_t)i * m + i] < min_diag ? gpost[(size_t)i * m + i] : min_diag;
+  free(R);
+  free(X);
+  free(gcol);
+  orc_plan_destroy(pf);
+  orc_plan_destroy(pfq);
+  return min_diag < -1e-10 * sqrt(nrm) ? 2 : 0; /* :276-282 */
+}

@@ -123,6 +123,15 @@ int orc_form_k(const double* f_rck, const double* g_rck, int rows, int nm, int n
  * Returns 0, or j + 1 for a non-positive pivot in column j. */
 int orc_cholesky(double* A, int n, size_t ld);
 
+/* form_Q + form_qoi_cov (bayes_engine.cpp:242-285): with n = nd * nt,
+ * m = nq * nt, R = F Gq* (column i = plan_F.apply(read_gstar_column(gq, i))),
+ * X = K^{-1} R (solve_k per column, factor L column-major ld n),
+ * Q = X^T (m x n, column-major ld m); P = Fq Gq* symmetrised (m x m);
+ * Gamma_post_q = P - R^T X symmetrised (m x m).  Returns 0, or 2 when a
+ * diagonal entry of Gamma_post_q < -1e-10 ||Gamma_post_q||_F. */
+int orc_form_q(const double* f_rck, const double* fq_rck, const double* gq_rck, int nd, int nq,
+               int nm, int nt, const double* L, double* Q, double* gpost, double* prior_cov);
+
 /* ---- online phase (bayes_engine.cpp:307-338) ---- */
 /* m_map = G* K^{-1} d: y = copy(d); solve_k(y); m = plan_g.apply_adjoint(y) */
 void orc_infer_map(const double* L, size_t ld, const orc_plan* plan_g,

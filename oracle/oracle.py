@@ -71,6 +71,7 @@ def lib():
         L.orc_form_k.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                  _dp, _dp]
         L.orc_cholesky.argtypes = [_dp, C.c_int, C.c_size_t]
+        L.orc_form_q.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp]
         L.orc_fft_create.argtypes = [C.c_int]
         L.orc_fft_create.restype = C.c_void_p
         L.orc_fft_destroy.argtypes = [C.c_void_p]
@@ -305,6 +306,28 @@ def cholesky(A):
     if st != 0:
         raise ValueError("factorize: K not positive definite (column %d)" % (st - 1))
     return np.ascontiguousarray(L)
+
+
+def form_q(f_rck, fq_rck, gq_rck, L):
+    """(Q, Gamma_post_q, prior_qoi_cov) of form_Q + form_qoi_cov
+    (bayes_engine.cpp:242-285) restated; L is the (n, n) factor."""
+    f = np.ascontiguousarray(f_rck, dtype=np.float64)
+    fq = np.ascontiguousarray(fq_rck, dtype=np.float64)
+    gq = np.ascontiguousarray(gq_rck, dtype=np.float64)
+    nd, nm, nt = f.shape
+    nq = fq.shape[0]
+    n, m = nd * nt, nq * nt
+    Lc = np.asfortranarray(L, dtype=np.float64)
+    Q = np.empty(m * n)
+    gp = np.empty(m * m)
+    pc = np.empty(m * m)
+    st = lib().orc_form_q(_ptr(f), _ptr(fq), _ptr(gq), nd, nq, nm, nt, Lc.ctypes.data_as(_dp),
+                          _ptr(Q), _ptr(gp), _ptr(pc))
+    if st == 2:
+        raise ValueError("form_qoi_cov: negative posterior QoI variance beyond tolerance")
+    if st != 0:
+        raise RuntimeError("orc_form_q status %d" % st)
+    return (Q.reshape(n, m).T.copy(), gp.reshape(m, m).T.copy(), pc.reshape(m, m).T.copy())
 
 
 def rel_err(a, b):

@@ -76,7 +76,7 @@ struct ltb_engine {
   TriFactor factor;
   bool factorized = false;
   bool kformed = false;          // factor.tiles hold K (form_K), not yet factorized
-  double formk_ms = 0.0, factorize_ms = 0.0;
+  double formk_ms = 0.0, factorize_ms = 0.0, formq_ms = 0.0;
   double* ypad = nullptr;       // nb * 64
   double* stage_in = nullptr;   // host-pointer staging: d (nd*nt)
   double* stage_m = nullptr;    // m_map (nm*nt)
@@ -407,10 +407,12 @@ ltb_status ltb_engine_factorize(ltb_engine* e) {
   return factor_finish(e, trsv_prepare_packed(e->factor, 0));
 }
 
-ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms) {
+ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms,
+                                 double* formq_ms) {
   if (!e) return efail(LTB_INVALID, "offline_ms: null engine");
   if (formk_ms) *formk_ms = e->formk_ms;
   if (factorize_ms) *factorize_ms = e->factorize_ms;
+  if (formq_ms) *formq_ms = e->formq_ms;
   return LTB_OK;
 }
 
@@ -690,8 +692,12 @@ struct QoIOperator {
   double* lo = nullptr;
   double* hi = nullptr;
   double* stage = nullptr;                // host-pointer staging for d
+  double* gpost = nullptr;                // full Gamma_post_q (form_Q only), m x m
+  double* prior_cov = nullptr;            // Fq Gq* (form_Q only), m x m
   GemvShape shape{};
   void release() {
+    cudaFree(gpost);
+    cudaFree(prior_cov);
     cudaFree(Q);
     cudaFree(gdiag);
     cudaFree(x);
@@ -976,4 +982,168 @@ extern "C" ltb_status ltb_engine_load_phase3_dnsm(ltb_engine* e, const char* q_p
   }
   fclose(fg);
   return ltb_engine_set_phase3(e, qcm.data(), rows, diag.data(), LTB_PTR_HOST);
+}
+
+// ---- form_Q + form_qoi_cov on the device (bayes_engine.cpp:242-285) ----
+namespace {
+
+struct DevArr {
+  double* p = nullptr;
+  ~DevArr() { cudaFree(p); }
+  cudaError_t alloc(size_t n, bool zero = false) {
+    cudaError_t e = cudaMalloc(&p, n * sizeof(double));
+    if (e == cudaSuccess && zero) e = cudaMemset(p, 0, n * sizeof(double));
+    return e;
+  }
+};
+
+// R, P, K^{-1} R, Gamma_post_q and Q from device kernels f [nd][nm][nt],
+// fq / gq [nq][nm][nt]; installs the Phase-3 operator (as set_phase3)
+ltb_status form_q_dev(ltb_engine* e, const double* f, const double* fq, const double* gq, int nq) {
+  const int nd = e->nd, nm = e->nm, nt = e->nt;
+  const int n = nd * nt, m = nq * nt;
+  const size_t ld = (size_t)e->factor.nb * kTB;
+  const int m_pad = (m + 63) / 64 * 64;
+  DevArr R, X, P, YtY, gpost, gdiag, Q, work, nrm;
+  ENG_CUDA(R.alloc(ld * m_pad, true));
+  ENG_CUDA(X.alloc(ld * m_pad, true));
+  ENG_CUDA(P.alloc((size_t)m * m));
+  ENG_CUDA(YtY.alloc((size_t)m * m));
+  ENG_CUDA(gpost.alloc((size_t)m * m + 1, true));
+  ENG_CUDA(gdiag.alloc(m));
+  ENG_CUDA(Q.alloc((size_t)m * n));
+  ENG_CUDA(work.alloc(2048));
+  ENG_CUDA(nrm.alloc(1));
+  ENG_CUDA(cudaEventRecord(e->ev0, 0));
+  int launches = 0;
+  cudaError_t err = block_toeplitz_product(f, nd, gq, nq, nm, nt, R.p, ld, 0);  // R = F Gq* (:244-249)
+  launches += formk_last_launches();
+  if (err == cudaSuccess) err = block_toeplitz_product(fq, nq, gq, nq, nm, nt, P.p, m, 0);  // :266-270
+  launches += formk_last_launches();
+  if (err == cudaSuccess) err = symmetrize(P.p, m, 0);  // :271
+  if (err == cudaSuccess) err = trsm_solve_k(e->factor, R.p, X.p, ld, m_pad, YtY.p, m, 0);  // :250-255
+  launches += formk_last_launches() + 1;
+  if (err == cudaSuccess) err = qoi_covariance(P.p, YtY.p, m, gpost.p, gdiag.p, 0);  // :273-274
+  if (err == cudaSuccess) err = transpose_to(R.p, ld, n, m, Q.p, 0);  // q_ = x_solve_^T (:256)
+  if (err == cudaSuccess)  // ||Gamma_post_q||_F^2 (the buffer has an even length, last entry 0)
+    err = launch_sqnorm(reinterpret_cast<const double2*>(gpost.p), ((long long)m * m + 1) / 2, work.p, nrm.p, 0);
+  launches += 4;
+  count_launches(launches);
+  if (err != cudaSuccess) return efail(LTB_CUDA, "form_Q: %s", cudaGetErrorString(err));
+  ENG_CUDA(cudaEventRecord(e->ev1, 0));
+  ENG_CUDA(cudaEventSynchronize(e->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  // :276-282 negative posterior variance check
+  std::vector<double> diag(m);
+  double n2 = 0.0;
+  ENG_CUDA(cudaMemcpy(diag.data(), gdiag.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  ENG_CUDA(cudaMemcpy(&n2, nrm.p, sizeof(double), cudaMemcpyDeviceToHost));
+  const double scale = std::sqrt(n2);
+  const double min_diag = *std::min_element(diag.begin(), diag.end());
+  if (min_diag < -1e-10 * scale)
+    return efail(LTB_NUMERICAL, "form_qoi_cov: negative posterior QoI variance beyond tolerance (%g vs norm %g)",
+                 min_diag, scale);
+  if (e->nq == 0) e->nq = nq;
+  ltb_status st = ltb_engine_set_phase3(e, Q.p, (size_t)m, gdiag.p, LTB_PTR_DEVICE);
+  if (st != LTB_OK) return st;
+  {
+    std::lock_guard<std::mutex> lk(g_qoi_mu);
+    QoIOperator& op = g_qoi[e];
+    op.gpost = gpost.p;
+    op.prior_cov = P.p;
+    gpost.p = nullptr;  // ownership moves to the operator
+    P.p = nullptr;
+  }
+  e->formq_ms = ms;
+  return LTB_OK;
+}
+
+ltb_status form_q_check(ltb_engine* e, int nq) {
+  if (!e->factorized) return efail(LTB_STATE, "engine: missing offline artifact: Cholesky factor (run factorize)");
+  if (e->world > 1) return efail(LTB_STATE, "form_Q: single-GPU engines only");
+  if (nq < 1) return efail(LTB_DIMENSION, "form_Q: N_q must be >= 1");
+  if (e->nq && nq != e->nq) return efail(LTB_DIMENSION, "form_Q: N_q (%d) differs from the F_q plan (%d)", nq, e->nq);
+  return LTB_OK;
+}
+
+}  // namespace
+
+extern "C" ltb_status ltb_engine_form_q(ltb_engine* e, const double* f_kernel, const double* fq_kernel,
+                                        const double* gq_kernel, const double* prior3, int nd, int nq,
+                                        int nm, int nt, int ptr_kind) {
+  if (!e || !f_kernel || !fq_kernel) return efail(LTB_INVALID, "form_Q: null argument");
+  if (!gq_kernel && !prior3) return efail(LTB_INVALID, "form_Q: need the Gq kernel or the prior (prior3)");
+  ltb_status st = form_q_check(e, nq);
+  if (st != LTB_OK) return st;
+  if (nd != e->nd || nt != e->nt || nm != e->nm)
+    return efail(LTB_DIMENSION, "form_Q: kernel dims do not match the engine");
+  Guard gd(e->device);
+  const size_t cf = (size_t)nd * nm * nt, cq = (size_t)nq * nm * nt;
+  DevArr df, dfq, dgq;
+  const double* f = f_kernel;
+  const double* fq = fq_kernel;
+  const double* gq = gq_kernel;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(df.alloc(cf));
+    ENG_CUDA(cudaMemcpy(df.p, f_kernel, cf * sizeof(double), cudaMemcpyHostToDevice));
+    ENG_CUDA(dfq.alloc(cq));
+    ENG_CUDA(cudaMemcpy(dfq.p, fq_kernel, cq * sizeof(double), cudaMemcpyHostToDevice));
+    f = df.p;
+    fq = dfq.p;
+  }
+  if (!gq_kernel) {
+    ENG_CUDA(dgq.alloc(cq));
+    ENG_CUDA(cudaMemcpy(dgq.p, fq, cq * sizeof(double), cudaMemcpyDeviceToDevice));
+    if ((st = premultiply_device(dgq.p, nq, nm, nt, prior3[0], prior3[1], prior3[2])) != LTB_OK) return st;
+    gq = dgq.p;
+  } else if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(dgq.alloc(cq));
+    ENG_CUDA(cudaMemcpy(dgq.p, gq_kernel, cq * sizeof(double), cudaMemcpyHostToDevice));
+    gq = dgq.p;
+  }
+  if ((st = check_finite_device(f, (long long)cf, "engine F")) != LTB_OK) return st;
+  if ((st = check_finite_device(fq, (long long)cq, "engine Fq")) != LTB_OK) return st;
+  return form_q_dev(e, f, fq, gq, nq);
+}
+
+extern "C" ltb_status ltb_engine_form_q_generated(ltb_engine* e, uint64_t seed, uint64_t stream_f,
+                                                  uint64_t stream_fq, int nq, double h_x, double gamma,
+                                                  double delta) {
+  if (!e) return efail(LTB_INVALID, "form_Q: null engine");
+  ltb_status st = form_q_check(e, nq);
+  if (st != LTB_OK) return st;
+  Guard gd(e->device);
+  const size_t cf = (size_t)e->nd * e->nm * e->nt, cq = (size_t)nq * e->nm * e->nt;
+  DevArr df, dfq, dgq;
+  ENG_CUDA(df.alloc(cf));
+  ENG_CUDA(dfq.alloc(cq));
+  ENG_CUDA(dgq.alloc(cq));
+  ENG_CUDA(launch_gen_fill(gen_key(seed, stream_f), 0, (long long)cf, df.p, 0));
+  ENG_CUDA(launch_gen_fill(gen_key(seed, stream_fq), 0, (long long)cq, dfq.p, 0));
+  count_launches(2);
+  ENG_CUDA(cudaMemcpy(dgq.p, dfq.p, cq * sizeof(double), cudaMemcpyDeviceToDevice));
+  if ((st = premultiply_device(dgq.p, nq, e->nm, e->nt, h_x, gamma, delta)) != LTB_OK) return st;
+  return form_q_dev(e, df.p, dfq.p, dgq.p, nq);
+}
+
+extern "C" ltb_status ltb_engine_export_phase3(const ltb_engine* e, double* Q, size_t ldq, double* gpost,
+                                               double* prior_cov, size_t ldg, int ptr_kind) {
+  if (!e) return efail(LTB_INVALID, "export_phase3: null engine");
+  Guard gd(e->device);
+  std::lock_guard<std::mutex> lk(g_qoi_mu);
+  auto it = g_qoi.find(e);
+  if (it == g_qoi.end() || !it->second.Q)
+    return efail(LTB_STATE, "engine: missing offline artifact: Phase-3 artifacts (run form_Q/form_qoi_cov)");
+  const QoIOperator& op = it->second;
+  const size_t m = (size_t)op.rows;
+  if ((Q && ldq < m) || ((gpost || prior_cov) && ldg < m))
+    return efail(LTB_DIMENSION, "export_phase3: leading dimension too small");
+  if ((gpost || prior_cov) && !op.gpost)
+    return efail(LTB_STATE, "export_phase3: Gamma_post_q / prior QoI covariance exist only after form_Q");
+  const cudaMemcpyKind k = ptr_kind == LTB_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (Q) ENG_CUDA(cudaMemcpy2D(Q, ldq * 8, op.Q, (size_t)op.ldp * 8, m * 8, (size_t)op.cols, k));
+  if (gpost) ENG_CUDA(cudaMemcpy2D(gpost, ldg * 8, op.gpost, m * 8, m * 8, m, k));
+  if (prior_cov) ENG_CUDA(cudaMemcpy2D(prior_cov, ldg * 8, op.prior_cov, m * 8, m * 8, m, k));
+  return LTB_OK;
 }

@@ -98,34 +98,61 @@ LTB_DEV void gram_load_stage(double* sA, double* sB, const double* f, const doub
   }
 }
 
-// split == 1: CTA b computes lower 128-tile tile0 + b over all of N_m and
-// writes it into the packed tiles.  split > 1 (the last, partial wave): CTA b
-// computes k-slice b % split of tile tile0 + b / split into `partial`
-// ([tile][slice][128 x 128]); reduce_partials_kernel sums the slices in
-// order (deterministic) and scatters them.
+// Output of a lag Gram: the packed lower 64x64 tiles of K (dense == 0), or
+// a dense column-major block (dense == 1, rows x cols, leading dim ld).
+struct GramOut {
+  int dense;
+  double* p;
+  size_t ld;
+  int rows, cols;  // dense extent
+  int nb;          // packed: 64-blocks
+  int tiles_j;     // dense: 128-wide column tiles
+};
+
+LTB_DEV double* out_elem(const GramOut& o, int i, int j) {
+  if (o.dense) return (i < o.rows && j < o.cols) ? o.p + (size_t)j * o.ld + i : nullptr;
+  const int I = i >> 6, J = j >> 6;
+  return (I < o.nb && J <= I) ? o.p + tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63) : nullptr;
+}
+
+LTB_DEV void gram_tile(const GramOut& o, long long t, int* bi, int* bj) {
+  if (o.dense) {
+    *bi = (int)(t / o.tiles_j);
+    *bj = (int)(t % o.tiles_j);
+  } else {
+    tri_pair(t, bi, bj);
+  }
+}
+
+// A[i][j] = sum_x a_row(i)[x] b_row(j)[x] for 128x128 CTA tiles, operand row
+// i = (r, lag) of a [rows][nm][nt] kernel.  split == 1: CTA b computes tile
+// tile0 + b over all of N_m and writes it out.  split > 1 (the last, partial
+// wave): CTA b computes k-slice b % split of tile tile0 + b / split into
+// `partial` ([tile][slice][128 x 128]); reduce_partials_kernel sums the
+// slices in order (deterministic) and writes them out.
 template <bool kPair>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     lag_gram_kernel(const double* __restrict__ f, const double* __restrict__ g, int nm, int nt,
-                    int n, int nb, double* __restrict__ tiles, long long tile0, int split,
+                    int na, int nbr, const GramOut o, long long tile0, int split,
                     double* __restrict__ partial) {
   extern __shared__ __align__(16) double gsm[];
   const long long tile = tile0 + blockIdx.x / split;
   const int slice = blockIdx.x % split;
   int bi, bj;
-  tri_pair(tile, &bi, &bj);
+  gram_tile(o, tile, &bi, &bj);
   const int i0 = bi * kBM, j0 = bj * kBM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // warp tile 64 (rows) x 32 (cols)
 
-  // this thread's operand row base pointers (nullptr = padding row >= n)
+  // this thread's operand row base pointers (nullptr = padding row)
   const double* rowA;
   const double* rowB;
   {
     const int m = kPair ? 2 * (tid & 63) : (tid & 127);
     const int ia = i0 + m, ib = j0 + m;
-    rowA = ia < n ? f + (size_t)(ia / nt) * nm * nt + ia % nt : nullptr;
-    rowB = ib < n ? g + (size_t)(ib / nt) * nm * nt + ib % nt : nullptr;
+    rowA = ia < na ? f + (size_t)(ia / nt) * nm * nt + ia % nt : nullptr;
+    rowB = ib < nbr ? g + (size_t)(ib / nt) * nm * nt + ib % nt : nullptr;
   }
 
   double acc[4][4][4];
@@ -194,7 +221,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
     return;
   }
-  // epilogue: scatter into the packed 64x64 tiles (skip J > I and I >= nb)
+  // epilogue: packed tiles (skip J > I and I >= nb) or the dense block
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -205,57 +232,61 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int c = 0; c < 2; ++c) {
           const int i = i0 + wm * 64 + mt * 16 + gq + 8 * h;
           const int j = j0 + wn * 32 + nt8 * 8 + 2 * tq + c;
-          const int I = i >> 6, J = j >> 6;
-          if (I < nb && J <= I) tiles[tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63)] = acc[mt][nt8][2 * h + c];
+          double* dst = out_elem(o, i, j);
+          if (dst) *dst = acc[mt][nt8][2 * h + c];
         }
 }
 
-// sum the k-slices of the split tiles in slice order, scatter like the
+// sum the k-slices of the split tiles in slice order, write like the
 // data-parallel epilogue
 __global__ void reduce_partials_kernel(const double* __restrict__ partial, long long tile0, int split,
-                                       int nb, double* __restrict__ tiles) {
+                                       const GramOut o) {
   const long long t = blockIdx.y;
   int bi, bj;
-  tri_pair(tile0 + t, &bi, &bj);
+  gram_tile(o, tile0 + t, &bi, &bj);
   const double* P = partial + (size_t)t * split * kBM * kBM;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kBM * kBM; e += gridDim.x * blockDim.x) {
     const int m = e / kBM, c = e % kBM;
     double v = 0.0;
     for (int s = 0; s < split; ++s) v += P[(size_t)s * kBM * kBM + e];
-    const int i = bi * kBM + m, j = bj * kBM + c;
-    const int I = i >> 6, J = j >> 6;
-    if (I < nb && J <= I) tiles[tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63)] = v;
+    double* dst = out_elem(o, bi * kBM + m, bj * kBM + c);
+    if (dst) *dst = v;
   }
 }
 
 // ---------------------------------------------------------------------------
-// (2) K(t, j) = A(t, j) + K(t-1, j-1) inside each (r, s) block (r >= s), plus
-// sigma2 on the diagonal.  One thread per diagonal; consecutive threads take
-// consecutive diagonal starts (coalesced on the left-edge diagonals).  Loads
-// of a diagonal are batched 8 at a time so the walk is not latency-serial.
+// (2) the diagonal recurrence C(t, j) = A(t, j) + C(t-1, j-1) inside each
+// (r, s) block of N_t x N_t (packed K: r >= s and only the lower diagonals of
+// r == s, plus sigma2 on the diagonal; dense: every block, every diagonal).
+// One thread per diagonal; consecutive threads take consecutive diagonal
+// starts (coalesced on the left-edge diagonals).  Loads of a diagonal are
+// batched 8 at a time so the walk is not latency-serial.
 // ---------------------------------------------------------------------------
-LTB_DEV double* elem(double* tiles, int i, int j) {
-  return tiles + tile_at(i >> 6, j >> 6) + (size_t)(j & 63) * kT + (i & 63);
-}
-
-__global__ void diag_prefix_kernel(double* __restrict__ tiles, int nd, int nt, double sigma2) {
+__global__ void diag_prefix_kernel(const GramOut o, int nda, int ndb, int nt, double sigma2) {
   const long long per = 2ll * nt - 1;
-  const long long total = (long long)nd * (nd + 1) / 2 * per;
+  const long long pairs = o.dense ? (long long)nda * ndb : (long long)nda * (nda + 1) / 2;
+  const long long total = pairs * per;
   for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
        id += (long long)gridDim.x * blockDim.x) {
     const long long p = id / per;
     const int d = (int)(id - p * per);
     int r, s;
-    tri_pair(p, &r, &s);
+    if (o.dense) {
+      r = (int)(p / ndb);
+      s = (int)(p % ndb);
+    } else {
+      tri_pair(p, &r, &s);
+    }
     int t0, j0;
     if (d < nt) {
       t0 = d;
       j0 = 0;
     } else {
-      if (r == s) continue;  // strict upper of a diagonal block: not stored
+      if (!o.dense && r == s) continue;  // strict upper of a diagonal block: not stored
       t0 = 0;
       j0 = d - nt + 1;
     }
+    const bool diag = !o.dense && r == s && t0 == 0;
     const int len = nt - max(t0, j0);
     const int ib = r * nt + t0, jb = s * nt + j0;
     double run = 0.0;
@@ -263,16 +294,19 @@ __global__ void diag_prefix_kernel(double* __restrict__ tiles, int nd, int nt, d
       double v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        if (k0 + q < len) v[q] = *elem(tiles, ib + k0 + q, jb + k0 + q);
+        if (k0 + q < len) v[q] = *out_elem(o, ib + k0 + q, jb + k0 + q);
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (k0 + q < len) {
           run += v[q];
-          const bool diag = (r == s) && (t0 == 0);
-          *elem(tiles, ib + k0 + q, jb + k0 + q) = diag ? run + sigma2 : run;
+          *out_elem(o, ib + k0 + q, jb + k0 + q) = diag ? run + sigma2 : run;
         }
     }
   }
+}
+
+LTB_DEV double* elem(double* tiles, int i, int j) {
+  return tiles + tile_at(i >> 6, j >> 6) + (size_t)(j & 63) * kT + (i & 63);
 }
 
 // identity on the padding diagonal (rows / columns >= n of the last block)
@@ -440,17 +474,189 @@ __global__ void export_lower_kernel(const double* __restrict__ tiles, int n, dou
   }
 }
 
+// ---------------------------------------------------------------------------
+// (5) multi-RHS block substitution (form_Q's K^{-1} R, bayes_engine.cpp:250-255)
+// on the packed factor, 64 right-hand sides per CTA, DMMA for every product.
+// Forward (kTrans = false), step I (-1 <= I <= nb-2), CTA (chunk, J = I+1+y):
+//   R_J -= L_JI X_I                   (I >= 0)
+//   J == I+1:  X_J = L_JJ^{-1} R_J    (into X; R_J is dead afterwards)
+// Transposed, step I (nb >= I >= 1), CTA (chunk, J = I-1-y):
+//   R_J -= L_IJ^T X_I                 (I < nb)
+//   J == I-1:  X_J = L_JJ^{-T} R_J
+// R, X column-major with ld = nb * 64 rows (padding rows zero).  8 warps, warp
+// tile 32 rows x 16 columns; shared tiles with stride 68 (== 4 mod 16) read
+// either way round conflict-free.
+// ---------------------------------------------------------------------------
+constexpr int kRC = 64;
+constexpr int kTS = kT + 4;
+constexpr size_t kTrsmSmem = (size_t)2 * kT * kTS * sizeof(double);
+
+template <bool kTrans>
+__global__ void __launch_bounds__(256)
+    trsm_step_kernel(const double* __restrict__ tiles, const double* __restrict__ dinv, int nb, int I,
+                     double* __restrict__ R, double* __restrict__ X, size_t ld) {
+  extern __shared__ __align__(16) double tsm[];
+  double* sA = tsm;             // [col][row] of a 64x64 tile
+  double* sB = tsm + kT * kTS;  // [rhs][k]
+  const int c0 = blockIdx.x * kRC;
+  const int J = kTrans ? I - 1 - (int)blockIdx.y : I + 1 + (int)blockIdx.y;
+  const bool upd = kTrans ? (I < nb) : (I >= 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  double* RJ = R + (size_t)c0 * ld + (size_t)J * kT;
+  double acc[2][2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          acc[mt][nt8][2 * h + c] =
+              RJ[(size_t)(wn * 16 + nt8 * 8 + 2 * tq + c) * ld + wm * 32 + mt * 16 + gq + 8 * h];
+  auto tile_mma = [&](double (&d)[2][2][4], bool trans_a, double sign) {
+#pragma unroll
+    for (int kk = 0; kk < kT / 4; ++kk) {
+      const int k = kk * 4 + tq;
+      double a[2][2], b[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm * 32 + mt * 16 + gq + 8 * h;
+          a[mt][h] = sign * (trans_a ? sA[r * kTS + k] : sA[k * kTS + r]);
+        }
+#pragma unroll
+      for (int nt8 = 0; nt8 < 2; ++nt8) b[nt8] = sB[(wn * 16 + nt8 * 8 + gq) * kTS + k];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt8 = 0; nt8 < 2; ++nt8) dmma(d[mt][nt8], a[mt][0], a[mt][1], b[nt8]);
+    }
+  };
+  if (upd) {
+    const double* T = tiles + (kTrans ? tile_at(I, J) : tile_at(J, I));
+    const double* XI = X + (size_t)c0 * ld + (size_t)I * kT;
+    for (int c = tid; c < kTile / 2; c += 256) {
+      const int col = c >> 5, r2 = 2 * (c & 31);
+      cp_async16(sA + col * kTS + r2, T + col * kT + r2, 16);
+      cp_async16(sB + col * kTS + r2, XI + (size_t)col * ld + r2, 16);
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    tile_mma(acc, kTrans, -1.0);
+  }
+  const bool last = J == (kTrans ? I - 1 : I + 1);
+  if (!last) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            RJ[(size_t)(wn * 16 + nt8 * 8 + 2 * tq + c) * ld + wm * 32 + mt * 16 + gq + 8 * h] =
+                acc[mt][nt8][2 * h + c];
+    return;
+  }
+  // X_J = L_JJ^{-1} R_J (or L_JJ^{-T} R_J): R_J becomes the B operand
+  __syncthreads();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          sB[(wn * 16 + nt8 * 8 + 2 * tq + c) * kTS + wm * 32 + mt * 16 + gq + 8 * h] = acc[mt][nt8][2 * h + c];
+  const double* D = dinv + (size_t)J * kTile;
+  for (int c = tid; c < kTile / 2; c += 256) {
+    const int col = c >> 5, r2 = 2 * (c & 31);
+    cp_async16(sA + col * kTS + r2, D + col * kT + r2, 16);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  double out[2][2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) out[mt][nt8][e] = 0.0;
+  tile_mma(out, kTrans, 1.0);
+  double* XJ = X + (size_t)c0 * ld + (size_t)J * kT;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          XJ[(size_t)(wn * 16 + nt8 * 8 + 2 * tq + c) * ld + wm * 32 + mt * 16 + gq + 8 * h] =
+              out[mt][nt8][2 * h + c];
+}
+
+// out = 0.5 ((P - G) + (P - G)^T), m x m column-major (form_qoi_cov :271-274
+// with P symmetrised first: identical in exact arithmetic)
+__global__ void gpost_kernel(const double* __restrict__ P, const double* __restrict__ G, int m,
+                             double* __restrict__ out, double* __restrict__ diag) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)m * m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    const double a = P[(size_t)j * m + i] - G[(size_t)j * m + i];
+    const double b = P[(size_t)i * m + j] - G[(size_t)i * m + j];
+    const double v = 0.5 * (a + b);
+    out[e] = v;
+    if (i == j) diag[i] = v;
+  }
+}
+
+__global__ void symmetrize_kernel(double* __restrict__ A, int m) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)m * m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    if (i > j) {
+      const double v = 0.5 * (A[(size_t)j * m + i] + A[(size_t)i * m + j]);
+      A[(size_t)j * m + i] = v;
+      A[(size_t)i * m + j] = v;
+    }
+  }
+}
+
+// Q (m x n, ld m) = X^T, X column-major (n rows used, ld ldx)
+__global__ void transpose_kernel(const double* __restrict__ X, size_t ldx, int n, int m,
+                                 double* __restrict__ Q) {
+  __shared__ double t[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;  // i: row of X (< n), j: column (< m)
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + threadIdx.x, j = j0 + r;
+    t[r][threadIdx.x] = (i < n && j < m) ? X[(size_t)j * ldx + i] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = j0 + threadIdx.x, i = i0 + r;
+    if (i < n && j < m) Q[(size_t)i * m + j] = t[threadIdx.x][r];
+  }
+}
+
 }  // namespace
 
 int formk_last_launches() { return g_last_launches; }
 
-cudaError_t formk_device(TriFactor& t, const double* f, const double* g, int nd, int nm, int nt,
-                         double sigma2, cudaStream_t st) {
-  if (t.P != 1 || t.n != nd * nt || nm < 1) return cudaErrorInvalidValue;
-  const int n = t.n, nb = t.nb;
-  const long long nbm = (n + kBM - 1) / kBM;
-  const long long ctas = nbm * (nbm + 1) / 2;
-  const bool pair = (nt % 2 == 0) && ((uintptr_t)f % 16 == 0) && ((uintptr_t)g % 16 == 0);
+namespace {
+
+// lag Gram of kernel rows (a: na rows, b: nbr rows, contraction N_m) into o,
+// then the diagonal recurrence over (nda x ndb) blocks
+cudaError_t lag_gram(const double* a, int na, const double* b, int nbr, int nm, int nt, const GramOut& o,
+                     long long ctas, cudaStream_t st) {
+  const bool pair = (nt % 2 == 0) && ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
   auto kern = pair ? lag_gram_kernel<true> : lag_gram_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   if (e != cudaSuccess) return e;
@@ -467,24 +673,63 @@ cudaError_t formk_device(TriFactor& t, const double* f, const double* g, int nd,
     e = cudaMallocAsync(&partial, (size_t)rem * split * kBM * kBM * sizeof(double), st);
     if (e != cudaSuccess) return e;
   }
-  g_last_launches = 0;
   if (ctas - rem > 0) {
-    kern<<<(unsigned)(ctas - rem), kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles, 0, 1, nullptr);
+    kern<<<(unsigned)(ctas - rem), kGemmThreads, kGemmSmem, st>>>(a, b, nm, nt, na, nbr, o, 0, 1, nullptr);
     ++g_last_launches;
   }
   if (rem) {
-    kern<<<(unsigned)(rem * split), kGemmThreads, kGemmSmem, st>>>(f, g, nm, nt, n, nb, t.tiles, ctas - rem,
-                                                                    split, partial);
-    reduce_partials_kernel<<<dim3(16, (unsigned)rem), 256, 0, st>>>(partial, ctas - rem, split, nb, t.tiles);
+    kern<<<(unsigned)(rem * split), kGemmThreads, kGemmSmem, st>>>(a, b, nm, nt, na, nbr, o, ctas - rem, split,
+                                                                    partial);
+    reduce_partials_kernel<<<dim3(16, (unsigned)rem), 256, 0, st>>>(partial, ctas - rem, split, o);
     cudaFreeAsync(partial, st);
     g_last_launches += 2;
   }
-  const long long diags = (long long)nd * (nd + 1) / 2 * (2ll * nt - 1);
-  const unsigned pblocks = (unsigned)std::max(1ll, std::min(148ll * 32, (diags + 255) / 256));
-  diag_prefix_kernel<<<pblocks, 256, 0, st>>>(t.tiles, nd, nt, sigma2);
-  pad_identity_kernel<<<1, kT, 0, st>>>(t.tiles, n, nb);
-  g_last_launches += 2;
   return cudaGetLastError();
+}
+
+cudaError_t diag_recurrence(const GramOut& o, int nda, int ndb, int nt, double sigma2, cudaStream_t st) {
+  const long long pairs = o.dense ? (long long)nda * ndb : (long long)nda * (nda + 1) / 2;
+  const long long diags = pairs * (2ll * nt - 1);
+  const unsigned pblocks = (unsigned)std::max(1ll, std::min(148ll * 32, (diags + 255) / 256));
+  diag_prefix_kernel<<<pblocks, 256, 0, st>>>(o, nda, ndb, nt, sigma2);
+  ++g_last_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t formk_device(TriFactor& t, const double* f, const double* g, int nd, int nm, int nt,
+                         double sigma2, cudaStream_t st) {
+  if (t.P != 1 || t.n != nd * nt || nm < 1) return cudaErrorInvalidValue;
+  const int n = t.n, nb = t.nb;
+  const long long nbm = (n + kBM - 1) / kBM;
+  GramOut o{};
+  o.dense = 0;
+  o.p = t.tiles;
+  o.nb = nb;
+  g_last_launches = 0;
+  cudaError_t e = lag_gram(f, n, g, n, nm, nt, o, nbm * (nbm + 1) / 2, st);
+  if (e == cudaSuccess) e = diag_recurrence(o, nd, nd, nt, sigma2, st);
+  if (e != cudaSuccess) return e;
+  pad_identity_kernel<<<1, kT, 0, st>>>(t.tiles, n, nb);
+  ++g_last_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t block_toeplitz_product(const double* a, int nda, const double* b, int ndb, int nm, int nt,
+                                   double* out, size_t ld, cudaStream_t st) {
+  GramOut o{};
+  o.dense = 1;
+  o.p = out;
+  o.ld = ld;
+  o.rows = nda * nt;
+  o.cols = ndb * nt;
+  o.tiles_j = (o.cols + kBM - 1) / kBM;
+  const long long ctas = (long long)((o.rows + kBM - 1) / kBM) * o.tiles_j;
+  g_last_launches = 0;
+  cudaError_t e = lag_gram(a, o.rows, b, o.cols, nm, nt, o, ctas, st);
+  if (e == cudaSuccess) e = diag_recurrence(o, nda, ndb, nt, 0.0, st);
+  return e;
 }
 
 cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
@@ -522,6 +767,61 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
 cudaError_t export_lower(const TriFactor& t, double* out, size_t ld, cudaStream_t st) {
   const long long ntiles = (long long)t.nb * (t.nb + 1) / 2;
   export_lower_kernel<<<(unsigned)ntiles, 256, 0, st>>>(t.tiles, t.n, out, ld);
+  return cudaGetLastError();
+}
+
+cudaError_t trsm_solve_k(const TriFactor& t, double* R, double* X, size_t ld, int nrhs_pad, double* YtY,
+                         int m, cudaStream_t st) {
+  if (t.P != 1 || nrhs_pad % kRC) return cudaErrorInvalidValue;
+  const int nb = t.nb;
+  cudaError_t e = cudaFuncSetAttribute(trsm_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kTrsmSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(trsm_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kTrsmSmem);
+  if (e != cudaSuccess) return e;
+  const unsigned chunks = (unsigned)(nrhs_pad / kRC);
+  g_last_launches = 0;
+  // forward: Y = L^{-1} R into X (R is scratch)
+  for (int I = -1; I <= nb - 2; ++I) {
+    trsm_step_kernel<false><<<dim3(chunks, (unsigned)(nb - 1 - I)), 256, kTrsmSmem, st>>>(t.tiles, t.dinv, nb, I,
+                                                                                       R, X, ld);
+    ++g_last_launches;
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // R^T K^{-1} R = Y^T Y (m x m), before the transposed sweep consumes Y
+  if (YtY) {
+    const int keep = g_last_launches;
+    e = block_toeplitz_product(X, m, X, m, (int)ld, 1, YtY, (size_t)m, st);
+    g_last_launches += keep;
+    if (e != cudaSuccess) return e;
+  }
+  // transposed: K^{-1} R = L^{-T} Y into R (Y is scratch)
+  for (int I = nb; I >= 1; --I) {
+    trsm_step_kernel<true><<<dim3(chunks, (unsigned)I), 256, kTrsmSmem, st>>>(t.tiles, t.dinv, nb, I, X, R, ld);
+    ++g_last_launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t qoi_covariance(const double* P, const double* YtY, int m, double* gpost, double* diag,
+                           cudaStream_t st) {
+  const long long mm = (long long)m * m;
+  const unsigned blocks = (unsigned)std::max(1ll, std::min(148ll * 8, (mm + 255) / 256));
+  gpost_kernel<<<blocks, 256, 0, st>>>(P, YtY, m, gpost, diag);
+  return cudaGetLastError();
+}
+
+cudaError_t symmetrize(double* A, int m, cudaStream_t st) {
+  const long long mm = (long long)m * m;
+  symmetrize_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 8, (mm + 255) / 256)), 256, 0, st>>>(A, m);
+  return cudaGetLastError();
+}
+
+cudaError_t transpose_to(const double* X, size_t ldx, int n, int m, double* Q, cudaStream_t st) {
+  transpose_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32)), dim3(32, 8), 0, st>>>(X, ldx, n, m,
+                                                                                                     Q);
   return cudaGetLastError();
 }
 

@@ -36,7 +36,27 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block);
 // Packed lower tiles -> column-major n x n device matrix (lower triangle
 // incl. the diagonal written; the strict upper part is left untouched).
 cudaError_t export_lower(const TriFactor& t, double* out, size_t ld, cudaStream_t st);
-// launches issued by the last formk_device / cholesky_packed call
+// launches issued by the last formk_device / cholesky_packed / ... call
 int formk_last_launches();
+
+// ---- form_Q / form_qoi_cov (bayes_engine.cpp:242-285) ----
+// out (column-major, ld) = the dense (nda N_t) x (ndb N_t) product of the
+// block-lower-triangular-Toeplitz map of kernel a with the adjoint of the map
+// of kernel b (both [nd][nm][nt]): F_a G_b^* -- R = F Gq* and P = Fq Gq*.
+// Same lag-Gram contraction + diagonal recurrence as form_K.
+cudaError_t block_toeplitz_product(const double* a, int nda, const double* b, int ndb, int nm, int nt,
+                                   double* out, size_t ld, cudaStream_t st);
+// K^{-1} R for nrhs_pad (multiple of 64) columns: R, X column-major n_pad x
+// nrhs_pad (ld = nb * 64, padding zero).  Forward sweep R -> Y (in X), then
+// (optional) YtY = Y^T Y (m x m, = R^T K^{-1} R), then the transposed sweep
+// Y -> K^{-1} R (in R).  Both R and X are overwritten.
+cudaError_t trsm_solve_k(const TriFactor& t, double* R, double* X, size_t ld, int nrhs_pad, double* YtY,
+                         int m, cudaStream_t st);
+// gpost = sym(P - YtY) (P already symmetric), diag = its diagonal
+cudaError_t qoi_covariance(const double* P, const double* YtY, int m, double* gpost, double* diag,
+                           cudaStream_t st);
+cudaError_t symmetrize(double* A, int m, cudaStream_t st);
+// Q (m x n, column-major, ld m) = X^T
+cudaError_t transpose_to(const double* X, size_t ldx, int n, int m, double* Q, cudaStream_t st);
 
 }  // namespace ltb

@@ -154,9 +154,73 @@ class InferenceEngine:
         check(_lib.load().ltb_engine_factorize(self._h))
 
     def offline_ms(self):
-        a, b = C.c_double(), C.c_double()
-        check(_lib.load().ltb_engine_offline_ms(self._h, C.byref(a), C.byref(b)))
+        """(form_K, factorize) device milliseconds of the last calls."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check(_lib.load().ltb_engine_offline_ms(self._h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value
+
+    def form_Q_ms(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check(_lib.load().ltb_engine_offline_ms(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return c.value
+
+    def form_Q(self, f_kernel, fq_kernel, gq_kernel=None, prior=None):
+        """form_Q + form_qoi_cov (bayes_engine.cpp:242-285) on the device; needs
+        the factor.  Installs the Phase-3 operator used by predict_qoi."""
+        f, fshape = _kernel_data(f_kernel, "form_Q f")
+        fq, qshape = _kernel_data(fq_kernel, "form_Q fq")
+        nd, nm, nt = fshape
+        nq = qshape[0]
+        if qshape[1:] != fshape[1:]:
+            raise DimensionError("form_Q: F and F_q kernel dims are inconsistent")
+        pf, kind, _a = _buffer(f, nd * nm * nt, "form_Q f")
+        pq, kind_q, _b = _buffer(fq, nq * nm * nt, "form_Q fq")
+        pg = None
+        if gq_kernel is not None:
+            gq, gshape = _kernel_data(gq_kernel, "form_Q gq")
+            if gshape != qshape:
+                raise DimensionError("form_Q: Gq kernel dims differ from F_q")
+            pg, kind_g, _c = _buffer(gq, nq * nm * nt, "form_Q gq")
+        elif prior is None:
+            raise ValueError("form_Q: need gq_kernel or prior=(h_x, gamma, delta)")
+        if kind_q != kind or (pg is not None and kind_g != kind):
+            raise ValueError("form_Q: kernels must all be host or all be device arrays")
+        p3 = (C.c_double * 3)(*prior) if prior is not None else None
+        check(_lib.load().ltb_engine_form_q(self._h, pf, pq, pg, p3, nd, nq, nm, nt, kind))
+        if not self.n_qoi:
+            self.n_qoi = nq
+
+    def form_Q_generated(self, seed, nq, prior, stream_f=1, stream_fq=2):
+        """form_Q of the generated F / F_q kernels (ltb_plan_create_generated's
+        streams: F = 1, F_q = 2) and the premultiplied Gq."""
+        h_x, gamma, delta = prior
+        check(_lib.load().ltb_engine_form_q_generated(self._h, int(seed), int(stream_f), int(stream_fq),
+                                                      int(nq), float(h_x), float(gamma), float(delta)))
+        if not self.n_qoi:
+            self.n_qoi = nq
+
+    def _phase3(self, which):
+        m = self.n_qoi * self.n_time
+        n = self.n_data()
+        Q = np.empty((m, n), order="F") if which == "Q" else None
+        G = np.empty((m, m), order="F") if which != "Q" else None
+        gp = G if which == "gpost" else None
+        pc = G if which == "prior" else None
+        check(_lib.load().ltb_engine_export_phase3(
+            self._h, C.c_void_p(Q.ctypes.data) if Q is not None else None, m,
+            C.c_void_p(gp.ctypes.data) if gp is not None else None,
+            C.c_void_p(pc.ctypes.data) if pc is not None else None, m, 0))
+        return Q if Q is not None else G
+
+    def Q(self):
+        """The Phase-3 operator Q (N_q N_t x N_d N_t)."""
+        return self._phase3("Q")
+
+    def gamma_post_q(self):
+        return self._phase3("gpost")
+
+    def prior_qoi_cov(self):
+        return self._phase3("prior")
 
     def _export(self):
         n = self.n_data()

@@ -217,3 +217,70 @@ def test_generated_small_inversion_config(ltb):
     fk, fz = eng.offline_ms()
     print("config2 form_K %.2f ms (%.1f TFLOP/s lag Gram), factorize %.2f ms" %
           (fk, n * n * nm / fk / 1e9, fz))
+
+
+# ---------------------------------------------------------------- form_Q
+@pytest.mark.gpu
+@pytest.mark.parametrize("nd,nq,nm,nt", [(2, 2, 4, 5), (4, 3, 40, 33), (8, 2, 300, 64), (16, 4, 256, 48)])
+def test_form_q_vs_oracle(ltb, nd, nq, nm, nt):
+    """form_Q + form_qoi_cov (bayes_engine.cpp:242-285) on the device vs the
+    oracle (column-by-column FFT assembly, per-column solve_k): Q, Gamma_post_q
+    and the prior QoI covariance within 1e-12; then predict_qoi with the
+    device-made artifacts equals F_q m_map (the Phase-4 chain identity)."""
+    rng = np.random.default_rng(nd * 100 + nq * 10 + nt)
+    s2 = 0.3
+    f = lti_like(rng, nd, nm, nt)
+    fq = lti_like(rng, nq, nm, nt)
+    g = orc.prior_premultiply(f, *PRIOR)
+    gq = orc.prior_premultiply(fq, *PRIOR)
+    kern_fq = ltb.BlockToeplitzKernel(*fq.shape, tag=ltb.KernelTag.Fq, data=fq)
+    plan_fq = ltb.MatvecPlan(kern_fq)
+    kern = ltb.BlockToeplitzKernel(*f.shape, tag=ltb.KernelTag.F, data=f)
+    plan_g = ltb.MatvecPlan.premultiplied(kern, PRIOR)
+    eng = ltb.InferenceEngine(plan_g, plan_fq)
+    with pytest.raises(ltb.StateError):  # needs the factor
+        eng.form_Q(f, fq, prior=PRIOR)
+    eng.form_K(f, prior=PRIOR, sigma2=s2)
+    eng.factorize()
+    eng.form_Q(f, fq, prior=PRIOR)
+    L = eng.chol_lower()
+    Q_o, gp_o, pc_o = orc.form_q(f, fq, gq, L)
+    assert orc.rel_err(eng.Q(), Q_o) <= 1e-12
+    assert orc.rel_err(eng.prior_qoi_cov(), pc_o) <= 1e-12
+    assert orc.rel_err(eng.gamma_post_q(), gp_o) <= 1e-11
+    # explicit Gq kernel gives the same operator
+    eng.form_Q(f, fq, gq_kernel=gq)
+    assert orc.rel_err(eng.Q(), Q_o) <= 1e-12
+    assert eng.form_Q_ms() > 0
+    d = rng.standard_normal(nd * nt)
+    obs = ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, d)
+    pred = eng.predict_qoi(obs)
+    res = eng.infer_map(obs, with_forecast=True)
+    assert orc.rel_err(pred.q_map.values, res.q_map.values) <= 1e-10  # Q d == F_q m_map
+    sd = np.sqrt(np.maximum(np.diag(gp_o), 0))
+    assert np.allclose(pred.ci_upper.values - pred.q_map.values, 1.96 * sd, rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_form_q_generated_small_inversion(ltb):
+    """Config 2 with N_q = 8 fully on the device (form_K -> factorize ->
+    form_Q -> predict_qoi); size-independent checks: Q d == F_q m_map and
+    diag(Gamma_post_q) <= diag(prior QoI covariance) (data only reduces
+    variance)."""
+    nd, nm, nt, nq, seed, s2 = 64, 16384, 128, 8, 4321, 1.0
+    prior = (1.0, 2.0, 1.0)
+    pg = ltb.MatvecPlan.generated_premultiplied(nd, nm, nt, seed, prior, tag=ltb.KernelTag.F)
+    fq = ltb.MatvecPlan.generated(nq, nm, nt, seed, tag=ltb.KernelTag.Fq)
+    eng = ltb.InferenceEngine(pg, fq)
+    eng.form_K_generated(seed, 1, prior, s2)
+    eng.factorize()
+    eng.form_Q_generated(seed, nq, prior)
+    rng = np.random.default_rng(3)
+    obs = ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, rng.standard_normal(nd * nt))
+    pred = eng.predict_qoi(obs)
+    res = eng.infer_map(obs, with_forecast=True)
+    assert orc.rel_err(pred.q_map.values, res.q_map.values) <= 1e-9
+    gp, pc = eng.gamma_post_q(), eng.prior_qoi_cov()
+    assert np.all(np.diag(gp) <= np.diag(pc) * (1 + 1e-12))
+    assert np.all(np.diag(gp) > 0)
+    print("config2 form_Q (N_q=8) %.2f ms" % eng.form_Q_ms())

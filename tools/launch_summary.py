@@ -9,7 +9,8 @@ h = rows[0]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
 tot, cnt, seq = defaultdict(float), defaultdict(int), []
 for r in rows[1:]:
-    name = r[ki].split("(")[0].split("<")[0]
+    name = r[ki].replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+    name = name.replace("void ", "").split("(")[0].split("<")[0]
     v = float(r[vi].replace(",", ""))
     v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     tot[name] += v
