@@ -86,12 +86,13 @@ LTB_DEV unsigned long long globaltimer() {
 // Poll a hand-off value until it is no longer the sentinel.  On timeout (or
 // once any CTA timed out) set *status and return 0.0 so the kernel runs to
 // completion and the host reports the error instead of the GPU hanging.
+template <bool kSleep = true>
 LTB_DEV double poll_value(const double* p, int* status) {
   unsigned long long v = ld_relaxed_u64(p);
   if (v != kSentinel) return __longlong_as_double((long long)v);
   const unsigned long long t0 = globaltimer();
   while (true) {
-    __nanosleep(20);
+    if (kSleep) __nanosleep(20);
     v = ld_relaxed_u64(p);
     if (v != kSentinel) return __longlong_as_double((long long)v);
     if (*(volatile int*)status) return 0.0;
@@ -160,9 +161,23 @@ LTB_DEV double red_sum(const double (&red)[kQ][kTB], int r) {
   return s;
 }
 
+// The chain is a cluster of two CTAs (CTAs 0 and 1 of rank 0): CTA h owns
+// rows [32 h, 32 h + 32) of every 64-block, so each ingests half of the chain
+// tiles per step; the two halves of each solution block are exchanged through
+// distributed shared memory (st.async completing on the peer's mbarrier).
+constexpr int kChainCtas = 2;
+constexpr int kHalf = kTB / kChainCtas;   // 32 rows per chain CTA
+constexpr int kCQ = kThreads / kHalf;     // 16 column groups
+constexpr int kCC = kTB / kCQ;            // 4 columns per thread
+constexpr int kHalfTile = kTB * kHalf;    // 2048 doubles
+constexpr int kYShift = 3;
+constexpr int kYSlots = 1 << kYShift;
+static_assert(kLook + 1 < kYSlots, "y ring too short");
+
 struct ChainSmem {
-  double ring[kLook][kTB];
-  double red[kQ][kTB];
+  double ring[kYSlots][kTB];  // solution blocks: own half written locally, peer half by st.async
+  double red[kCQ][kHalf];
+  uint64_t ybar[kYSlots];     // completes when the peer's half of a slot has arrived
 };
 
 struct WorkerSmem {
@@ -192,123 +207,192 @@ LTB_DEV void grid_barrier(unsigned* gsync) {
 }
 
 // ---------------- chain ------------------------------------------------------
-// The chain tiles of a step (kLook contiguous 32 KB tiles) arrive by ONE bulk
-// async copy (TMA 1-D) into a two-stage shared-memory buffer, issued a full
-// step ahead: register prefetches of the same data made every step wait on
-// the scoreboard of the NEXT step's loads (measured: ~1100 cycles per step
-// stalled in the FMA phase), async copies into shared memory do not.
+// Chain tiles are stored split by half: step I, half h, tile k, column c,
+// row ii (< 32) at ((I * 2 + h) * kLook + k) * kHalfTile + c * kHalf + ii, so
+// the kLook tiles a chain CTA needs per step are one contiguous 32 KB run,
+// brought in by one bulk async copy (TMA 1-D) into a two-stage shared buffer
+// a full step ahead.  (Register prefetches of the same data stalled every
+// step on the scoreboard of the next step's loads; one SM's bulk-copy intake
+// (~36 B/cycle from HBM, tools/probes/tma_latency.cu) is why the tiles are
+// split over two SMs.)
 struct ChainRing {
-  double* stage;   // 2 stages x kLook tiles (dynamic shared memory)
+  double* stage;   // 2 stages x kLook half tiles (dynamic shared memory)
   uint64_t* full;  // 2 mbarriers
 };
 
-LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int step) {
+__host__ __device__ inline size_t chain_idx(int I, int k, int row, int col) {
+  return ((size_t)(I * 2 + (row >> 5)) * kLook + k) * kHalfTile + (size_t)col * kHalf + (row & 31);
+}
+
+LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int u, int I, unsigned h) {
   if (threadIdx.x == 0) {
-    const int s = step & 1;
-    constexpr unsigned kBytes = kLook * kTile * sizeof(double);
+    const int s = u & 1;
+    constexpr unsigned kBytes = kLook * kHalfTile * sizeof(double);
     mbar_arrive_expect_tx(cr.full + s, kBytes);
-    bulk_g2s(cr.stage + (size_t)s * kLook * kTile, mtiles + (size_t)step * kLook * kTile, kBytes,
+    bulk_g2s(cr.stage + (size_t)s * kLook * kHalfTile, mtiles + ((size_t)I * 2 + h) * kLook * kHalfTile, kBytes,
              cr.full + s, policy_evict_first());
   }
 }
 
-// Hand-off of step I: forward = cf[I] (one worker); transposed = sum over the
-// P ranks' cb[h][I].  `cur` is this step's hand-off prefetched one step ago;
-// `nxt` receives the next one.
+LTB_DEV bool mbar_test(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// mbarrier wait with the dependency-wait timeout of poll_value
+LTB_DEV void mbar_wait_bounded(uint64_t* bar, unsigned parity, int* status) {
+  if (mbar_test(bar, parity)) return;
+  const unsigned long long t0 = globaltimer();
+  while (!mbar_test(bar, parity)) {
+    if (*(volatile int*)status) return;
+    if (globaltimer() - t0 > kSpinNs) {
+      atomicExch(status, 1);
+      return;
+    }
+  }
+}
+
+LTB_DEV uint32_t mapa_rank(const void* p, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+LTB_DEV void st_async_f64(uint32_t dst, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v),
+               "r"(bar)
+               : "memory");
+}
+LTB_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+struct ChainCtx {
+  unsigned h;          // this CTA's half
+  uint32_t peer_ring;  // &ring[0][0] in the peer CTA (cluster address)
+  uint32_t peer_bar;   // &ybar[0] in the peer CTA
+};
+
+// Step u of a sweep (block I = u forward, nb - 1 - u transposed).  `cur` is
+// this step's hand-off prefetched one step ago; `nxt` receives the next one.
+// Hand-off: forward = cf[I] (one worker); transposed = sum over the P ranks'
+// cb[h][I].
 template <bool kForward>
-LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, int I, int nvalid,
-                        unsigned long long cur, unsigned long long& nxt) {
-  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u,
+                        int nvalid, unsigned long long cur, unsigned long long& nxt,
+                        unsigned long long& nxt2) {
+  const int tid = threadIdx.x, i = tid & (kHalf - 1), q = tid / kHalf;
   const int nb = a.nb, P = kForward ? 1 : a.P;
+  const int I = kForward ? u : nb - 1 - u;
+  const int row0 = (int)cx.h * kHalf;
   double* recv0 = a.loc[0].recv;  // the chain runs on rank 0 = local rank 0
   const double* cbuf = recv0 + (kForward ? off_cf(nb) : off_cb(nb));
-  const int In = kForward ? I + 1 : I - 1;
-  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I] = clock64();
-  // prefetch rank 0's hand-off of the next step (the others are polled)
-  if (tid < kTB && In >= 0 && In < nb) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
-  // the step's tiles: stage I & 1, its (I >> 1)-th use
-  mbar_wait(cr.full + (I & 1), (unsigned)((kForward ? I : nb - 1 - I) >> 1) & 1);
-  const double* ms = cr.stage + (size_t)(I & 1) * kLook * kTile;
+  const int In = kForward ? I + 1 : I - 1, In2 = kForward ? I + 2 : I - 2;
+  const int slot = u & (kYSlots - 1);
+  if (tid == 0) mbar_arrive_expect_tx(&sm.ybar[slot], kHalf * sizeof(double));  // the peer's half of step u
+  if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I] = clock64();
+  // rank 0's hand-offs are prefetched two steps ahead and re-read a step
+  // ahead while still unpublished, so the wait below is rarely a round trip
+  if (tid < kHalf) {
+    if (In2 >= 0 && In2 < nb) nxt2 = ld_relaxed_u64(cbuf + (size_t)In2 * kTB + row0 + tid);
+    if (In >= 0 && In < nb && nxt == kSentinel) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + row0 + tid);
+  }
+  mbar_wait_bounded(cr.full + (u & 1), (unsigned)(u >> 1) & 1, a.status);  // this step's tiles
+  if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
+  if (u >= 1)  // the peer's half of the previous block (older ones were waited for earlier)
+    mbar_wait_bounded(&sm.ybar[(u - 1) & (kYSlots - 1)], (unsigned)((u - 1) >> kYShift) & 1, a.status);
+  const double* ms = cr.stage + (size_t)(u & 1) * kLook * kHalfTile;
   double p = 0.0;
 #pragma unroll
   for (int k = 0; k < kLook; ++k) {
     if (k < nvalid) {
-      const int src = kForward ? I - k - 1 : I + k + 1;
-      const double* v = sm.ring[src % kLook] + kCPT * q;
-      const double* M = ms + (size_t)k * kTile + (size_t)kCPT * q * kTB + i;
+      const double* v = sm.ring[(u - k - 1) & (kYSlots - 1)] + kCC * q;
+      const double* M = ms + (size_t)k * kHalfTile + (size_t)kCC * q * kHalf + i;
 #pragma unroll
-      for (int kk = 0; kk < kCPT; ++kk) p = fma(M[kk * kTB], v[kk], p);
+      for (int kk = 0; kk < kCC; ++kk) p = fma(M[kk * kHalf], v[kk], p);
     }
   }
-  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
   sm.red[q][i] = p;
-  __syncthreads();  // also: every thread is done with stage I & 1
-  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
-  // refill the stage just consumed with the tiles of step I +- 2
-  {
-    const int I2 = kForward ? I + 2 : I - 2;
-    if (I2 >= 0 && I2 < nb) chain_issue(cr, kForward ? a.mf : a.mb, I2);
-  }
-  if (tid < kTB) {
+  __syncthreads();  // also: every thread is done with stage u & 1
+  if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
+  if (u + 2 < nb) chain_issue(cr, kForward ? a.mf : a.mb, u + 2, kForward ? I + 2 : I - 2, cx.h);
+  if (tid < kHalf) {
     unsigned long long raw[kMaxRanks];
-    for (int h = 1; h < P; ++h) raw[h] = ld_relaxed_u64(cbuf + ((size_t)h * nb + I) * kTB + tid);
+    for (int hh = 1; hh < P; ++hh) raw[hh] = ld_relaxed_u64(cbuf + ((size_t)hh * nb + I) * kTB + row0 + tid);
     double c = cur != kSentinel ? __longlong_as_double((long long)cur)
-                                : poll_value(cbuf + (size_t)I * kTB + tid, a.status);
-    for (int h = 1; h < P; ++h)  // fixed order h = 0, 1, ..., P-1
-      c += raw[h] != kSentinel ? __longlong_as_double((long long)raw[h])
-                               : poll_value(cbuf + ((size_t)h * nb + I) * kTB + tid, a.status);
-    if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
-    const double v = c - red_sum(sm.red, tid);
-    const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + tid;
+                                : poll_value<false>(cbuf + (size_t)I * kTB + row0 + tid, a.status);
+    for (int hh = 1; hh < P; ++hh)  // fixed order h = 0, 1, ..., P-1
+      c += raw[hh] != kSentinel ? __longlong_as_double((long long)raw[hh])
+                                : poll_value<false>(cbuf + ((size_t)hh * nb + I) * kTB + row0 + tid, a.status);
+    if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
+    double s = 0.0;
+#pragma unroll
+    for (int g = 0; g < kCQ; ++g) s += sm.red[g][tid];
+    const double v = c - s;
+    const int e = slot * kTB + row0 + tid;
+    sm.ring[slot][row0 + tid] = v;
+    st_async_f64(cx.peer_ring + (uint32_t)e * 8u, v, cx.peer_bar + (uint32_t)slot * 8u);
+    const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + row0 + tid;
     for (int r = 0; r < a.P; ++r) a.peer[r][o] = v;  // push to every rank
-    sm.ring[I % kLook][tid] = v;
   }
   __syncthreads();
-  if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
+  if (a.trace && threadIdx.x == 0 && cx.h == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
 }
 
-// Both sweeps use the same two stages; every stage's mbarrier completes once
-// per use, so the forward sweep's uses (steps 0..nb-1) and the transposed
-// sweep's (nb-1..0) each start from parity 0 on a freshly initialised pair.
-LTB_DEV void chain_init(const ChainRing& cr) {
+// fresh barriers for a sweep; both chain CTAs must be past their previous
+// sweep (all of its peer data received) before either starts sending
+LTB_DEV void chain_sweep_init(const ChainRing& cr, ChainSmem& sm, bool reinit) {
   if (threadIdx.x == 0) {
+    if (reinit) {
+      for (int s = 0; s < 2; ++s)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(cr.full + s)) : "memory");
+      for (int s = 0; s < kYSlots; ++s)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.ybar[s])) : "memory");
+    }
     mbar_init(cr.full, 1);
     mbar_init(cr.full + 1, 1);
+    for (int s = 0; s < kYSlots; ++s) mbar_init(&sm.ybar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
+  cluster_sync_all();
 }
 
-LTB_DEV void chain_forward(const DistArgs& a, ChainSmem& sm, const ChainRing& cr) {
-  chain_init(cr);
-  auto nvalid = [&](int I) { return I < kLook ? I : kLook; };
-  chain_issue(cr, a.mf, 0);
-  if (a.nb > 1) chain_issue(cr, a.mf, 1);
-  unsigned long long cA = kSentinel, cB = kSentinel;
-  for (int I = 0; I < a.nb; I += 2) {
-    chain_step<true>(a, sm, cr, I, nvalid(I), cA, cB);
-    if (I + 1 < a.nb) chain_step<true>(a, sm, cr, I + 1, nvalid(I + 1), cB, cA);
-  }
-}
-
-LTB_DEV void chain_transposed(const DistArgs& a, ChainSmem& sm, const ChainRing& cr) {
+template <bool kForward>
+LTB_DEV void chain_sweep(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx) {
   const int nb = a.nb;
-  // fresh barriers for the second sweep (all forward copies were consumed)
+  const double* mt = kForward ? a.mf : a.mb;
+  chain_issue(cr, mt, 0, kForward ? 0 : nb - 1, cx.h);
+  if (nb > 1) chain_issue(cr, mt, 1, kForward ? 1 : nb - 2, cx.h);
+  auto nvalid = [&](int u) { return u < kLook ? u : kLook; };
+  // three hand-off registers in rotating roles (no moves of pending loads)
+  unsigned long long cA = kSentinel, cB = kSentinel, cC = kSentinel;
+  for (int u = 0; u < nb; u += 3) {
+    chain_step<kForward>(a, sm, cr, cx, u, nvalid(u), cA, cB, cC);
+    cA = kSentinel;
+    if (u + 1 < nb) chain_step<kForward>(a, sm, cr, cx, u + 1, nvalid(u + 1), cB, cC, cA);
+    cB = kSentinel;
+    if (u + 2 < nb) chain_step<kForward>(a, sm, cr, cx, u + 2, nvalid(u + 2), cC, cA, cB);
+    cC = kSentinel;
+  }
+  // the peer's half of the last block is never read by a later step: wait for it
+  mbar_wait_bounded(&sm.ybar[(nb - 1) & (kYSlots - 1)], (unsigned)((nb - 1) >> kYShift) & 1, a.status);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(cr.full)) : "memory");
-    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(cr.full + 1)) : "memory");
-  }
-  chain_init(cr);
-  auto nvalid = [&](int I) { return nb - 1 - I < kLook ? nb - 1 - I : kLook; };
-  // stage of step I is I & 1; use index (nb - 1 - I) >> 1 of that stage
-  chain_issue(cr, a.mb, nb - 1);
-  if (nb > 1) chain_issue(cr, a.mb, nb - 2);
-  unsigned long long cA = kSentinel, cB = kSentinel;
-  for (int I = nb - 1; I >= 0; I -= 2) {
-    chain_step<false>(a, sm, cr, I, nvalid(I), cA, cB);
-    if (I - 1 >= 0) chain_step<false>(a, sm, cr, I - 1, nvalid(I - 1), cB, cA);
-  }
+  cluster_sync_all();
+}
+
+LTB_DEV void chain_run(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, unsigned h) {
+  ChainCtx cx;
+  cx.h = h;
+  cx.peer_ring = mapa_rank(&sm.ring[0][0], h ^ 1u);
+  cx.peer_bar = mapa_rank(&sm.ybar[0], h ^ 1u);
+  chain_sweep_init(cr, sm, false);
+  chain_sweep<true>(a, sm, cr, cx);
+  chain_sweep_init(cr, sm, true);
+  chain_sweep<false>(a, sm, cr, cx);
 }
 
 // ---------------- workers: TMA tile ring ------------------------------------
@@ -501,12 +585,11 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && a.r0 == 0) a.trace[4 * nb] = globaltimer();
 
-  if (r == 0 && lc == 0) {
+  if (r == 0 && lc < kChainCtas) {
     ChainRing cr;
     cr.stage = reinterpret_cast<double*>(ring_smem);
     cr.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kRing * kTile * sizeof(double));
-    chain_forward(a, sm.chain, cr);
-    chain_transposed(a, sm.chain, cr);
+    chain_run(a, sm.chain, cr, (unsigned)lc);
   } else {
     TileRing ring;
     ring.stage = reinterpret_cast<double*>(ring_smem);
@@ -519,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
       policy = policy_evict_first();
     }
     __syncthreads();
-    const int w = r == 0 ? lc - 1 : lc, W = r == 0 ? a.gper - 1 : a.gper;
+    const int w = r == 0 ? lc - kChainCtas : lc, W = r == 0 ? a.gper - kChainCtas : a.gper;
     // forward: this rank's rows I = r + P li
     const int nrows = r < nb ? (nb - 1 - r) / a.P + 1 : 0;
     for (int li = w; li < nrows; li += W)
@@ -536,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
 }
 
 constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
-static_assert(2 * kLook <= kRing, "the chain's two tile stages live in the worker ring's space");
+static_assert(2 * kLook * kHalfTile <= kRing * kTile, "the chain's two tile stages live in the worker ring's space");
 
 // ---------------- setup kernels ----------------------------------------------
 // local tile index t of rank r -> (I, J)
@@ -625,11 +708,11 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
   double* sA = ct_smem;               // Dinv_II, sA[col * kPad + row]
   double* sB = ct_smem + kTB * kPad;  // panel tile, same layout
   const int I = blockIdx.x, k = blockIdx.y + 1, dir = blockIdx.z;
-  double* C = (dir == 0 ? mf : mb) + ((size_t)I * kLook + k - 1) * kTile;
+  double* C = dir == 0 ? mf : mb;  // split layout, chain_idx
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
   const int J = dir == 0 ? I - k : I + k;
   if (J < 0 || J >= nb) {
-    for (int e = tid; e < kTile; e += blockDim.x) C[e] = 0.0;
+    for (int e = tid; e < kTile; e += blockDim.x) C[chain_idx(I, k - 1, e & 63, e >> 6)] = 0.0;
     return;
   }
   const double* A = dinv + (size_t)I * kTile;
@@ -644,7 +727,7 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
     } else {
       for (int l = 0; l < kTB; ++l) s = fma(sA[i * kPad + l], sB[l * kPad + jj], s);
     }
-    C[(size_t)jj * kTB + i] = s;
+    C[chain_idx(I, k - 1, i, jj)] = s;
   }
 }
 
@@ -658,8 +741,23 @@ cudaError_t coop_blocks(int* out) {
     cudaError_t e = cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRingSmem);
     if (e != cudaSuccess) return e;
+    // clusters of two co-resident CTAs (the chain pair); workers come in pairs too
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kChainCtas * 16);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kRingSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kChainCtas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&clusters, (void*)trsv_kernel, &cfg);
+    if (e != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, kRingSmem);
-    g_coop_blocks = std::max(2, sms * per);
+    g_coop_blocks = std::min(sms * per, clusters * kChainCtas) & ~(kChainCtas - 1);
   }
   *out = g_coop_blocks;
   return cudaSuccess;
@@ -706,9 +804,21 @@ DistArgs make_args(TriFactor* const* ts, const double* const* bs, int nloc, int 
 }
 
 cudaError_t launch(const DistArgs& a, cudaStream_t st) {
-  void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((const void*)trsv_kernel, a.nloc * a.gper, kThreads, args,
-                                     kRingSmem, st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.nloc * a.gper));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kRingSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;  // co-residency: grid barrier + spin waits
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = kChainCtas;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, trsv_kernel, a);
 }
 
 }  // namespace
@@ -802,8 +912,8 @@ cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
   int blocks = 0;
   cudaError_t e = coop_blocks(&blocks);
   if (e != cudaSuccess) return e;
-  // one chain CTA + up to one worker per block row
-  const int gper = std::min(blocks, t.nb + 1);
+  // the chain pair + up to one worker per block row, in whole clusters
+  const int gper = std::min(blocks, std::max(2 * kChainCtas, (t.nb + kChainCtas + 1) & ~(kChainCtas - 1)));
   TriFactor* ts[1] = {&t};
   const double* bs[1] = {b};
   return launch(make_args(ts, bs, 1, gper), st);
@@ -814,8 +924,8 @@ cudaError_t trsv_solve_emulated(TriFactor* const* ts, const double* const* bs, i
   int blocks = 0;
   cudaError_t e = coop_blocks(&blocks);
   if (e != cudaSuccess) return e;
-  const int gper = blocks / P;
-  if (gper < 2) return cudaErrorInvalidValue;
+  const int gper = (blocks / P) & ~(kChainCtas - 1);
+  if (gper < 2 * kChainCtas) return cudaErrorInvalidValue;
   return launch(make_args(ts, bs, P, gper), st);
 }
 

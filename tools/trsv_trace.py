@@ -28,7 +28,7 @@ cf, cb, wf, wb = a[:nb] - t0, a[nb:2 * nb] - t0, a[2 * nb:3 * nb] - t0, a[3 * nb
 det = np.array(buf[4 * nb + 1:8 * nb + 1], dtype=np.float64).reshape(nb, 4)  # SM cycles
 ph = np.stack([det[:, 1] - det[:, 0], det[:, 2] - det[:, 1], det[:, 3] - det[:, 2],
                np.concatenate([det[1:, 0] - det[:-1, 3], [np.nan]])], 1)[3:-1]
-detail = {"unit": "SM cycles (median)", "fma": float(np.median(ph[:, 0])), "bar1": float(np.median(ph[:, 1])),
+detail = {"unit": "SM cycles (median)", "tile_wait": float(np.median(ph[:, 0])), "peer_fma_bar1": float(np.median(ph[:, 1])),
           "c_resolve": float(np.median(ph[:, 2])), "push_bar2_next_issue": float(np.median(ph[:, 3])),
           "step_total": float(np.median(np.diff(det[:, 0])))}
 out = {"nb": nb, "fwd_detail": detail, "fwd_chain_end_us": cf[-1] / 1e3, "bwd_chain_end_us": cb[0] / 1e3,
