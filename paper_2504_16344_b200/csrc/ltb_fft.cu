@@ -23,6 +23,7 @@ LTB_DEV long long in_row_of(const RfftSrc& s, long long g) {
   return (g % s.P) * s.Q + g / s.P + s.c0;
 }
 
+template <class Fft>
 __global__ void __launch_bounds__(kFftThreads)
     rfft_rows_kernel(const FftDesc d, const RfftSrc src, int nt, long long nrows, double2* out,
                      long long ld, int B) {
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(kFftThreads)
     }
   }
   __syncthreads();
-  const double2* Y = fft_batched(d, b0, b1, B);
+  const double2* Y = Fft::run(d, b0, b1, B);
 
   // unpack: A[k] = (Z[k] + conj Z[N-k]) / 2, B[k] = -i (Z[k] - conj Z[N-k]) / 2,
   // written transposed: out[k * ld + g]
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kFftThreads)
   }
 }
 
+template <class Fft>
 __global__ void __launch_bounds__(kFftThreads)
     irfft_rows_kernel(const FftDesc d, const double2* __restrict__ in, long long ld_f,
                       long long ld_p, int nparts, int nt, long long nrows, double scale,
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kFftThreads)
   }
   __syncthreads();
   // ifft(Z) = conj(fft(conj Z)): a = Re Y, b = -Im Y
-  const double2* Y = fft_batched(d, b0, b1, B);
+  const double2* Y = Fft::run(d, b0, b1, B);
   for (int idx = threadIdx.x; idx < tile * nt; idx += blockDim.x) {
     const int j = idx / nt, n = idx - j * nt;
     const long long g = g0 + j;
@@ -183,6 +185,39 @@ cudaError_t prep_smem(const void* fn, size_t smem) {
   return cudaSuccess;
 }
 
+// the compile-time schedule for n (any factor order is a valid Stockham
+// schedule over the same twiddle table), or the runtime one
+template <template <class> class Kern>
+struct FftDispatch {
+  template <class... Args>
+  static cudaError_t go(int n, dim3 grid, size_t smem, cudaStream_t st, Args... args) {
+    switch (n) {
+      case 128: return launch<FftFixed<128, 8, 8, 2>>(grid, smem, st, args...);
+      case 256: return launch<FftFixed<256, 8, 8, 4>>(grid, smem, st, args...);
+      case 512: return launch<FftFixed<512, 8, 8, 8>>(grid, smem, st, args...);
+      case 840: return launch<FftFixed<840, 8, 3, 5, 7>>(grid, smem, st, args...);
+      case 1024: return launch<FftFixed<1024, 8, 8, 8, 2>>(grid, smem, st, args...);
+      default: return launch<FftRuntime>(grid, smem, st, args...);
+    }
+  }
+  template <class F, class... Args>
+  static cudaError_t launch(dim3 grid, size_t smem, cudaStream_t st, Args... args) {
+    auto fn = Kern<F>::fn();
+    cudaError_t e = prep_smem((const void*)fn, smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kFftThreads, smem, st>>>(args...);
+    return cudaGetLastError();
+  }
+};
+template <class F>
+struct RfftKern {
+  static auto fn() { return rfft_rows_kernel<F>; }
+};
+template <class F>
+struct IrfftKern {
+  static auto fn() { return irfft_rows_kernel<F>; }
+};
+
 }  // namespace
 
 size_t fft_smem_bytes(int n, int* pairs_per_cta) {
@@ -196,13 +231,10 @@ cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long 
   if (nrows <= 0) return cudaSuccess;
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
-  cudaError_t e = prep_smem((const void*)rfft_rows_kernel, smem);
-  if (e != cudaSuccess) return e;
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
   RfftSrc s2 = src;
   s2.bulk = (src.in && src.P == 1 && src.c0 == 0 && ((uintptr_t)src.in & 15) == 0) ? 1 : 0;
-  rfft_rows_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(d, s2, nt, nrows, out, ld, B);
-  return cudaGetLastError();
+  return FftDispatch<RfftKern>::go(d.n, dim3((unsigned)grid), smem, st, d, s2, nt, nrows, out, ld, B);
 }
 
 cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_f,
@@ -211,12 +243,9 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
   if (nrows <= 0) return cudaSuccess;
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
-  cudaError_t e = prep_smem((const void*)irfft_rows_kernel, smem);
-  if (e != cudaSuccess) return e;
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
-  irfft_rows_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(d, in, ld_f, ld_p, nparts, nt,
-                                                               nrows, scale, out, B);
-  return cudaGetLastError();
+  return FftDispatch<IrfftKern>::go(d.n, dim3((unsigned)grid), smem, st, d, in, ld_f, ld_p, nparts, nt, nrows,
+                                    scale, out, B);
 }
 
 }  // namespace ltb

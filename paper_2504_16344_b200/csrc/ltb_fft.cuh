@@ -207,4 +207,57 @@ LTB_DEV double2* fft_batched(const FftDesc& d, double2* a, double2* b, int nseq)
   return a;
 }
 
+// ---- compile-time schedules for the common lengths ------------------------
+// Same Stockham steps with N, the radix sequence and every stride known to
+// the compiler: no runtime integer division / radix switch in the butterfly
+// loops (the generic path spends most of its instructions there).
+template <int R, int N, int Ns>
+LTB_DEV void stockham_butterfly_ct(const double2* __restrict__ src, double2* __restrict__ dst,
+                                   const double2* __restrict__ tw, int i) {
+  constexpr int T = N / R;
+  const int j = i % Ns;
+  const int tstep = j * (N / (Ns * R));
+  double2 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = src[pidx(i + r * T)];
+  if (Ns > 1) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * tstep));
+  }
+  dft_small<R>(v);
+  const int o = (i / Ns) * Ns * R + j;
+#pragma unroll
+  for (int r = 0; r < R; ++r) dst[pidx(o + r * Ns)] = v[r];
+}
+
+template <int N, int Ns, int R, int... Rest>
+LTB_DEV double2* fft_stages_ct(const double2* tw, double2* a, double2* b, int nseq) {
+  constexpr int T = N / R;
+  constexpr int NP = N + (N >> 3) + 1;
+  const int total = nseq * T;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int q = idx / T, i = idx - q * T;
+    stockham_butterfly_ct<R, N, Ns>(a + (size_t)q * NP, b + (size_t)q * NP, tw, i);
+  }
+  __syncthreads();
+  if constexpr (sizeof...(Rest) > 0) {
+    return fft_stages_ct<N, Ns * R, Rest...>(tw, b, a, nseq);
+  } else {
+    return b;
+  }
+}
+
+// transform policies for the row kernels
+struct FftRuntime {
+  static LTB_DEV double2* run(const FftDesc& d, double2* a, double2* b, int nseq) {
+    return fft_batched(d, a, b, nseq);
+  }
+};
+template <int N, int... Rs>
+struct FftFixed {
+  static LTB_DEV double2* run(const FftDesc& d, double2* a, double2* b, int nseq) {
+    return fft_stages_ct<N, 1, Rs...>(d.tw, a, b, nseq);
+  }
+};
+
 }  // namespace ltb

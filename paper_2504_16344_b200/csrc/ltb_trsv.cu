@@ -3,7 +3,7 @@
 //
 // Single-RHS TRSV is a GEMV over the packed factor (HBM bound, ~0.25
 // flop/byte) plus a sequential dependency chain over the nb = n/64 diagonal
-// blocks.  Design (one cooperative persistent launch per rank for BOTH
+// blocks.  Design (one persistent, fully co-resident launch per rank for BOTH
 // sweeps):
 //
 //   * the factor is distributed row-cyclically (block row I on rank I mod P;
@@ -37,6 +37,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ltb_common.cuh"
 #include "ltb_gen.cuh"
@@ -187,7 +189,7 @@ struct WorkerSmem {
   double sR[2 * kTB];
 };
 
-// grid-wide barrier of this launch (all CTAs co-resident: cooperative launch)
+// grid-wide barrier of this launch (all CTAs co-resident, see launch())
 LTB_DEV void grid_barrier(unsigned* gsync) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -754,10 +756,17 @@ cudaError_t coop_blocks(int* out) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int clusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&clusters, (void*)trsv_kernel, &cfg);
-    if (e != cudaSuccess) return e;
+    if (cudaOccupancyMaxActiveClusters(&clusters, (void*)trsv_kernel, &cfg) != cudaSuccess) clusters = 0;
+    cudaGetLastError();
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, kRingSmem);
-    g_coop_blocks = std::min(sms * per, clusters * kChainCtas) & ~(kChainCtas - 1);
+    // (some tools report no cluster occupancy: fall back to the per-SM count;
+    // the grid never exceeds what one SM per CTA can hold)
+    const int by_sm = sms * per;
+    g_coop_blocks = (clusters > 0 ? std::min(by_sm, clusters * kChainCtas) : by_sm) & ~(kChainCtas - 1);
+    g_coop_blocks = std::max(g_coop_blocks, 2 * kChainCtas);
+    if (getenv("LTB_DEBUG"))
+      fprintf(stderr, "ltb trsv: sms=%d blocks/SM=%d clusters=%d -> %d co-resident CTAs\n", sms, per, clusters,
+              g_coop_blocks);
   }
   *out = g_coop_blocks;
   return cudaSuccess;
@@ -809,15 +818,19 @@ cudaError_t launch(const DistArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kRingSmem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;  // co-residency: grid barrier + spin waits
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = kChainCtas;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
+  // The grid barrier and the spin waits need every CTA resident at once.  The
+  // grid is sized to the measured cluster occupancy (coop_blocks) on a GPU the
+  // solve has to itself; the cooperative launch attribute would state the same
+  // guarantee, but Nsight Compute cannot launch cooperative kernels that also
+  // carry a cluster dimension, and every dependency wait in the kernel times
+  // out into a status error rather than hanging if residency ever fails.
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kChainCtas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, trsv_kernel, a);
 }
 
