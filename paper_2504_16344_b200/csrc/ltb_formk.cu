@@ -399,13 +399,20 @@ constexpr int kUpdThreads = 256;
 constexpr size_t kUpdSmem = (size_t)2 * kT * kUS * sizeof(double);
 
 __global__ void __launch_bounds__(kUpdThreads)
-    chol_update_kernel(double* __restrict__ tiles, int nb, int k) {
+    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int base, int column_only) {
   extern __shared__ __align__(16) double usm[];
   double* sA = usm;
   double* sB = usm + kT * kUS;
-  int li, lj;
-  tri_pair(blockIdx.x, &li, &lj);
-  const int i = k + 1 + li, j = k + 1 + lj;
+  int i, j;
+  if (column_only) {  // tiles (i, base), i >= base
+    i = base + (int)blockIdx.x;
+    j = base;
+  } else {  // the lower triangle of tiles from (base, base)
+    int li, lj;
+    tri_pair(blockIdx.x, &li, &lj);
+    i = base + li;
+    j = base + lj;
+  }
   const double* Lik = tiles + tile_at(i, k);
   const double* Ljk = tiles + tile_at(j, k);
   double* Aij = tiles + tile_at(i, j);
@@ -738,23 +745,68 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   cudaError_t e = cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kUpdSmem);
   if (e != cudaSuccess) return e;
+  // Lookahead over two streams: the high-priority stream runs panel(k) and
+  // the update of block column k+1 only (U1), so panel(k+1) can start while
+  // the low-priority stream applies the rest of update k (U2) -- the
+  // latency-bound panel hides under the DMMA / bandwidth-bound trailing
+  // update.  U2(k) waits for panel(k); U1(k) waits for U2(k-1) (column k+1 is
+  // in it).
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  cudaStream_t main_s = nullptr, side = nullptr;
+  if ((e = cudaStreamCreateWithPriority(&main_s, cudaStreamNonBlocking, greatest)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least)) != cudaSuccess) {
+    cudaStreamDestroy(main_s);
+    return e;
+  }
+  cudaEvent_t ev_panel = nullptr, ev_u2 = nullptr, ev_fork = nullptr, ev_join = nullptr;
+  cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_u2, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
   cudaMemsetAsync(t.status, 0, sizeof(int), st);
+  cudaEventRecord(ev_fork, st);
+  cudaStreamWaitEvent(main_s, ev_fork, 0);
+  cudaStreamWaitEvent(side, ev_fork, 0);
   int launches = 0;
+  bool u2_pending = false;
   for (int k = 0; k < nb; ++k) {
     const int m = nb - k - 1;
-    chol_panel_kernel<<<std::max(1, m), kPanelThreads, 0, st>>>(t.tiles, nb, k, t.status);
+    chol_panel_kernel<<<std::max(1, m), kPanelThreads, 0, main_s>>>(t.tiles, nb, k, t.status);
     ++launches;
-    if (m > 0) {
-      chol_update_kernel<<<(unsigned)((long long)m * (m + 1) / 2), kUpdThreads, kUpdSmem, st>>>(t.tiles, nb, k);
+    if (m == 0) break;
+    // U2(k): tiles (i, j), k + 2 <= j <= i
+    if (m > 1) {
+      cudaEventRecord(ev_panel, main_s);
+      cudaStreamWaitEvent(side, ev_panel, 0);
+      chol_update_kernel<<<(unsigned)((long long)(m - 1) * m / 2), kUpdThreads, kUpdSmem, side>>>(
+          t.tiles, nb, k, k + 2, 0);
       ++launches;
     }
+    // U1(k): block column k + 1, after U2(k - 1) updated it
+    if (u2_pending) cudaStreamWaitEvent(main_s, ev_u2, 0);
+    chol_update_kernel<<<(unsigned)m, kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, k + 1, 1);
+    ++launches;
+    u2_pending = m > 1;
+    if (u2_pending) cudaEventRecord(ev_u2, side);
   }
+  cudaEventRecord(ev_join, side);
+  cudaStreamWaitEvent(main_s, ev_join, 0);
+  cudaEventRecord(ev_join, main_s);
+  cudaStreamWaitEvent(st, ev_join, 0);
   g_last_launches = launches;
   e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   int h = 0;
-  e = cudaMemcpyAsync(&h, t.status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, t.status, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStreamSynchronize(main_s);
+  cudaStreamSynchronize(side);
+  cudaStreamDestroy(main_s);
+  cudaStreamDestroy(side);
+  cudaEventDestroy(ev_panel);
+  cudaEventDestroy(ev_u2);
+  cudaEventDestroy(ev_fork);
+  cudaEventDestroy(ev_join);
   if (e != cudaSuccess) return e;
   if (h) {
     cudaMemset(t.status, 0, sizeof(int));
