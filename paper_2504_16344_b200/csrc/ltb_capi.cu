@@ -132,6 +132,9 @@ struct ltb_scratch {
   double* stage_in = nullptr;   // host-pointer staging (lazily allocated)
   double* stage_out = nullptr;
   size_t stage_in_n = 0, stage_out_n = 0;
+  // host-pointer pipelining: a copy stream and per-chunk events
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t pipe_ev[17] = {};
   // per-stage timing (ltb_scratch_timing): 4 events per timed apply
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -273,6 +276,77 @@ ltb_status apply_adjoint_dev(const ltb_plan* p, ltb_scratch* s, const double* d,
 
 using DevFn = ltb_status (*)(const ltb_plan*, ltb_scratch*, const double*, double*);
 
+// Host-pointer applies move n_cols * N_t values one way (m in for F m, m out
+// for F* d): 110 MB at Cascadia, ~2 ms over PCIe.  Cut into column chunks,
+// those copies run on a second stream against the transforms and GEMVs of
+// the other chunks (GEMV-N accumulates the chunks' products into y-hat in
+// chunk order, so the result is deterministic).  Returns LTB_OK after the
+// results are on the host.
+constexpr size_t kPipeMinBytes = 16u << 20;
+constexpr int kPipeChunks = 8;
+
+ltb_status pipe_setup(ltb_scratch* s) {
+  if (!s->copy_stream) LTB_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : s->pipe_ev)
+    if (!e) LTB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return LTB_OK;
+}
+
+ltb_status apply_host_pipelined(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
+                                bool adjoint) {
+  ltb_status st = pipe_setup(s);
+  if (st != LTB_OK) return st;
+  const cudaStream_t cs = s->stream, xs = s->copy_stream;
+  const long long cols = p->cols, nt = p->nt;
+  long long cc = (cols + kPipeChunks - 1) / kPipeChunks;
+  cc = (cc + p->shape.unit_cols - 1) / p->shape.unit_cols * p->shape.unit_cols;  // whole GEMV units
+  const int K = (int)((cols + cc - 1) / cc);
+  // order the copy stream after everything already queued on the compute stream
+  LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[16], cs));
+  LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[16], 0));
+  if (!adjoint) {
+    for (int k = 0; k < K; ++k) {
+      const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+      LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in + c0 * nt, in + c0 * nt, sizeof(double) * nc * nt,
+                                   cudaMemcpyHostToDevice, xs));
+      LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], xs));
+    }
+    for (int k = 0; k < K; ++k) {
+      const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+      LTB_CUDA_TRY(cudaStreamWaitEvent(cs, s->pipe_ev[k], 0));
+      RfftSrc src{s->stage_in + c0 * nt, 0, 1, 0, 0};
+      LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, nc, s->xhat + c0, cols, cs), 1);
+      LTB_LAUNCH(launch_gemv_n(gemv_window(p->shape, c0, nc, k > 0), p->fhat, s->xhat, s->partials, s->dhat,
+                               s->tickets, cs),
+                 1);
+    }
+    LTB_LAUNCH(launch_irfft_rows(p->fft, s->dhat, p->rows, 0, 1, p->nt, p->rows, 1.0 / p->npad, s->stage_out,
+                                 cs),
+               1);
+    LTB_CUDA_TRY(cudaMemcpyAsync(out, s->stage_out, sizeof(double) * p->rows * nt, cudaMemcpyDeviceToHost, cs));
+    LTB_CUDA_TRY(cudaStreamSynchronize(cs));
+    LTB_CUDA_TRY(cudaStreamSynchronize(xs));
+    return LTB_OK;
+  }
+  LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in, in, sizeof(double) * p->rows * nt, cudaMemcpyHostToDevice, cs));
+  RfftSrc src{s->stage_in, 0, 1, 0, 0};
+  LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, p->rows, s->dhat, p->rows, cs), 1);
+  for (int k = 0; k < K; ++k) {
+    const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+    LTB_LAUNCH(launch_gemv_h(gemv_window(p->shape, c0, nc, 0), p->fhat, s->dhat, s->xhat, cs), 1);
+    LTB_LAUNCH(launch_irfft_rows(p->fft, s->xhat + c0, cols, 0, 1, p->nt, nc, 1.0 / p->npad,
+                                 s->stage_out + c0 * nt, cs),
+               1);
+    LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], cs));
+    LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[k], 0));
+    LTB_CUDA_TRY(cudaMemcpyAsync(out + c0 * nt, s->stage_out + c0 * nt, sizeof(double) * nc * nt,
+                                 cudaMemcpyDeviceToHost, xs));
+  }
+  LTB_CUDA_TRY(cudaStreamSynchronize(cs));
+  LTB_CUDA_TRY(cudaStreamSynchronize(xs));
+  return LTB_OK;
+}
+
 ltb_status run_apply(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
                      int ptr_kind, bool adjoint) {
   if (!p || !s) return fail(LTB_INVALID, "apply: null plan or scratch");
@@ -286,6 +360,8 @@ ltb_status run_apply(const ltb_plan* p, ltb_scratch* s, const double* in, double
   if (ptr_kind != LTB_PTR_HOST) return fail(LTB_INVALID, "apply: bad ptr_kind %d", ptr_kind);
   ltb_status st = ensure_stage(s, std::max(nin, nout), std::max(nin, nout));
   if (st != LTB_OK) return st;
+  if (!s->timing && (size_t)p->cols * p->nt * sizeof(double) >= kPipeMinBytes)
+    return apply_host_pipelined(p, s, in, out, adjoint);
   LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in, in, sizeof(double) * nin, cudaMemcpyHostToDevice, s->stream));
   st = fn(p, s, s->stage_in, s->stage_out);
   if (st != LTB_OK) return st;
@@ -477,6 +553,9 @@ ltb_status ltb_scratch_destroy(ltb_scratch* s) {
   cudaFree(s->stage_in);
   cudaFree(s->stage_out);
   for (cudaEvent_t e : s->events) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->pipe_ev)
+    if (e) cudaEventDestroy(e);
+  if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
   if (s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
   return LTB_OK;

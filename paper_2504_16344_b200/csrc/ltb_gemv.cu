@@ -47,8 +47,8 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
   const int f = unit / s.units_per_f;
   const int u = unit - f * s.units_per_f;
   const int row0 = blockIdx.y * RT * RPT;  // row tile
-  const long long c_begin = (long long)u * s.unit_cols;
-  const long long c_end = min(s.nm, c_begin + s.unit_cols);
+  const long long c_begin = s.c0 + (long long)u * s.unit_cols;
+  const long long c_end = min(s.c0 + s.nc, c_begin + s.unit_cols);
   const int t = threadIdx.x;
   const int rt = t % RT, cl = t / RT;
   const bool active = cl < CL;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
     const int r = row0 + i;
     double2 v = __ldcg(Pf + r);
     for (int q = 1; q < s.units_per_f; ++q) v = cadd(v, __ldcg(Pf + (long long)q * s.nd + r));
-    y[(long long)f * s.nd + r] = v;
+    y[(long long)f * s.nd + r] = s.accumulate ? cadd(y[(long long)f * s.nd + r], v) : v;
   }
 }
 
@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
   const int unit = blockIdx.x;
   const int f = unit / s.units_per_f;
   const int u = unit - f * s.units_per_f;
-  const long long c_begin = (long long)u * s.unit_cols;
-  const long long c_end = min(s.nm, c_begin + s.unit_cols);
+  const long long c_begin = s.c0 + (long long)u * s.unit_cols;
+  const long long c_end = min(s.c0 + s.nc, c_begin + s.unit_cols);
   const int ncols = (int)(c_end - c_begin);
   const int nchunks = (ncols + cps - 1) / cps;
   const int t = threadIdx.x;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kGemvNMaxThreads)
   for (int r = t; r < s.nd; r += blockDim.x) {
     double2 v = __ldcg(Pf + r);
     for (int q = 1; q < s.units_per_f; ++q) v = cadd(v, __ldcg(Pf + (long long)q * s.nd + r));
-    y[(long long)f * s.nd + r] = v;
+    y[(long long)f * s.nd + r] = s.accumulate ? cadd(y[(long long)f * s.nd + r], v) : v;
   }
 }
 
@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(kGemvThreads)
   const int unit = blockIdx.x;
   const int f = unit / s.units_per_f;
   const int u = unit - f * s.units_per_f;
-  const long long c_begin = (long long)u * s.unit_cols;
-  const long long c_end = min(s.nm, c_begin + s.unit_cols);
+  const long long c_begin = s.c0 + (long long)u * s.unit_cols;
+  const long long c_end = min(s.c0 + s.nc, c_begin + s.unit_cols);
   const int ncols = (int)(c_end - c_begin);
   const int nchunks = (ncols + cps - 1) / cps;
   const int t = threadIdx.x;
@@ -345,8 +345,8 @@ __global__ void __launch_bounds__(kGemvThreads)
   const int unit = blockIdx.x;
   const int f = unit / s.units_per_f;
   const int u = unit - f * s.units_per_f;
-  const long long c_begin = (long long)u * s.unit_cols;
-  const long long c_end = min(s.nm, c_begin + s.unit_cols);
+  const long long c_begin = s.c0 + (long long)u * s.unit_cols;
+  const long long c_end = min(s.c0 + s.nc, c_begin + s.unit_cols);
   for (int r = threadIdx.x; r < s.nd; r += blockDim.x) dsm[r] = __ldg(dhat + (long long)f * s.nd + r);
   __syncthreads();
   const int lane = threadIdx.x % GS;
@@ -456,7 +456,19 @@ GemvShape gemv_shape(int nd, long long nm, int nf, int unit_cols_hint) {
   uc = std::min(uc, nm);
   s.unit_cols = (int)uc;
   s.units_per_f = (int)((nm + uc - 1) / uc);
+  s.c0 = 0;
+  s.nc = nm;
+  s.accumulate = 0;
   return s;
+}
+
+GemvShape gemv_window(const GemvShape& s, long long c0, long long nc, int accumulate) {
+  GemvShape w = s;
+  w.c0 = c0;
+  w.nc = nc;
+  w.units_per_f = (int)((nc + s.unit_cols - 1) / s.unit_cols);
+  w.accumulate = accumulate;
+  return w;
 }
 
 size_t gemv_n_partials(const GemvShape& s) {

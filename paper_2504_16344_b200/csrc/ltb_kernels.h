@@ -40,12 +40,18 @@ size_t fft_smem_bytes(int n, int* pairs_per_cta);
 // ---- per-frequency GEMVs (K2 / K3) ----
 struct GemvShape {
   int nd;          // rows of each frequency block
-  long long nm;    // columns
+  long long nm;    // columns (the per-frequency stride of F-hat / x-hat)
   int nf;          // frequencies
   int unit_cols;   // columns per work unit
   int units_per_f;
+  // column window [c0, c0 + nc) this launch covers (the host-pointer applies
+  // pipeline the copies against column chunks); GEMV-N with accumulate != 0
+  // adds the window's products into y instead of overwriting it
+  long long c0 = 0, nc = 0;
+  int accumulate = 0;
 };
 GemvShape gemv_shape(int nd, long long nm, int nf, int unit_cols_hint);
+GemvShape gemv_window(const GemvShape& s, long long c0, long long nc, int accumulate);
 
 // Y[f][r] = sum_c Fhat[f][c][r] * X[f][c]; per-unit partials go to
 // `partials` (gemv_n_partials(s) entries), `tickets` holds
