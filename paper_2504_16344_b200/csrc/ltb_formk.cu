@@ -64,8 +64,8 @@ LTB_DEV void cp_wait() {
 // loads of a half-warp hit 32 distinct banks).
 // ---------------------------------------------------------------------------
 constexpr int kBM = 128;
-constexpr int kBK = 16;
-constexpr int kStages = 4;
+constexpr int kBK = 32;
+constexpr int kStages = 3;
 constexpr int kSS = kBM + 4;
 constexpr int kGemmThreads = 256;
 constexpr size_t kStageDoubles = (size_t)2 * kBK * kSS;
@@ -79,7 +79,7 @@ LTB_DEV void gram_load_stage(double* sA, double* sB, const double* f, const doub
     // thread: row pair m = 2 (tid & 63), x rows kr + 4 q
     const int m = 2 * (tid & 63), kr = tid >> 6;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kBK / 4; ++q) {
       const int k = kr + 4 * q, x = x0 + k;
       const bool okx = x < nm;
       cp_async16(sA + k * kSS + m, (pa && okx) ? pa + (size_t)x * nt : f, (pa && okx) ? 16 : 0);
@@ -89,7 +89,7 @@ LTB_DEV void gram_load_stage(double* sA, double* sB, const double* f, const doub
     // thread: row m = tid & 127, x rows kr + 2 q
     const int m = tid & 127, kr = tid >> 7;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < kBK / 2; ++q) {
       const int k = kr + 2 * q, x = x0 + k;
       const bool okx = x < nm;
       cp_async8(sA + k * kSS + m, (pa && okx) ? pa + (size_t)x * nt : f, (pa && okx) ? 8 : 0);
