@@ -312,6 +312,21 @@ ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned long long* 
 ltb_status ltb_debug_dtrsv_emulated(int n, int P, uint64_t seed, const double* b_host,
                                     double* x_host, double* max_rank_diff, double* seconds);
 
+/* infer_map's untimed normal-equation residual (bayes_engine.cpp:322-336):
+ * || (F*F / sigma2 + Gamma_prior^{-1}) m_map - F* d / sigma2 || / || F* d / sigma2 ||,
+ * evaluated with three F-plan applies and the prior precision A_x^2 per time
+ * slice (prior.cpp:44-47,82-92).  set_residual_model gives the engine the F
+ * plan (not only G*), sigma2 and the prior {h_x, gamma, delta}. */
+ltb_status ltb_engine_set_residual_model(ltb_engine* e, const ltb_plan* plan_f, double sigma2,
+                                         double h_x, double gamma, double delta);
+ltb_status ltb_engine_map_residual(const ltb_engine* e, ltb_scratch* s, const double* d,
+                                   const double* m_map, double* rel_residual, int ptr_kind);
+
+/* integrate_displacement (bayes_engine.cpp:411-419): out[x] = dt_obs *
+ * sum_j m[x][j] of a SpaceMajorRows field (n_rows x n_time) */
+ltb_status ltb_integrate_displacement(const double* m, int n_rows, int n_time, double dt_obs,
+                                      double* out, int ptr_kind);
+
 /* infer_map + forecast in one call: m_map and q (either nullable) */
 ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e, ltb_scratch* s,
                                          const double* d, double* m_map, double* q,

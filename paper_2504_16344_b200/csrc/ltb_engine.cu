@@ -77,6 +77,11 @@ struct ltb_engine {
   bool factorized = false;
   bool kformed = false;          // factor.tiles hold K (form_K), not yet factorized
   double formk_ms = 0.0, factorize_ms = 0.0, formq_ms = 0.0;
+  // infer_map's untimed normal-equation residual (bayes_engine.cpp:322-336)
+  const ltb_plan* plan_f = nullptr;
+  double sigma2 = 0.0, prior_w = 0.0, prior_delta = 0.0;
+  ltb_scratch* f_scratch = nullptr;
+  cudaStream_t f_stream = nullptr;
   double* ypad = nullptr;       // nb * 64
   double* stage_in = nullptr;   // host-pointer staging: d (nd*nt)
   double* stage_m = nullptr;    // m_map (nm*nt)
@@ -132,6 +137,7 @@ ltb_status ltb_engine_destroy(ltb_engine* e) {
   cudaFree(e->stage_m);
   cudaFree(e->stage_q);
   if (e->fq_scratch) ltb_scratch_destroy(e->fq_scratch);
+  if (e->f_scratch) ltb_scratch_destroy(e->f_scratch);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   release_phase3(e);
@@ -1145,5 +1151,140 @@ extern "C" ltb_status ltb_engine_export_phase3(const ltb_engine* e, double* Q, s
   if (Q) ENG_CUDA(cudaMemcpy2D(Q, ldq * 8, op.Q, (size_t)op.ldp * 8, m * 8, (size_t)op.cols, k));
   if (gpost) ENG_CUDA(cudaMemcpy2D(gpost, ldg * 8, op.gpost, m * 8, m * 8, m, k));
   if (prior_cov) ENG_CUDA(cudaMemcpy2D(prior_cov, ldg * 8, op.prior_cov, m * 8, m * 8, m, k));
+  return LTB_OK;
+}
+
+// ---- infer_map's normal-equation residual and integrate_displacement ----
+namespace {
+
+// out = A_x v on every time slice of a SpaceMajorRows field (nm x nt):
+// A_x = delta I - gamma L_Neumann / h_x^2 (prior.cpp:16-31), i.e. diagonal
+// delta + w (#neighbours), off-diagonals -w
+__global__ void apply_ax_kernel(const double* __restrict__ v, int nm, int nt, double w, double delta,
+                                double* __restrict__ out) {
+  const long long n = (long long)nm * nt;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(e / nt);
+    double acc = delta * v[e];
+    if (x > 0) acc += w * (v[e] - v[e - nt]);
+    if (x + 1 < nm) acc += w * (v[e] - v[e + nt]);
+    out[e] = acc;
+  }
+}
+
+// r = ftfm / s2 + prec - b / s2; b_scaled = b / s2 (both padded with a zero)
+__global__ void residual_kernel(const double* __restrict__ ftfm, const double* __restrict__ prec,
+                                const double* __restrict__ b, long long n, double inv_s2,
+                                double* __restrict__ r, double* __restrict__ bs) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const double bb = b[e] * inv_s2;
+    r[e] = ftfm[e] * inv_s2 + prec[e] - bb;
+    bs[e] = bb;
+  }
+}
+
+__global__ void integrate_kernel(const double* __restrict__ m, int n_rows, int n_time, double dt,
+                                 double* __restrict__ out) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n_rows; x += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < n_time; ++j) acc += m[(size_t)x * n_time + j];  // bayes_engine.cpp:415-417
+    out[x] = acc * dt;
+  }
+}
+
+}  // namespace
+
+extern "C" ltb_status ltb_engine_set_residual_model(ltb_engine* e, const ltb_plan* plan_f, double sigma2,
+                                                    double h_x, double gamma, double delta) {
+  if (!e || !plan_f) return efail(LTB_INVALID, "set_residual_model: null argument");
+  int r, c, t;
+  plan_dims(plan_f, &r, &c, &t);
+  if (r != e->nd || c != e->nm || t != e->nt) return efail(LTB_DIMENSION, "set_residual_model: F plan dims differ from the engine");
+  if (!(sigma2 > 0)) return efail(LTB_CONFIG, "set_residual_model: sigma2 must be positive");
+  if (!(h_x > 0) || !(delta > 0) || gamma < 0) return efail(LTB_CONFIG, "set_residual_model: invalid prior parameters");
+  e->plan_f = plan_f;
+  e->sigma2 = sigma2;
+  e->prior_w = gamma / (h_x * h_x);
+  e->prior_delta = delta;
+  return LTB_OK;
+}
+
+extern "C" ltb_status ltb_engine_map_residual(const ltb_engine* e_, ltb_scratch* s, const double* d,
+                                              const double* m_map, double* rel_residual, int ptr_kind) {
+  ltb_engine* e = const_cast<ltb_engine*>(e_);
+  if (!e || !s || !d || !m_map || !rel_residual) return efail(LTB_INVALID, "map_residual: null argument");
+  if (!e->plan_f) return efail(LTB_STATE, "engine: no residual model (set_residual_model)");
+  Guard gd(e->device);
+  const cudaStream_t st = scratch_stream(s);
+  if (e->f_scratch && e->f_stream != st) {
+    ltb_scratch_destroy(e->f_scratch);
+    e->f_scratch = nullptr;
+  }
+  if (!e->f_scratch) {
+    ltb_status r = ltb_scratch_create(e->plan_f, (void*)st, &e->f_scratch);
+    if (r != LTB_OK) return r;
+    e->f_stream = st;
+  }
+  const long long nd = (long long)e->nd * e->nt, nmt = (long long)e->nm * e->nt;
+  DevArr dd, mm, fm, ftfm, b, prec, tmp, r, bs, work, nrm;
+  ENG_CUDA(fm.alloc(nd));
+  ENG_CUDA(ftfm.alloc(nmt));
+  ENG_CUDA(b.alloc(nmt));
+  ENG_CUDA(prec.alloc(nmt));
+  ENG_CUDA(tmp.alloc(nmt));
+  ENG_CUDA(r.alloc(nmt + 1, true));
+  ENG_CUDA(bs.alloc(nmt + 1, true));
+  ENG_CUDA(work.alloc(2048));
+  ENG_CUDA(nrm.alloc(2));
+  const double* dsrc = d;
+  const double* msrc = m_map;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(dd.alloc(nd));
+    ENG_CUDA(mm.alloc(nmt));
+    ENG_CUDA(cudaMemcpyAsync(dd.p, d, nd * 8, cudaMemcpyHostToDevice, st));
+    ENG_CUDA(cudaMemcpyAsync(mm.p, m_map, nmt * 8, cudaMemcpyHostToDevice, st));
+    dsrc = dd.p;
+    msrc = mm.p;
+  }
+  ltb_status rs;
+  if ((rs = apply_device(e->plan_f, e->f_scratch, msrc, fm.p, false)) != LTB_OK) return rs;    // F m
+  if ((rs = apply_device(e->plan_f, e->f_scratch, fm.p, ftfm.p, true)) != LTB_OK) return rs;   // F* F m
+  if ((rs = apply_device(e->plan_f, e->f_scratch, dsrc, b.p, true)) != LTB_OK) return rs;      // F* d
+  const unsigned blocks = (unsigned)std::max(1ll, std::min(148ll * 8, (nmt + 255) / 256));
+  apply_ax_kernel<<<blocks, 256, 0, st>>>(msrc, e->nm, e->nt, e->prior_w, e->prior_delta, tmp.p);
+  apply_ax_kernel<<<blocks, 256, 0, st>>>(tmp.p, e->nm, e->nt, e->prior_w, e->prior_delta, prec.p);
+  residual_kernel<<<blocks, 256, 0, st>>>(ftfm.p, prec.p, b.p, nmt, 1.0 / e->sigma2, r.p, bs.p);
+  ENG_CUDA(cudaGetLastError());
+  ENG_CUDA(launch_sqnorm(reinterpret_cast<const double2*>(r.p), (nmt + 1) / 2, work.p, nrm.p, st));
+  ENG_CUDA(launch_sqnorm(reinterpret_cast<const double2*>(bs.p), (nmt + 1) / 2, work.p, nrm.p + 1, st));
+  count_launches(5);
+  double h[2];
+  ENG_CUDA(cudaMemcpyAsync(h, nrm.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  ENG_CUDA(cudaStreamSynchronize(st));
+  *rel_residual = std::sqrt(h[0]) / std::max(std::sqrt(h[1]), 1e-300);
+  return LTB_OK;
+}
+
+extern "C" ltb_status ltb_integrate_displacement(const double* m, int n_rows, int n_time, double dt_obs,
+                                                 double* out, int ptr_kind) {
+  if (!m || !out) return efail(LTB_INVALID, "integrate_displacement: null argument");
+  if (n_rows < 1 || n_time < 1) return efail(LTB_DIMENSION, "integrate_displacement: series dims must be >= 1");
+  const size_t n = (size_t)n_rows * n_time;
+  DevArr dm, dout;
+  const double* src = m;
+  double* dst = out;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(dm.alloc(n));
+    ENG_CUDA(dout.alloc(n_rows));
+    ENG_CUDA(cudaMemcpy(dm.p, m, n * 8, cudaMemcpyHostToDevice));
+    src = dm.p;
+    dst = dout.p;
+  }
+  integrate_kernel<<<(unsigned)std::max(1, std::min(148 * 4, (n_rows + 127) / 128)), 128>>>(src, n_rows, n_time,
+                                                                                           dt_obs, dst);
+  count_launches(1);
+  ENG_CUDA(cudaGetLastError());
+  if (ptr_kind == LTB_PTR_HOST) ENG_CUDA(cudaMemcpy(out, dout.p, (size_t)n_rows * 8, cudaMemcpyDeviceToHost));
+  else ENG_CUDA(cudaDeviceSynchronize());
   return LTB_OK;
 }

@@ -32,9 +32,13 @@ def _kernel_data(k, what):
 
 @dataclass
 class MapResult:
+    """bayes_engine.hpp MapResult: m_map, the device seconds of the timed
+    region, the untimed normal-equation residual (None without a residual
+    model) and, optionally, the forecast."""
     m_map: SpaceTimeField
     seconds: float
     q_map: QoISeries = None
+    smw_rel_residual: float = None
 
 
 @dataclass
@@ -265,7 +269,35 @@ class InferenceEngine:
             self._h, self._scratch._h, C.c_void_p(d_obs.values.ctypes.data),
             C.c_void_p(m.values.ctypes.data), C.c_void_p(q.values.ctypes.data) if q else None,
             C.byref(secs), 0))
-        return MapResult(m, secs.value, q)
+        res = MapResult(m, secs.value, q)
+        if getattr(self, "_resid_plan", None) is not None:
+            r = C.c_double()
+            check(_lib.load().ltb_engine_map_residual(self._h, self._scratch._h,
+                                                      C.c_void_p(d_obs.values.ctypes.data),
+                                                      C.c_void_p(m.values.ctypes.data), C.byref(r), 0))
+            res.smw_rel_residual = r.value
+        return res
+
+    def set_residual_model(self, plan_f, sigma2, prior):
+        """Enable infer_map's untimed normal-equation residual
+        (bayes_engine.cpp:322-336): the F plan, sigma2 and (h_x, gamma, delta)."""
+        h_x, gamma, delta = prior
+        check(_lib.load().ltb_engine_set_residual_model(self._h, plan_f._h, float(sigma2), float(h_x),
+                                                        float(gamma), float(delta)))
+        self._resid_plan = plan_f
+
+    @staticmethod
+    def integrate_displacement(m, dt_obs):
+        """bayes_engine.cpp:411-419: dt * sum over time of every row of m."""
+        m.check_consistent("integrate_displacement")
+        vals = np.ascontiguousarray(m.values, dtype=np.float64)
+        if m.layout != Layout.SpaceMajorRows:  # SpaceTimeField::at() is layout aware
+            from .matvec import reindex as _re
+            vals = _re(m, Layout.SpaceMajorRows).values
+        out = np.empty(m.n_rows)
+        check(_lib.load().ltb_integrate_displacement(C.c_void_p(vals.ctypes.data), m.n_rows, m.n_time,
+                                                     float(dt_obs), C.c_void_p(out.ctypes.data), 0))
+        return out
 
     def infer_raw(self, d, m_map, q=None, scratch=None):
         """Raw-pointer variant (numpy host arrays or CUDA tensors); returns the

@@ -70,9 +70,11 @@ def test_identity_engine(ltb):
         ident[i, i, 0] = 1.0
     eng = ltb.InferenceEngine(plan_of(ltb, ident, 2), plan_of(ltb, ident, 1))
     eng.set_factor(np.sqrt(1 + s2) * np.eye(n * nt))
+    eng.set_residual_model(plan_of(ltb, ident, 0), s2, (1.0, 0.0, 1.0))
     d = np.random.default_rng(2).standard_normal(n * nt)
     res = eng.infer_map(obs(ltb, n, nt, d), with_forecast=True)
     assert np.allclose(res.m_map.values, d / (1 + s2), rtol=1e-12, atol=0)
+    assert res.smw_rel_residual <= 1e-12  # :106
     assert np.allclose(res.q_map.values, d / (1 + s2), rtol=1e-12, atol=0)
     zero = eng.infer_map(obs(ltb, n, nt, np.zeros(n * nt)))
     assert np.all(zero.m_map.values == 0.0)
@@ -108,7 +110,9 @@ def test_pipeline_vs_dense_normal_equations(ltb, nd, nq, nm, nt):
     d = rng.standard_normal(nd * nt)
     eng = ltb.InferenceEngine(plan_of(ltb, g, 2), plan_of(ltb, fq, 1))
     eng.set_factor(L)
+    eng.set_residual_model(plan_of(ltb, f, 0), s2, (h, gamma, delta))
     res = eng.infer_map(obs(ltb, nd, nt, d), with_forecast=True)
+    assert res.smw_rel_residual <= 1e-8  # test_bayes_engine.cpp:158
     m_orc = np.empty(nm * nt)
     y = orc.solve_k(L, d)
     m_orc = pg.apply_adjoint(y)
@@ -211,3 +215,15 @@ def test_predict_qoi_with_credible_intervals(ltb):
 def orc_normal_quantile(p):
     from scipy.stats import norm
     return float(norm.ppf(p))
+
+
+def test_integrate_displacement(ltb):
+    """bayes_engine.cpp:411-419 (left Riemann sum over time, either layout)."""
+    rng = np.random.default_rng(11)
+    nm, nt, dt = 37, 19, 0.25
+    v = rng.standard_normal(nm * nt)
+    f = ltb.SpaceTimeField(nm, nt, ltb.Layout.SpaceMajorRows, v)
+    ref = dt * v.reshape(nm, nt).sum(axis=1)
+    assert np.allclose(ltb.InferenceEngine.integrate_displacement(f, dt), ref, rtol=1e-14, atol=1e-14)
+    ft = ltb.reindex(f, ltb.Layout.TimeMajorBlocks)
+    assert np.allclose(ltb.InferenceEngine.integrate_displacement(ft, dt), ref, rtol=1e-14, atol=1e-14)
