@@ -115,6 +115,8 @@ struct ltb_plan {
   double2* fhat = nullptr;
   double2* tw = nullptr;
   FftDesc fft{};
+  BigFft big{};                 // four-step tables when 2 N_t is too long for one CTA
+  double2* big_tw = nullptr;    // [W_n1 | W_n2 | W_N]
   GemvShape shape{};
   size_t bytes = 0;
 };
@@ -183,11 +185,36 @@ ltb_status plan_init(ltb_plan* p, int rows, int cols, int nt, int tag, const ltb
   p->nf = nt + 1;
   p->tag = tag;
   int B = 0;
-  if (fft_smem_bytes(p->npad, &B) > 227 * 1024)
-    return fail(LTB_CAPACITY, "MatvecPlan: N_t=%d exceeds the shared-memory FFT limit", nt);
-  if (!fft_radices(p->npad, p->fft.radix, &p->fft.nstages))
+  const bool big = fft_smem_bytes(p->npad, &B) > 227 * 1024;
+  if (!big && !fft_radices(p->npad, p->fft.radix, &p->fft.nstages))
     return fail(LTB_CAPACITY, "MatvecPlan: too many FFT stages for 2*N_t=%d", p->npad);
   p->fft.n = p->npad;
+  if (big) {
+    // four-step: 2 N_t = n1 n2, both within the shared-memory FFT
+    int max_len = 2;
+    while (fft_smem_bytes(2 * max_len, &B) <= 227 * 1024) max_len *= 2;
+    while (fft_smem_bytes(max_len + 1, &B) <= 227 * 1024) ++max_len;
+    int n1 = 0, n2 = 0;
+    if (!big_fft_split(p->npad, max_len, &n1, &n2) || !fft_radices(n1, p->big.d1.radix, &p->big.d1.nstages) ||
+        !fft_radices(n2, p->big.d2.radix, &p->big.d2.nstages))
+      return fail(LTB_CAPACITY, "MatvecPlan: 2*N_t=%d has no factorisation into two transforms of <= %d", p->npad,
+                  max_len);
+    const auto w1 = twiddles(n1), w2 = twiddles(n2), wn = twiddles(p->npad);
+    LTB_CUDA_TRY(cudaMalloc(&p->big_tw, sizeof(double2) * (w1.size() + w2.size() + wn.size())));
+    LTB_CUDA_TRY(cudaMemcpy(p->big_tw, w1.data(), sizeof(double2) * w1.size(), cudaMemcpyHostToDevice));
+    LTB_CUDA_TRY(cudaMemcpy(p->big_tw + w1.size(), w2.data(), sizeof(double2) * w2.size(), cudaMemcpyHostToDevice));
+    LTB_CUDA_TRY(cudaMemcpy(p->big_tw + w1.size() + w2.size(), wn.data(), sizeof(double2) * wn.size(),
+                            cudaMemcpyHostToDevice));
+    p->big.n = p->npad;
+    p->big.n1 = n1;
+    p->big.n2 = n2;
+    p->big.d1.n = n1;
+    p->big.d1.tw = p->big_tw;
+    p->big.d2.n = n2;
+    p->big.d2.tw = p->big_tw + w1.size();
+    p->big.twN = p->big_tw + w1.size() + w2.size();
+    p->fft.big = &p->big;
+  }
   p->shape = gemv_shape(rows, cols, p->nf, opts ? opts->unit_cols : 0);
   const size_t fhat_bytes = sizeof(double2) * (size_t)p->nf * rows * cols;
   size_t free_b = 0, total_b = 0;
@@ -209,6 +236,7 @@ void plan_free(ltb_plan* p) {
   DeviceGuard g(p->device);
   cudaFree(p->fhat);
   cudaFree(p->tw);
+  cudaFree(p->big_tw);
   delete p;
 }
 

@@ -229,6 +229,7 @@ size_t fft_smem_bytes(int n, int* pairs_per_cta) {
 cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long long nrows,
                              double2* out, long long ld, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
+  if (d.big) return big_rfft_rows(*d.big, src, nt, nrows, out, ld, st);
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
@@ -241,6 +242,7 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
                               long long ld_p, int nparts, int nt, long long nrows,
                               double scale, double* out, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
+  if (d.big) return big_irfft_rows(*d.big, in, ld_f, ld_p, nparts, nt, nrows, scale, out, st);
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
   const long long grid = (nrows + 2 * B - 1) / (2 * B);

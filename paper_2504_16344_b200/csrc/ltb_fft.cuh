@@ -28,11 +28,21 @@ constexpr int kMaxStages = 32;
 __host__ __device__ __forceinline__ int pidx(int x) { return x + (x >> 3); }
 __host__ __device__ __forceinline__ int padded_len(int n) { return n + (n >> 3) + 1; }
 
+struct BigFft;  // four-step plan for lengths beyond one CTA (ltb_fft_big.cu)
+
 struct FftDesc {
   int n;        // complex transform length N = 2 N_t
   int nstages;
   int radix[kMaxStages];
   const double2* tw;  // W[j] = exp(-2 pi i j / N), j in [0, N)
+  const BigFft* big = nullptr;  // host-side: set when N needs the four-step path
+};
+
+// N = n1 n2 four-step transform: both factors run through fft_batched
+struct BigFft {
+  int n = 0, n1 = 0, n2 = 0;
+  FftDesc d1{}, d2{};
+  const double2* twN = nullptr;  // W_N^j, j in [0, N)
 };
 
 // One radix-R Stockham step (Bainville formulation): butterfly i of T = N/R

@@ -37,6 +37,13 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
 
 size_t fft_smem_bytes(int n, int* pairs_per_cta);
 
+// four-step path (ltb_fft_big.cu): N = n1 n2 with both factors <= max_len
+bool big_fft_split(int n, int max_len, int* n1, int* n2);
+cudaError_t big_rfft_rows(const BigFft& b, const RfftSrc& src, int nt, long long nrows, double2* out, long long ld,
+                          cudaStream_t st);
+cudaError_t big_irfft_rows(const BigFft& b, const double2* in, long long ld_f, long long ld_p, int nparts, int nt,
+                           long long nrows, double scale, double* out, cudaStream_t st);
+
 // ---- per-frequency GEMVs (K2 / K3) ----
 struct GemvShape {
   int nd;          // rows of each frequency block
