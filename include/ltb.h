@@ -97,7 +97,7 @@ ltb_status ltb_plan_create_generated(int rows, int cols, int nt, int tag, uint64
  * Laplacian on the n_cols nodes, spacing h_x), along its column axis before
  * the transform -- PriorOp::premultiply_kernel (prior.cpp:108-134; A_x
  * prior.cpp:9-39).  Tag F -> Gstar, Fq -> Gqstar; LTB_CONFIG for an already
- * premultiplied tag or invalid prior parameters.  Built slab by slab (<= 16
+ * premultiplied tag or invalid prior parameters.  Built slab by slab (<= 64
  * kernel rows at a time), so the time-domain kernel is never resident. */
 ltb_status ltb_plan_create_premultiplied(const double* kernel_rck, int rows, int cols, int nt,
                                          int tag, int ptr_kind, double h_x, double gamma,
