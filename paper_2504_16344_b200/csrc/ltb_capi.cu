@@ -320,6 +320,36 @@ ltb_status pipe_setup(ltb_scratch* s) {
   return LTB_OK;
 }
 
+// F* of a device-resident d into dev_out (n_cols x N_t), GEMV-H / c2r in
+// column chunks with each chunk's copy to host_out queued on the copy stream
+// as soon as it is ready.  Asynchronous: the copy stream is joined back into
+// the compute stream at the end (later work on it waits for the copies).
+ltb_status adjoint_chunks_to_host(const ltb_plan* p, ltb_scratch* s, const double* d_dev, double* dev_out,
+                                  double* host_out) {
+  ltb_status st = pipe_setup(s);
+  if (st != LTB_OK) return st;
+  const cudaStream_t cs = s->stream, xs = s->copy_stream;
+  const long long cols = p->cols, nt = p->nt;
+  long long cc = (cols + kPipeChunks - 1) / kPipeChunks;
+  cc = (cc + p->shape.unit_cols - 1) / p->shape.unit_cols * p->shape.unit_cols;
+  const int K = (int)((cols + cc - 1) / cc);
+  RfftSrc src{d_dev, 0, 1, 0, 0};
+  LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, p->rows, s->dhat, p->rows, cs), 1);
+  for (int k = 0; k < K; ++k) {
+    const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+    LTB_LAUNCH(launch_gemv_h(gemv_window(p->shape, c0, nc, 0), p->fhat, s->dhat, s->xhat, cs), 1);
+    LTB_LAUNCH(launch_irfft_rows(p->fft, s->xhat + c0, cols, 0, 1, p->nt, nc, 1.0 / p->npad, dev_out + c0 * nt, cs),
+               1);
+    LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], cs));
+    LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[k], 0));
+    LTB_CUDA_TRY(cudaMemcpyAsync(host_out + c0 * nt, dev_out + c0 * nt, sizeof(double) * nc * nt,
+                                 cudaMemcpyDeviceToHost, xs));
+  }
+  LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[16], xs));
+  LTB_CUDA_TRY(cudaStreamWaitEvent(cs, s->pipe_ev[16], 0));
+  return LTB_OK;
+}
+
 ltb_status apply_host_pipelined(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
                                 bool adjoint) {
   ltb_status st = pipe_setup(s);
@@ -357,19 +387,8 @@ ltb_status apply_host_pipelined(const ltb_plan* p, ltb_scratch* s, const double*
     return LTB_OK;
   }
   LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in, in, sizeof(double) * p->rows * nt, cudaMemcpyHostToDevice, cs));
-  RfftSrc src{s->stage_in, 0, 1, 0, 0};
-  LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, p->rows, s->dhat, p->rows, cs), 1);
-  for (int k = 0; k < K; ++k) {
-    const long long c0 = k * cc, nc = std::min(cc, cols - c0);
-    LTB_LAUNCH(launch_gemv_h(gemv_window(p->shape, c0, nc, 0), p->fhat, s->dhat, s->xhat, cs), 1);
-    LTB_LAUNCH(launch_irfft_rows(p->fft, s->xhat + c0, cols, 0, 1, p->nt, nc, 1.0 / p->npad,
-                                 s->stage_out + c0 * nt, cs),
-               1);
-    LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], cs));
-    LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[k], 0));
-    LTB_CUDA_TRY(cudaMemcpyAsync(out + c0 * nt, s->stage_out + c0 * nt, sizeof(double) * nc * nt,
-                                 cudaMemcpyDeviceToHost, xs));
-  }
+  st = adjoint_chunks_to_host(p, s, s->stage_in, s->stage_out, out);
+  if (st != LTB_OK) return st;
   LTB_CUDA_TRY(cudaStreamSynchronize(cs));
   LTB_CUDA_TRY(cudaStreamSynchronize(xs));
   return LTB_OK;
@@ -667,6 +686,18 @@ ltb_status ltb_apply_adjoint_series(const ltb_plan* p, ltb_scratch* s, const dou
 
 // ---- internal hooks for ltb_engine.cu ----
 namespace ltb_internal {
+ltb_status adjoint_to_host(const ltb_plan* p, ltb_scratch* s, const double* d_dev, double* dev_out,
+                           double* host_out) {
+  if (!p || !s || s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");
+  if (s->timing || (size_t)p->cols * p->nt * sizeof(double) < kPipeMinBytes) {
+    ltb_status st = apply_adjoint_dev(p, s, d_dev, dev_out);
+    if (st != LTB_OK) return st;
+    LTB_CUDA_TRY(cudaMemcpyAsync(host_out, dev_out, sizeof(double) * p->cols * p->nt, cudaMemcpyDeviceToHost,
+                                 s->stream));
+    return LTB_OK;
+  }
+  return adjoint_chunks_to_host(p, s, d_dev, dev_out, host_out);
+}
 ltb_status set_error(ltb_status st, const char* msg) {
   g_err = msg;
   return st;

@@ -33,6 +33,8 @@ void count_launches(uint64_t n);
 ltb_status premultiply_device(double* kernel, int rows, int cols, int nt, double h_x, double gamma,
                               double delta);
 ltb_status check_finite_device(const double* x, long long n, const char* what);
+ltb_status adjoint_to_host(const ltb_plan* p, ltb_scratch* s, const double* d_dev, double* dev_out,
+                           double* host_out);
 }  // namespace ltb_internal
 
 using namespace ltb_internal;
@@ -493,14 +495,17 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
     ENG_CUDA(cudaMemcpyAsync(e->stage_in, d, nd_nt * sizeof(double), cudaMemcpyHostToDevice, strm));
   // y = K^{-1} d  (bayes_engine.cpp:312-313)
   if ((st = solve_dev(e, din, nullptr, strm)) != LTB_OK) return st;
-  // m_map = G* y  (:316-319)
-  if ((st = apply_device(e->g, s, trsv_result(e->factor), mout, true)) != LTB_OK) return st;
+  // m_map = G* y  (:316-319); host m_map: copied out in column chunks while
+  // the rest of G* (and the forecast) run
+  if (ptr_kind == LTB_PTR_HOST && m_map) {
+    if ((st = adjoint_to_host(e->g, s, trsv_result(e->factor), mout, m_map)) != LTB_OK) return st;
+  } else if ((st = apply_device(e->g, s, trsv_result(e->factor), mout, true)) != LTB_OK) {
+    return st;
+  }
   // q = F_q m_map
   if (q && (st = apply_device(e->fq, sq, mout, qout, false)) != LTB_OK) return st;
-  if (ptr_kind == LTB_PTR_HOST) {
-    if (m_map) ENG_CUDA(cudaMemcpyAsync(m_map, mout, nm_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
-    if (q) ENG_CUDA(cudaMemcpyAsync(q, qout, nq_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
-  }
+  if (ptr_kind == LTB_PTR_HOST && q)
+    ENG_CUDA(cudaMemcpyAsync(q, qout, nq_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
   ENG_CUDA(cudaEventRecord(e->ev1, strm));
   if ((st = check_solve_status(e, strm)) != LTB_OK) return st;
   if (seconds) {

@@ -159,6 +159,15 @@ def test_generated_factor_small_inversion_config(ltb):
     q_ref = orc.OraclePlan(orc.gen_kernel(seed, nq, nm, nt, stream=2)).apply(res.m_map.values)
     assert orc.rel_err(res.q_map.values, q_ref) <= 1e-12
     assert res.seconds > 0
+    # the host-pointer call copies m_map out in column chunks during G*: same
+    # bits as the device-pointer call
+    import torch
+    md = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
+    qd = torch.empty(nq * nt, dtype=torch.float64, device="cuda")
+    eng.infer_raw(torch.from_numpy(d).cuda(), md, qd)
+    torch.cuda.synchronize()
+    assert np.array_equal(md.cpu().numpy(), res.m_map.values)
+    assert np.array_equal(qd.cpu().numpy(), res.q_map.values)
 
 
 @pytest.mark.parametrize("n,P", [(64, 1), (200, 2), (1000, 2), (3000, 3), (8192, 4), (777, 4)])
