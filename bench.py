@@ -158,6 +158,15 @@ def cpu_reference_run(nd, nt, seed, nm_sample, threads, reps):
                       % (nd, nt, nm_sample, threads, reps)}
 
 
+def arm_config(workload, nd, nm, nt, world):
+    """The bench line's config; identical on both arms (the reference arm
+    states its bounded column sample in cpu_baseline.sample)."""
+    return {"workload": "%s: Nd=%d, Nt=%d, Nm=%d per GPU (Nm_total=%d), F-hat %.1f GB/GPU"
+                        % (workload, nd, nt, nm, nm * world, 16 * (nt + 1) * nd * nm / 1e9),
+            "step": "one F m + one F* d", "l2": "inputs larger than L2 (F-hat streamed)",
+            "parallelism": "Nm sharded x%d (NCCL all-reduce of F m, broadcast of d)" % world}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -176,8 +185,7 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (counter-based generator)",
-        "config": {"workload": "%s (Nd=%d, Nt=%d); reference timed on a %d-column sample"
-                               % (args.workload, nd, nt, nm_sample)},
+        "config": arm_config(args.workload, nd, nm, nt, world),
         "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": threads,
                          "kind": "reference", "sample": res["sample"]},
         "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -487,11 +495,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (counter-based generator kernel, torch.rand vectors)",
-            "config": {"workload": "%s: Nd=%d, Nt=%d, Nm=%d per GPU (Nm_total=%d), F-hat %.1f GB/GPU"
-                                   % (args.workload, nd, nt, nm, nm * world,
-                                      16 * (nt + 1) * nd * nm / 1e9),
-                       "step": "one F m + one F* d", "l2": "inputs larger than L2 (F-hat streamed)",
-                       "parallelism": "Nm sharded x%d (NCCL all-reduce of F m, broadcast of d)" % world},
+            "config": arm_config(args.workload, nd, nm, nt, world),
             "f_ms": f_ms, "fstar_ms": fs_ms,
             "hbm_frac_step": value / world / peak,
             "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
