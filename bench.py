@@ -158,6 +158,38 @@ def cpu_reference_run(nd, nt, seed, nm_sample, threads, reps):
                       % (nd, nt, nm_sample, threads, reps)}
 
 
+def cpu_reference_online(eng, nd, nm, nt, nq, seed, d_dev):
+    """The reference's online path on one host core, as infer_map runs it
+    (bayes_engine.cpp:311-320 is single threaded): the two triangular solves
+    with the same factor (oracle C restatement of the Eigen TRSVs, 'port') +
+    G* and F_q applies of the reference's own MatvecPlan (oracle/_ref),
+    timed on column samples and scaled to N_m (both are column-separable)."""
+    import ctypes as C
+    import numpy as np
+    from oracle import oracle as orc  # baseline leg only
+    if not orc.ref_available():
+        return None
+    L = eng.chol_lower()
+    d = d_dev.cpu().numpy()
+    t0 = time.perf_counter()
+    orc.solve_k(L, d)
+    t_solve = time.perf_counter() - t0
+    del L
+    R = orc.ref()
+    out = {}
+    for name, rows, sample, adjoint in (("gstar", nd, 1024, True), ("fq", nq, 2048, False)):
+        tb, ta, tj = C.c_double(), C.c_double(), C.c_double()
+        if R.ref_bench(rows, nm, sample, nt, seed, 1, 3, C.byref(tb), C.byref(ta), C.byref(tj)) != 0:
+            return None
+        out[name] = (tj.value if adjoint else ta.value) * nm / sample
+    total = t_solve + out["gstar"] + out["fq"]
+    return {"latency_ms": total * 1e3, "solve_k_ms": t_solve * 1e3, "gstar_ms": out["gstar"] * 1e3,
+            "fq_ms": out["fq"] * 1e3, "cores": 1,
+            "kind": "reference (MatvecPlan, oracle/_ref) + port (TRSV pair, oracle)",
+            "sample": "TRSV pair in full (n=%d); G* on 1024 and F_q on 2048 of the %d columns, "
+                      "scaled by N_m / sample" % (nd * nt, nm)}
+
+
 def arm_config(workload, nd, nm, nt, world):
     """The bench line's config; identical on both arms (the reference arm
     states its bounded column sample in cpu_baseline.sample)."""
@@ -199,7 +231,7 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def bench_online(ltb, torch, reps=20):
+def bench_online(ltb, torch, reps=20, cpu=True):
     """BASELINE config 2: posterior mean + forecast latency (device time)."""
     nd, nm, nt, seed = WORKLOADS["small"]
     nq = 8
@@ -263,6 +295,7 @@ def bench_online(ltb, torch, reps=20):
            "gstar_ms": sum(gst["Fstar"]) / reps, "fq_ms": sum(fqt["F"]) / reps,
            "predict_qoi_ms": pq[len(pq) // 2] * 1e3,
            "paper_online_s": 0.2,
+           "cpu_reference": cpu_reference_online(eng, nd, nm, nt, nq, seed, d) if cpu else None,
            "offline": {"form_k_ms": fk_ms, "form_k_tflops": n * n * nm / (fk_ms * 1e-3) / 1e12,
                        "form_k_flops": n * n * nm,
                        "factorize_ms": fz_ms, "factorize_tflops": n ** 3 / 3 / (fz_ms * 1e-3) / 1e12,
@@ -472,7 +505,7 @@ def run_ours(args):
     online = None
     if not args.no_online:
         if world == 1:
-            online = bench_online(ltb, torch)
+            online = bench_online(ltb, torch, cpu=not args.no_cpu_baseline)
         else:
             online = bench_online_dist(ltb, torch, dist, rank, world)
 
