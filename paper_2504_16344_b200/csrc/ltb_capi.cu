@@ -686,6 +686,52 @@ ltb_status ltb_apply_adjoint_series(const ltb_plan* p, ltb_scratch* s, const dou
 
 // ---- internal hooks for ltb_engine.cu ----
 namespace ltb_internal {
+// m = G* y (device y) and q = F_q m with the G* c2r and the F_q r2c fused
+// (launch_c2r_r2c_rows: m is written once and never read back); with m_host
+// the G* columns run in chunks and each chunk of m is copied out while the
+// next ones compute.  All on sg's stream (sq must share it).
+ltb_status gstar_then_fq(const ltb_plan* g, ltb_scratch* sg, const ltb_plan* fq, ltb_scratch* sq,
+                         const double* y_dev, double* m_dev, double* q_dev, double* m_host) {
+  if (!g || !fq || !sg || !sq || sg->plan != g || sq->plan != fq)
+    return fail(LTB_INVALID, "forecast: plan / scratch mismatch");
+  if (g->cols != fq->cols || g->nt != fq->nt) return fail(LTB_DIMENSION, "engine: F and Fq dims are inconsistent");
+  const cudaStream_t cs = sg->stream;
+  const long long cols = g->cols, nt = g->nt;
+  RfftSrc src{y_dev, 0, 1, 0, 0};
+  LTB_LAUNCH(launch_rfft_rows(g->fft, src, g->nt, g->rows, sg->dhat, g->rows, cs), 1);
+  const bool chunked = m_host && !sg->timing && (size_t)cols * nt * sizeof(double) >= kPipeMinBytes;
+  int K = 1;
+  long long cc = cols;
+  if (chunked) {
+    ltb_status st = pipe_setup(sg);
+    if (st != LTB_OK) return st;
+    cc = (cols + kPipeChunks - 1) / kPipeChunks;
+    cc = (cc + g->shape.unit_cols - 1) / g->shape.unit_cols * g->shape.unit_cols;
+    K = (int)((cols + cc - 1) / cc);
+  }
+  for (int k = 0; k < K; ++k) {
+    const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+    LTB_LAUNCH(launch_gemv_h(gemv_window(g->shape, c0, nc, 0), g->fhat, sg->dhat, sg->xhat, cs), 1);
+    LTB_LAUNCH(launch_c2r_r2c_rows(g->fft, sg->xhat + c0, cols, g->nt, nc, 1.0 / g->npad, m_dev + c0 * nt,
+                                   sq->xhat + c0, cols, cs),
+               1);
+    if (chunked) {
+      LTB_CUDA_TRY(cudaEventRecord(sg->pipe_ev[k], cs));
+      LTB_CUDA_TRY(cudaStreamWaitEvent(sg->copy_stream, sg->pipe_ev[k], 0));
+      LTB_CUDA_TRY(cudaMemcpyAsync(m_host + c0 * nt, m_dev + c0 * nt, sizeof(double) * nc * nt,
+                                   cudaMemcpyDeviceToHost, sg->copy_stream));
+    }
+  }
+  LTB_LAUNCH(launch_gemv_n(fq->shape, fq->fhat, sq->xhat, sq->partials, sq->dhat, sq->tickets, cs), 1);
+  LTB_LAUNCH(launch_irfft_rows(fq->fft, sq->dhat, fq->rows, 0, 1, fq->nt, fq->rows, 1.0 / fq->npad, q_dev, cs), 1);
+  if (chunked) {
+    LTB_CUDA_TRY(cudaEventRecord(sg->pipe_ev[16], sg->copy_stream));
+    LTB_CUDA_TRY(cudaStreamWaitEvent(cs, sg->pipe_ev[16], 0));
+  } else if (m_host) {
+    LTB_CUDA_TRY(cudaMemcpyAsync(m_host, m_dev, sizeof(double) * cols * nt, cudaMemcpyDeviceToHost, cs));
+  }
+  return LTB_OK;
+}
 ltb_status adjoint_to_host(const ltb_plan* p, ltb_scratch* s, const double* d_dev, double* dev_out,
                            double* host_out) {
   if (!p || !s || s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");

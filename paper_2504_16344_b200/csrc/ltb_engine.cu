@@ -35,6 +35,8 @@ ltb_status premultiply_device(double* kernel, int rows, int cols, int nt, double
 ltb_status check_finite_device(const double* x, long long n, const char* what);
 ltb_status adjoint_to_host(const ltb_plan* p, ltb_scratch* s, const double* d_dev, double* dev_out,
                            double* host_out);
+ltb_status gstar_then_fq(const ltb_plan* g, ltb_scratch* sg, const ltb_plan* fq, ltb_scratch* sq,
+                         const double* y_dev, double* m_dev, double* q_dev, double* m_host);
 }  // namespace ltb_internal
 
 using namespace ltb_internal;
@@ -497,13 +499,15 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
   if ((st = solve_dev(e, din, nullptr, strm)) != LTB_OK) return st;
   // m_map = G* y  (:316-319); host m_map: copied out in column chunks while
   // the rest of G* (and the forecast) run
-  if (ptr_kind == LTB_PTR_HOST && m_map) {
-    if ((st = adjoint_to_host(e->g, s, trsv_result(e->factor), mout, m_map)) != LTB_OK) return st;
+  double* m_host = (ptr_kind == LTB_PTR_HOST) ? m_map : nullptr;
+  if (q) {
+    // + q = F_q m_map, the c2r of m and the r2c for F_q in one pass
+    if ((st = gstar_then_fq(e->g, s, e->fq, sq, trsv_result(e->factor), mout, qout, m_host)) != LTB_OK) return st;
+  } else if (m_host) {
+    if ((st = adjoint_to_host(e->g, s, trsv_result(e->factor), mout, m_host)) != LTB_OK) return st;
   } else if ((st = apply_device(e->g, s, trsv_result(e->factor), mout, true)) != LTB_OK) {
     return st;
   }
-  // q = F_q m_map
-  if (q && (st = apply_device(e->fq, sq, mout, qout, false)) != LTB_OK) return st;
   if (ptr_kind == LTB_PTR_HOST && q)
     ENG_CUDA(cudaMemcpyAsync(q, qout, nq_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
   ENG_CUDA(cudaEventRecord(e->ev1, strm));

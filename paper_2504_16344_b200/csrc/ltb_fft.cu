@@ -163,6 +163,79 @@ __global__ void __launch_bounds__(kFftThreads)
   }
 }
 
+// c2r of 2B rows' spectra (the G* output) -> the rows m (written out) ->
+// zero padded -> r2c into the transposed spectra of the next map (F_q):
+// the forecast's round trip in one pass, m never read back from HBM.
+template <class Fft>
+__global__ void __launch_bounds__(kFftThreads)
+    c2r_r2c_rows_kernel(const FftDesc d, const double2* __restrict__ in, long long ld_f, int nt, long long nrows,
+                        double scale, double* __restrict__ mout, double2* __restrict__ xout, long long ld_x,
+                        int B) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int N = d.n;
+  const int NP = padded_len(N);
+  const int nf = nt + 1;
+  const int tile = 2 * B;
+  double2* b0 = smem;
+  double2* b1 = smem + (size_t)B * NP;
+  const long long g0 = (long long)blockIdx.x * tile;
+#pragma unroll 8
+  for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
+    const int k = idx / tile, j = idx - k * tile;
+    const long long g = g0 + j;
+    double2 v = g < nrows ? __ldg(in + (long long)k * ld_f + g) : make_double2(0.0, 0.0);
+    if (k == 0 || k == nt) v.y = 0.0;
+    b1[(size_t)j * nf + k] = v;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
+    const int s = idx / N, k = idx - s * N;
+    double2 a, b;
+    if (k <= nt) {
+      a = b1[(size_t)(2 * s) * nf + k];
+      b = b1[(size_t)(2 * s + 1) * nf + k];
+    } else {
+      a = conjg(b1[(size_t)(2 * s) * nf + (N - k)]);
+      b = conjg(b1[(size_t)(2 * s + 1) * nf + (N - k)]);
+    }
+    b0[(size_t)s * NP + pidx(k)] = make_double2(a.x - b.y, -(a.y + b.x));
+  }
+  __syncthreads();
+  const double2* Y = Fft::run(d, b0, b1, B);
+  double2* Z = (Y == b0) ? b1 : b0;
+  for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
+    const int s = idx / N, n = idx - s * N;
+    double va = 0.0, vb = 0.0;
+    if (n < nt) {
+      const double2 y = Y[(size_t)s * NP + pidx(n)];
+      va = y.x * scale;
+      vb = -y.y * scale;
+      const long long ga = g0 + 2 * s;
+      if (ga < nrows) mout[ga * nt + n] = va;
+      if (ga + 1 < nrows) mout[(ga + 1) * nt + n] = vb;
+    }
+    Z[(size_t)s * NP + pidx(n)] = make_double2(va, vb);
+  }
+  __syncthreads();
+  const double2* Y2 = Fft::run(d, Z, const_cast<double2*>(Y), B);
+  for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
+    const int k = idx / tile, j = idx - k * tile;
+    const long long g = g0 + j;
+    if (g >= nrows) continue;
+    const double2* ys = Y2 + (size_t)(j >> 1) * NP;
+    const double2 zk = ys[pidx(k)];
+    const double2 zn = ys[pidx(k == 0 ? 0 : N - k)];
+    double2 v;
+    if ((j & 1) == 0) {
+      v = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
+    } else {
+      const double dx = zk.x - zn.x, dy = zk.y + zn.y;
+      v = make_double2(0.5 * dy, -0.5 * dx);
+    }
+    xout[(long long)k * ld_x + g] = v;
+  }
+}
+
 size_t smem_for(int n, int B) {
   const size_t np = (size_t)padded_len(n);
   const size_t stage = std::max(np * B, (size_t)2 * B * (n / 2 + 1));
@@ -217,6 +290,10 @@ template <class F>
 struct IrfftKern {
   static auto fn() { return irfft_rows_kernel<F>; }
 };
+template <class F>
+struct RoundTripKern {
+  static auto fn() { return c2r_r2c_rows_kernel<F>; }
+};
 
 }  // namespace
 
@@ -248,6 +325,22 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
   return FftDispatch<IrfftKern>::go(d.n, dim3((unsigned)grid), smem, st, d, in, ld_f, ld_p, nparts, nt, nrows,
                                     scale, out, B);
+}
+
+cudaError_t launch_c2r_r2c_rows(const FftDesc& d, const double2* in, long long ld_f, int nt, long long nrows,
+                                double scale, double* mout, double2* xout, long long ld_x, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  if (d.big) {  // four-step path: the two transforms separately
+    cudaError_t e = big_irfft_rows(*d.big, in, ld_f, 0, 1, nt, nrows, scale, mout, st);
+    if (e != cudaSuccess) return e;
+    RfftSrc src{mout, 0, 1, 0, 0};
+    return big_rfft_rows(*d.big, src, nt, nrows, xout, ld_x, st);
+  }
+  const int B = pairs_for(d.n, nrows);
+  const size_t smem = smem_for(d.n, B);
+  const long long grid = (nrows + 2 * B - 1) / (2 * B);
+  return FftDispatch<RoundTripKern>::go(d.n, dim3((unsigned)grid), smem, st, d, in, ld_f, nt, nrows, scale, mout,
+                                        xout, ld_x, B);
 }
 
 }  // namespace ltb

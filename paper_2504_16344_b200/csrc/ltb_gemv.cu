@@ -479,9 +479,31 @@ int gemv_n_row_tiles(const GemvShape& s) {
   return (s.nd + c.rt * c.rpt - 1) / (c.rt * c.rpt);
 }
 
-cudaError_t launch_gemv_n(const GemvShape& s, const double2* fhat, const double2* x,
+cudaError_t launch_gemv_n(const GemvShape& s_in, const double2* fhat, const double2* x,
                           double2* partials, double2* y, unsigned* tickets,
                           cudaStream_t st) {
+  // Small problems: gemv_shape widened the split to fill the machine, but
+  // every extra unit per frequency is another partial for GEMV-N's
+  // last-unit reduction -- here about one wave of 2 CTAs per SM is faster
+  // (tools/gemv_units.py: F_q of config 2, 63.5 -> 52 us).  Fewer units than
+  // the plan's shape always fit its partials buffer.
+  GemvShape s = s_in;
+  {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    if ((long long)s.nf * s.units_per_f <= kMinUnits + s.nf) {
+      const int upf = std::max(1, 2 * sms / std::max(1, s.nf));
+      if (upf < s.units_per_f) {
+        s.unit_cols = (int)((s.nc + upf - 1) / upf);
+        s.units_per_f = (int)((s.nc + s.unit_cols - 1) / s.unit_cols);
+      }
+    }
+  }
   const NConfig c = n_config(s.nd);
   const int tiles = (s.nd + c.rt * c.rpt - 1) / (c.rt * c.rpt);
   cudaError_t e = cudaMemsetAsync(tickets, 0, sizeof(unsigned) * (size_t)s.nf * tiles, st);

@@ -35,6 +35,12 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
                               long long ld_p, int nparts, int nt, long long nrows,
                               double scale, double* out, cudaStream_t st);
 
+// c2r + truncate + scale of the spectra in[f * ld_f + g] into rows mout (as
+// launch_irfft_rows), then pad + r2c of those rows into xout[f * ld_x + g]
+// (as launch_rfft_rows): one pass for an F* apply feeding an F apply
+cudaError_t launch_c2r_r2c_rows(const FftDesc& d, const double2* in, long long ld_f, int nt, long long nrows,
+                                double scale, double* mout, double2* xout, long long ld_x, cudaStream_t st);
+
 size_t fft_smem_bytes(int n, int* pairs_per_cta);
 
 // four-step path (ltb_fft_big.cu): N = n1 n2 with both factors <= max_len
