@@ -10,7 +10,7 @@
 namespace ltb {
 
 constexpr int kTB = 64;        // factor tile edge
-constexpr int kLook = 3;       // diagonal-chain lookahead depth (tiles per chain step)
+constexpr int kLook = 4;       // diagonal-chain lookahead depth (tiles per chain step)
 constexpr int kMaxRanks = 8;
 
 // Row-cyclic block distribution over P ranks: rank r holds the 64-row block
