@@ -295,6 +295,14 @@ ltb_status ltb_fnv1a64_file(const char* path, uint64_t* out);
  * into the packed tiles; the strict upper part is ignored (chol.dnsm may
  * hold K there, bayes_engine.cpp:180-193).  Single-GPU engines only. */
 ltb_status ltb_engine_load_factor_dnsm(ltb_engine* e, const char* path);
+/* writers, the inverse of the loaders (io.cpp:40-85 write_kernel, :102-115
+ * write_dense), written to a temp name in the target directory and renamed
+ * (atomic_write); m is column-major with leading dimension ld (host or
+ * device), written row-major as DNSM1 does */
+ltb_status ltb_write_btpz(const char* path, const double* kernel_rck, int rows, int cols, int nt, int tag,
+                          int ptr_kind);
+ltb_status ltb_write_dnsm(const char* path, const double* m, int rows, int cols, size_t ld, int symmetric,
+                          int ptr_kind);
 /* set_phase3 from Q.dnsm and Gamma_post_q.dnsm (workflow.cpp:325-330) */
 ltb_status ltb_engine_load_phase3_dnsm(ltb_engine* e, const char* q_path, const char* gpost_path);
 

@@ -65,6 +65,8 @@ SIGNATURES = {
     "ltb_engine_set_residual_model": ([_vp, _vp, C.c_double, C.c_double, C.c_double, C.c_double], C.c_int),
     "ltb_engine_map_residual": ([_vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
     "ltb_integrate_displacement": ([_vp, C.c_int, C.c_int, C.c_double, _vp, C.c_int], C.c_int),
+    "ltb_write_btpz": ([C.c_char_p, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
+    "ltb_write_dnsm": ([C.c_char_p, _vp, C.c_int, C.c_int, C.c_size_t, C.c_int, C.c_int], C.c_int),
     "ltb_engine_export_lower": ([_vp, _vp, C.c_size_t, C.c_int], C.c_int),
     "ltb_engine_infer_map": ([_vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
     "ltb_engine_forecast": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),

@@ -4,7 +4,12 @@
 // plan.  infer_map's timed region (:311-320) = copy d -> TRSV pair -> G*
 // adjoint apply; the forecast is F_q m (acceptance_main.cpp:243-264).
 #include <cstdarg>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1296,4 +1301,85 @@ extern "C" ltb_status ltb_integrate_displacement(const double* m, int n_rows, in
   if (ptr_kind == LTB_PTR_HOST) ENG_CUDA(cudaMemcpy(out, dout.p, (size_t)n_rows * 8, cudaMemcpyDeviceToHost));
   else ENG_CUDA(cudaDeviceSynchronize());
   return LTB_OK;
+}
+
+// ---- artifact writers (io.cpp:40-85,102-115): BTPZ1 kernels, DNSM1 dense ----
+namespace {
+
+// atomic_write (io.cpp:40-60): a unique temp name in the target directory,
+// then rename
+ltb_status atomic_write(const char* path, const std::function<bool(FILE*)>& body) {
+  static std::atomic<uint64_t> counter{0};
+  std::string p(path);
+  const size_t slash = p.find_last_of('/');
+  if (slash != std::string::npos && slash > 0) {
+    std::string dir = p.substr(0, slash);
+    // create_directories
+    for (size_t i = 1; i <= dir.size(); ++i)
+      if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0777);
+  }
+  const std::string tmp = p + ".tmp" + std::to_string(counter.fetch_add(1)) + "." + std::to_string(getpid());
+  FILE* fh = fopen(tmp.c_str(), "wb");
+  if (!fh) return efail(LTB_IO, "cannot open %s for writing", tmp.c_str());
+  const bool ok = body(fh);
+  const bool closed = fclose(fh) == 0;
+  if (!ok || !closed) {
+    remove(tmp.c_str());
+    return efail(LTB_IO, "write failed for %s", tmp.c_str());
+  }
+  if (rename(tmp.c_str(), path) != 0) {
+    remove(tmp.c_str());
+    return efail(LTB_IO, "cannot rename %s to %s", tmp.c_str(), path);
+  }
+  return LTB_OK;
+}
+
+bool put_u64(FILE* fh, uint64_t v) { return fwrite(&v, sizeof(v), 1, fh) == 1; }
+
+}  // namespace
+
+extern "C" ltb_status ltb_write_btpz(const char* path, const double* kernel_rck, int rows, int cols, int nt, int tag,
+                                     int ptr_kind) {
+  if (!path || !kernel_rck) return efail(LTB_INVALID, "write_kernel: null argument");
+  if (rows < 1 || cols < 1 || nt < 1) return efail(LTB_DIMENSION, "write_kernel: kernel dims must be >= 1");
+  if (tag < 0 || tag > 3) return efail(LTB_INVALID, "write_kernel: bad kernel tag %d", tag);
+  const size_t n = (size_t)rows * cols * nt;
+  std::vector<double> host;
+  const double* src = kernel_rck;
+  if (ptr_kind == LTB_PTR_DEVICE) {
+    host.resize(n);
+    ENG_CUDA(cudaMemcpy(host.data(), kernel_rck, n * 8, cudaMemcpyDeviceToHost));
+    src = host.data();
+  }
+  for (size_t i = 0; i < n; ++i)  // check_consistent (core.cpp:73-77)
+    if (!std::isfinite(src[i])) return efail(LTB_NUMERICAL, "write_kernel: non-finite kernel entry");
+  return atomic_write(path, [&](FILE* fh) {
+    return fwrite("BTPZ1", 1, 5, fh) == 5 && put_u64(fh, (uint64_t)rows) && put_u64(fh, (uint64_t)cols) &&
+           put_u64(fh, (uint64_t)nt) && put_u64(fh, (uint64_t)tag) && fwrite(src, sizeof(double), n, fh) == n;
+  });
+}
+
+extern "C" ltb_status ltb_write_dnsm(const char* path, const double* m, int rows, int cols, size_t ld, int symmetric,
+                                     int ptr_kind) {
+  if (!path || !m) return efail(LTB_INVALID, "write_dense: null argument");
+  if (rows < 1 || cols < 1) return efail(LTB_DIMENSION, "write_dense: dims must be >= 1");
+  if (ld < (size_t)rows) return efail(LTB_DIMENSION, "write_dense: ld < rows");
+  std::vector<double> host;
+  const double* src = m;
+  if (ptr_kind == LTB_PTR_DEVICE) {
+    host.resize(ld * (size_t)cols);
+    ENG_CUDA(cudaMemcpy(host.data(), m, host.size() * 8, cudaMemcpyDeviceToHost));
+    src = host.data();
+  }
+  return atomic_write(path, [&](FILE* fh) {
+    if (fwrite("DNSM1", 1, 5, fh) != 5 || !put_u64(fh, (uint64_t)rows) || !put_u64(fh, (uint64_t)cols) ||
+        !put_u64(fh, symmetric ? 1u : 0u))
+      return false;
+    std::vector<double> row(cols);
+    for (int i = 0; i < rows; ++i) {  // row-major on disk; the input is column-major
+      for (int j = 0; j < cols; ++j) row[j] = src[(size_t)j * ld + i];
+      if (fwrite(row.data(), sizeof(double), cols, fh) != (size_t)cols) return false;
+    }
+    return true;
+  });
 }

@@ -75,3 +75,29 @@ def test_no_product_import_of_oracle():
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "ltb_oracle.h" not in txt and "liboracle" not in txt, f
                 assert "_ref/" not in txt and "libltibayes_ref" not in txt, f
+
+
+def test_artifact_writers_match_the_reference_byte_layout(tmp_path):
+    """ltb_write_btpz / ltb_write_dnsm (host pointers: no GPU involved) write
+    exactly io.cpp's bytes (write_kernel :71-85, write_dense :102-115),
+    restated here independently with struct; atomic_write leaves no temp."""
+    import struct
+    import paper_2504_16344_b200 as ltb
+    rng = np.random.default_rng(4)
+    k = rng.standard_normal((3, 5, 7))
+    ltb.write_kernel(tmp_path / "sub" / "f.btpz", ltb.BlockToeplitzKernel(3, 5, 7, tag=ltb.KernelTag.Fq, data=k))
+    want = b"BTPZ1" + struct.pack("<4Q", 3, 5, 7, 1) + np.ascontiguousarray(k, dtype="<f8").tobytes()
+    assert (tmp_path / "sub" / "f.btpz").read_bytes() == want
+    m = rng.standard_normal((6, 4))
+    ltb.write_dense(tmp_path / "m.dnsm", m, symmetric=False)
+    want = b"DNSM1" + struct.pack("<3Q", 6, 4, 0) + np.ascontiguousarray(m, dtype="<f8").tobytes()
+    assert (tmp_path / "m.dnsm").read_bytes() == want
+    ltb.write_dense(tmp_path / "s.dnsm", np.asfortranarray(m @ m.T), symmetric=True)
+    assert (tmp_path / "s.dnsm").read_bytes()[5:29] == struct.pack("<3Q", 6, 6, 1)
+    assert sorted(p.name for p in tmp_path.iterdir()) == ["m.dnsm", "s.dnsm", "sub"]
+    with pytest.raises(ltb.NumericalError):
+        bad = k.copy()
+        bad[0, 0, 0] = np.nan
+        ltb.write_kernel(tmp_path / "bad.btpz", ltb.BlockToeplitzKernel(3, 5, 7, data=bad))
+    with pytest.raises(ltb.IoError):
+        ltb.write_dense("/proc/forbidden/x.dnsm", m)

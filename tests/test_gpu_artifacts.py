@@ -151,3 +151,35 @@ def test_dnsm_factor_and_phase3_loaders(ltb, tmp_path):
         eng.load_factor(tmp_path / "small.dnsm")
     with pytest.raises(ltb.IoError):
         eng.load_factor(tmp_path / "none.dnsm")
+
+
+def test_device_built_artifacts_roundtrip(ltb, tmp_path):
+    """form_K -> factorize -> form_Q on the device, the reference's artifact
+    set written (workflow.cpp:256-264 names), then a fresh engine built from
+    those files (MatvecPlan.load, load_factor, load_phase3) predicts the same
+    posterior mean and QoI intervals."""
+    nd, nq, nm, nt, s2, prior = 4, 2, 48, 16, 0.3, (1.0, 2.0, 1.0)
+    rng = np.random.default_rng(21)
+    f = rng.standard_normal((nd, nm, nt)) * 0.9 ** np.arange(nt)
+    fq = rng.standard_normal((nq, nm, nt)) * 0.9 ** np.arange(nt)
+    kf = ltb.BlockToeplitzKernel(nd, nm, nt, tag=ltb.KernelTag.F, data=f)
+    kq = ltb.BlockToeplitzKernel(nq, nm, nt, tag=ltb.KernelTag.Fq, data=fq)
+    eng = ltb.InferenceEngine(ltb.MatvecPlan.premultiplied(kf, prior), ltb.MatvecPlan(kq))
+    eng.form_K(f, prior=prior, sigma2=s2)
+    K = eng.K()
+    eng.factorize()
+    eng.form_Q(f, fq, prior=prior)
+    ltb.write_engine_artifacts(tmp_path, eng, f_kernel=kf, fq_kernel=kq, K=K)
+    assert sorted(p.name for p in tmp_path.iterdir()) == sorted(
+        ["K.dnsm", "chol.dnsm", "Q.dnsm", "gamma_post_q.dnsm", "prior_qoi_cov.dnsm", "f.btpz", "fq.btpz"])
+    eng2 = ltb.InferenceEngine(ltb.MatvecPlan.load(tmp_path / "f.btpz", prior=prior),
+                               ltb.MatvecPlan.load(tmp_path / "fq.btpz"))
+    eng2.load_factor(tmp_path / "chol.dnsm")
+    eng2.load_phase3(tmp_path / "Q.dnsm", tmp_path / "gamma_post_q.dnsm")
+    d = ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, rng.standard_normal(nd * nt))
+    a, b = eng.infer_map(d, with_forecast=True), eng2.infer_map(d, with_forecast=True)
+    assert np.array_equal(a.m_map.values, b.m_map.values)
+    assert np.array_equal(a.q_map.values, b.q_map.values)
+    pa, pb = eng.predict_qoi(d), eng2.predict_qoi(d)
+    assert np.array_equal(pa.q_map.values, pb.q_map.values)
+    assert np.array_equal(pa.ci_upper.values, pb.ci_upper.values)
