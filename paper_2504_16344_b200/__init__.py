@@ -12,4 +12,5 @@ from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, ConfigErro
                      NumericalError, ObsSeries, QoISeries, SpaceTimeField, StateError,
                      algorithmic_bytes, reindex)
 from .engine import InferenceEngine, MapResult, QoIPrediction, normal_quantile  # noqa: F401
-from .artifacts import write_dense, write_engine_artifacts, write_kernel  # noqa: F401
+from .artifacts import (infer_from_artifacts, read_series, write_dense, write_engine_artifacts,  # noqa: F401
+                        write_kernel, write_series)

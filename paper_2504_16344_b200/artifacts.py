@@ -53,3 +53,102 @@ def write_engine_artifacts(directory, engine, f_kernel=None, fq_kernel=None, K=N
     write_dense(os.path.join(directory, "Q.dnsm"), engine.Q(), False)
     write_dense(os.path.join(directory, "gamma_post_q.dnsm"), engine.gamma_post_q(), True)
     write_dense(os.path.join(directory, "prior_qoi_cov.dnsm"), engine.prior_qoi_cov(), True)
+
+
+# ---------------------------------------------------------------------------
+# series files (io.cpp:138-188): raw little-endian doubles + a ".hdr" sidecar
+# "rows=R nt=T layout=SpaceMajorRows|TimeMajorBlocks"
+# ---------------------------------------------------------------------------
+def write_series(path, series):
+    """write_series (io.cpp:138-150)."""
+    from .matvec import Layout
+    series.check_consistent("write_series")
+    path = str(path)
+    _atomic_bytes(path, np.ascontiguousarray(series.values, dtype="<f8").tobytes())
+    _atomic_bytes(path + ".hdr", ("rows=%d nt=%d layout=%s\n" % (
+        series.n_rows, series.n_time, Layout(series.layout).name)).encode())
+
+
+def read_series(path, cls):
+    """read_series (io.cpp:152-180) into ``cls`` (ObsSeries, SpaceTimeField,
+    QoISeries); IoError on a missing / malformed sidecar or short data."""
+    import re
+    from .matvec import IoError, Layout
+    path = str(path)
+    try:
+        with open(path + ".hdr") as fh:
+            line = fh.readline()
+    except OSError:
+        raise IoError("missing series sidecar %s.hdr" % path)
+    mt = re.match(r"rows=(\d+) nt=(\d+) layout=(\S+)", line)
+    if not mt or int(mt.group(1)) < 1 or int(mt.group(2)) < 1:
+        raise IoError("malformed series sidecar %s.hdr" % path)
+    if mt.group(3) not in ("TimeMajorBlocks", "SpaceMajorRows"):
+        raise IoError("unknown layout in sidecar %s.hdr" % path)
+    rows, nt = int(mt.group(1)), int(mt.group(2))
+    try:
+        data = np.fromfile(path, dtype="<f8")
+    except OSError:
+        raise IoError("cannot open series %s" % path)
+    if data.size < rows * nt:
+        raise IoError("truncated archive while reading series data")
+    return cls(rows, nt, Layout[mt.group(3)], data[:rows * nt].astype(np.float64))
+
+
+def _atomic_bytes(path, payload):
+    d = os.path.dirname(path)
+    if d:
+        os.makedirs(d, exist_ok=True)
+    tmp = "%s.tmp%d.%d" % (path, id(payload) & 0xFFFF, os.getpid())
+    with open(tmp, "wb") as fh:
+        fh.write(payload)
+    os.replace(tmp, path)
+
+
+def infer_from_artifacts(directory, d_obs_path, sigma2, prior, dt_obs, h_x=None, level=0.95, device=None):
+    """cmd_infer (workflow.cpp:300-380) over this library: the artifact set
+    (f.btpz, fq.btpz, gstar.btpz if present -- else F premultiplied by the
+    prior --, chol.dnsm, Q.dnsm, gamma_post_q.dnsm) and d_obs (a series file)
+    -> infer_map + predict_qoi + integrate_displacement on the device; writes
+    m_map.f64 (+ .hdr), map_displacement.csv (std = nan: no Hutchinson
+    probes), qoi_forecast.csv and latency.txt next to the artifacts.  The
+    manifest / configuration checks of the CLI are out of scope: sigma2, the
+    prior (h_x, gamma, delta) and dt_obs are arguments."""
+    import time
+    from .engine import InferenceEngine
+    from .matvec import Layout, MatvecPlan, ObsSeries, reindex
+    t0 = time.perf_counter()
+    f_plan = MatvecPlan.load(os.path.join(directory, "f.btpz"), device=device)
+    gpath = os.path.join(directory, "gstar.btpz")
+    g_plan = (MatvecPlan.load(gpath, device=device) if os.path.exists(gpath)
+              else MatvecPlan.load(os.path.join(directory, "f.btpz"), prior=prior, device=device))
+    fq_plan = MatvecPlan.load(os.path.join(directory, "fq.btpz"), device=device)
+    eng = InferenceEngine(g_plan, fq_plan, device=device)
+    eng.load_factor(os.path.join(directory, "chol.dnsm"))
+    eng.load_phase3(os.path.join(directory, "Q.dnsm"), os.path.join(directory, "gamma_post_q.dnsm"))
+    eng.set_residual_model(f_plan, sigma2, prior)
+    d_obs = read_series(d_obs_path, ObsSeries)
+    if d_obs.layout != Layout.SpaceMajorRows:
+        d_obs = reindex(d_obs, Layout.SpaceMajorRows)
+    load_s = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    res = eng.infer_map(d_obs)
+    qoi = eng.predict_qoi(d_obs, level)
+    disp = InferenceEngine.integrate_displacement(res.m_map, dt_obs)
+    compute_s = time.perf_counter() - t1
+    write_series(os.path.join(directory, "m_map.f64"), res.m_map)
+    hx = prior[0] if h_x is None else h_x
+    lines = ["x,mean,std"] + ["%r,%r,nan" % (float(x * hx), float(disp[x])) for x in range(eng.n_space)]
+    _atomic_bytes(os.path.join(directory, "map_displacement.csv"), ("\n".join(lines) + "\n").encode())
+    q, lo, hi = (v.values.reshape(eng.n_qoi, eng.n_time) for v in (qoi.q_map, qoi.ci_lower, qoi.ci_upper))
+    lines = ["qoi_id,t,mean,ci_lo,ci_hi"] + [
+        "%d,%r,%r,%r,%r" % (s, (j + 1) * dt_obs, float(q[s, j]), float(lo[s, j]), float(hi[s, j]))
+        for s in range(eng.n_qoi) for j in range(eng.n_time)]
+    _atomic_bytes(os.path.join(directory, "qoi_forecast.csv"), ("\n".join(lines) + "\n").encode())
+    _atomic_bytes(os.path.join(directory, "latency.txt"), (
+        "load_seconds %g\ncompute_seconds %g\nsmw_rel_residual %g\nwave_solver_invocations 0\n"
+        % (load_s, compute_s, res.smw_rel_residual)).encode())
+    out = {"load_seconds": load_s, "compute_seconds": compute_s, "device_seconds": res.seconds,
+           "smw_rel_residual": res.smw_rel_residual, "m_map": res.m_map, "qoi": qoi, "displacement": disp}
+    eng.close()
+    return out

@@ -101,3 +101,25 @@ def test_artifact_writers_match_the_reference_byte_layout(tmp_path):
         ltb.write_kernel(tmp_path / "bad.btpz", ltb.BlockToeplitzKernel(3, 5, 7, data=bad))
     with pytest.raises(ltb.IoError):
         ltb.write_dense("/proc/forbidden/x.dnsm", m)
+
+
+def test_series_files_roundtrip(tmp_path):
+    """io.cpp:138-180 series format: raw doubles + the "rows= nt= layout="
+    sidecar; bit-exact round trip, IoError contract."""
+    import paper_2504_16344_b200 as ltb
+    rng = np.random.default_rng(8)
+    s = ltb.ObsSeries(3, 5, ltb.Layout.TimeMajorBlocks, rng.standard_normal(15))
+    ltb.write_series(tmp_path / "d.f64", s)
+    assert (tmp_path / "d.f64.hdr").read_text() == "rows=3 nt=5 layout=TimeMajorBlocks\n"
+    assert (tmp_path / "d.f64").read_bytes() == s.values.astype("<f8").tobytes()
+    r = ltb.read_series(tmp_path / "d.f64", ltb.ObsSeries)
+    assert r.layout == ltb.Layout.TimeMajorBlocks and np.array_equal(r.values, s.values)
+    with pytest.raises(ltb.IoError):
+        ltb.read_series(tmp_path / "missing.f64", ltb.ObsSeries)
+    (tmp_path / "bad.f64.hdr").write_text("rows=3 nt=5 layout=Diagonal\n")
+    with pytest.raises(ltb.IoError):
+        ltb.read_series(tmp_path / "bad.f64", ltb.ObsSeries)
+    (tmp_path / "short.f64.hdr").write_text("rows=30 nt=5 layout=SpaceMajorRows\n")
+    (tmp_path / "short.f64").write_bytes(b"\0" * 64)
+    with pytest.raises(ltb.IoError):
+        ltb.read_series(tmp_path / "short.f64", ltb.ObsSeries)

@@ -183,3 +183,35 @@ def test_device_built_artifacts_roundtrip(ltb, tmp_path):
     pa, pb = eng.predict_qoi(d), eng2.predict_qoi(d)
     assert np.array_equal(pa.q_map.values, pb.q_map.values)
     assert np.array_equal(pa.ci_upper.values, pb.ci_upper.values)
+
+
+def test_infer_from_artifacts_like_cmd_infer(ltb, tmp_path):
+    """workflow.cpp:300-380 (cmd_infer) over the library: artifacts written
+    from a device-built engine + a d_obs series file -> m_map.f64, the
+    displacement / QoI CSVs and latency.txt, equal to the engine's own
+    results."""
+    nd, nq, nm, nt, s2, prior, dt = 3, 2, 40, 12, 0.3, (1.0, 2.0, 1.0), 0.5
+    rng = np.random.default_rng(33)
+    f = rng.standard_normal((nd, nm, nt)) * 0.9 ** np.arange(nt)
+    fq = rng.standard_normal((nq, nm, nt)) * 0.9 ** np.arange(nt)
+    kf = ltb.BlockToeplitzKernel(nd, nm, nt, tag=ltb.KernelTag.F, data=f)
+    kq = ltb.BlockToeplitzKernel(nq, nm, nt, tag=ltb.KernelTag.Fq, data=fq)
+    eng = ltb.InferenceEngine(ltb.MatvecPlan.premultiplied(kf, prior), ltb.MatvecPlan(kq))
+    eng.form_K(f, prior=prior, sigma2=s2)
+    eng.factorize()
+    eng.form_Q(f, fq, prior=prior)
+    ltb.write_engine_artifacts(tmp_path, eng, f_kernel=kf, fq_kernel=kq)
+    d = ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, rng.standard_normal(nd * nt))
+    ltb.write_series(tmp_path / "d_obs.f64", ltb.reindex(d, ltb.Layout.TimeMajorBlocks))
+    out = ltb.infer_from_artifacts(str(tmp_path), tmp_path / "d_obs.f64", s2, prior, dt)
+    ref = eng.infer_map(d)
+    assert np.array_equal(out["m_map"].values, ref.m_map.values)
+    m = ltb.read_series(tmp_path / "m_map.f64", ltb.SpaceTimeField)
+    assert np.array_equal(m.values, ref.m_map.values)
+    assert out["smw_rel_residual"] <= 1e-8
+    disp = np.loadtxt(tmp_path / "map_displacement.csv", delimiter=",", skiprows=1, usecols=(0, 1))
+    assert np.allclose(disp[:, 1], dt * ref.m_map.values.reshape(nm, nt).sum(axis=1), rtol=1e-13, atol=1e-15)
+    qcsv = np.loadtxt(tmp_path / "qoi_forecast.csv", delimiter=",", skiprows=1)
+    assert qcsv.shape == (nq * nt, 5)
+    assert np.allclose(qcsv[:, 2], eng.predict_qoi(d).q_map.values, rtol=1e-15, atol=0)
+    assert "smw_rel_residual" in (tmp_path / "latency.txt").read_text()
