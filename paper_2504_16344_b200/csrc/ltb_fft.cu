@@ -19,6 +19,13 @@ constexpr size_t kFftSmemBudget = 56 * 1024;  // >= 4 CTAs per SM
 constexpr size_t kFftSmemMax = 227 * 1024;
 constexpr long long kFftTargetCtas = 8 * 148;  // shrink tiles for few rows
 
+// second buffer: the ping-pong partner, also the c2r staging of 2B half spectra
+__host__ __device__ inline size_t stage_len(int n, int B) {
+  const size_t np = (size_t)padded_len(n);
+  const size_t st = (size_t)2 * B * (n / 2 + 1);
+  return np * B > st ? np * B : st;
+}
+
 LTB_DEV long long in_row_of(const RfftSrc& s, long long g) {
   return (g % s.P) * s.Q + g / s.P + s.c0;
 }
@@ -28,10 +35,12 @@ __global__ void __launch_bounds__(kFftThreads)
     rfft_rows_kernel(const FftDesc d, const RfftSrc src, int nt, long long nrows, double2* out,
                      long long ld, int B) {
   extern __shared__ __align__(16) double2 smem[];
-  const int N = d.n;
+  const int N = Fft::kN ? Fft::kN : d.n;
   const int NP = padded_len(N);
   double2* b0 = smem;
   double2* b1 = smem + (size_t)B * NP;
+  double2* tws = b1 + stage_len(N, B);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tws[j] = __ldg(d.tw + j);
   const long long g0 = (long long)blockIdx.x * 2 * B;
   const long long rows_here = min((long long)2 * B, nrows - g0);
 
@@ -80,7 +89,7 @@ __global__ void __launch_bounds__(kFftThreads)
     }
   }
   __syncthreads();
-  const double2* Y = Fft::run(d, b0, b1, B);
+  const double2* Y = Fft::run(d, tws, b0, b1, B);
 
   // unpack: A[k] = (Z[k] + conj Z[N-k]) / 2, B[k] = -i (Z[k] - conj Z[N-k]) / 2,
   // written transposed: out[k * ld + g]
@@ -112,12 +121,14 @@ __global__ void __launch_bounds__(kFftThreads)
                       long long ld_p, int nparts, int nt, long long nrows, double scale,
                       double* __restrict__ out, int B) {
   extern __shared__ __align__(16) double2 smem[];
-  const int N = d.n;
+  const int N = Fft::kN ? Fft::kN : d.n;
   const int NP = padded_len(N);
   const int nf = nt + 1;
   const int tile = 2 * B;
   double2* b0 = smem;
   double2* b1 = smem + (size_t)B * NP;  // also the staging area (2B * nf)
+  double2* tws = b1 + stage_len(N, B);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tws[j] = __ldg(d.tw + j);
   const long long g0 = (long long)blockIdx.x * tile;
 
   // gather the half spectra of the 2B rows (summing partial slabs in a fixed
@@ -152,7 +163,7 @@ __global__ void __launch_bounds__(kFftThreads)
   }
   __syncthreads();
   // ifft(Z) = conj(fft(conj Z)): a = Re Y, b = -Im Y
-  const double2* Y = Fft::run(d, b0, b1, B);
+  const double2* Y = Fft::run(d, tws, b0, b1, B);
   for (int idx = threadIdx.x; idx < tile * nt; idx += blockDim.x) {
     const int j = idx / nt, n = idx - j * nt;
     const long long g = g0 + j;
@@ -172,12 +183,14 @@ __global__ void __launch_bounds__(kFftThreads)
                         double scale, double* __restrict__ mout, double2* __restrict__ xout, long long ld_x,
                         int B) {
   extern __shared__ __align__(16) double2 smem[];
-  const int N = d.n;
+  const int N = Fft::kN ? Fft::kN : d.n;
   const int NP = padded_len(N);
   const int nf = nt + 1;
   const int tile = 2 * B;
   double2* b0 = smem;
   double2* b1 = smem + (size_t)B * NP;
+  double2* tws = b1 + stage_len(N, B);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tws[j] = __ldg(d.tw + j);
   const long long g0 = (long long)blockIdx.x * tile;
 #pragma unroll 8
   for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
@@ -201,7 +214,7 @@ __global__ void __launch_bounds__(kFftThreads)
     b0[(size_t)s * NP + pidx(k)] = make_double2(a.x - b.y, -(a.y + b.x));
   }
   __syncthreads();
-  const double2* Y = Fft::run(d, b0, b1, B);
+  const double2* Y = Fft::run(d, tws, b0, b1, B);
   double2* Z = (Y == b0) ? b1 : b0;
   for (int idx = threadIdx.x; idx < B * N; idx += blockDim.x) {
     const int s = idx / N, n = idx - s * N;
@@ -217,7 +230,7 @@ __global__ void __launch_bounds__(kFftThreads)
     Z[(size_t)s * NP + pidx(n)] = make_double2(va, vb);
   }
   __syncthreads();
-  const double2* Y2 = Fft::run(d, Z, const_cast<double2*>(Y), B);
+  const double2* Y2 = Fft::run(d, tws, Z, const_cast<double2*>(Y), B);
   for (int idx = threadIdx.x; idx < nf * tile; idx += blockDim.x) {
     const int k = idx / tile, j = idx - k * tile;
     const long long g = g0 + j;
@@ -237,9 +250,7 @@ __global__ void __launch_bounds__(kFftThreads)
 }
 
 size_t smem_for(int n, int B) {
-  const size_t np = (size_t)padded_len(n);
-  const size_t stage = std::max(np * B, (size_t)2 * B * (n / 2 + 1));
-  return (np * B + stage) * sizeof(double2);
+  return ((size_t)padded_len(n) * B + stage_len(n, B) + n) * sizeof(double2);  // + the twiddles
 }
 
 int pairs_for(int n, long long nrows) {

@@ -155,7 +155,7 @@ LTB_DEV void stockham_butterfly(const double2* __restrict__ src, double2* __rest
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = src[pidx(i + r * T)];
 #pragma unroll
-  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * tstep));
+  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * tstep]);
   dft_small<R>(v);
   const int o = (i / Ns) * Ns * R + j;
 #pragma unroll
@@ -175,8 +175,8 @@ LTB_DEV void stockham_butterfly_generic(const double2* __restrict__ src, double2
     double2 acc = make_double2(0.0, 0.0);
     for (int r = 0; r < R; ++r) {
       double2 x = src[pidx(i + r * T)];
-      if (r) x = cmul(x, __ldg(tw + r * tstep));
-      cmac(acc, x, __ldg(tw + ((r * q) % R) * rstep));
+      if (r) x = cmul(x, tw[r * tstep]);
+      cmac(acc, x, tw[((r * q) % R) * rstep]);
     }
     dst[pidx(o + q * Ns)] = acc;
   }
@@ -186,7 +186,9 @@ LTB_DEV void stockham_butterfly_generic(const double2* __restrict__ src, double2
 // padded_len(N), element n at pidx(n)) in `a`; `b` is the ping-pong buffer.
 // Returns the buffer holding the result.  Must be called by all threads of
 // the CTA.
-LTB_DEV double2* fft_batched(const FftDesc& d, double2* a, double2* b, int nseq) {
+LTB_DEV double2* fft_batched(const FftDesc& d, double2* a, double2* b, int nseq,
+                             const double2* tw = nullptr) {
+  if (!tw) tw = d.tw;
   const int N = d.n;
   const int NP = padded_len(N);
   int Ns = 1;
@@ -199,13 +201,13 @@ LTB_DEV double2* fft_batched(const FftDesc& d, double2* a, double2* b, int nseq)
       const double2* src = a + (size_t)q * NP;
       double2* dst = b + (size_t)q * NP;
       switch (R) {
-        case 8: stockham_butterfly<8>(src, dst, d.tw, N, Ns, i); break;
-        case 4: stockham_butterfly<4>(src, dst, d.tw, N, Ns, i); break;
-        case 2: stockham_butterfly<2>(src, dst, d.tw, N, Ns, i); break;
-        case 3: stockham_butterfly<3>(src, dst, d.tw, N, Ns, i); break;
-        case 5: stockham_butterfly<5>(src, dst, d.tw, N, Ns, i); break;
-        case 7: stockham_butterfly<7>(src, dst, d.tw, N, Ns, i); break;
-        default: stockham_butterfly_generic(src, dst, d.tw, N, Ns, R, i); break;
+        case 8: stockham_butterfly<8>(src, dst, tw, N, Ns, i); break;
+        case 4: stockham_butterfly<4>(src, dst, tw, N, Ns, i); break;
+        case 2: stockham_butterfly<2>(src, dst, tw, N, Ns, i); break;
+        case 3: stockham_butterfly<3>(src, dst, tw, N, Ns, i); break;
+        case 5: stockham_butterfly<5>(src, dst, tw, N, Ns, i); break;
+        case 7: stockham_butterfly<7>(src, dst, tw, N, Ns, i); break;
+        default: stockham_butterfly_generic(src, dst, tw, N, Ns, R, i); break;
       }
     }
     __syncthreads();
@@ -232,7 +234,7 @@ LTB_DEV void stockham_butterfly_ct(const double2* __restrict__ src, double2* __r
   for (int r = 0; r < R; ++r) v[r] = src[pidx(i + r * T)];
   if (Ns > 1) {
 #pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * tstep));
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * tstep]);
   }
   dft_small<R>(v);
   const int o = (i / Ns) * Ns * R + j;
@@ -258,15 +260,20 @@ LTB_DEV double2* fft_stages_ct(const double2* tw, double2* a, double2* b, int ns
 }
 
 // transform policies for the row kernels
+// (tw: the twiddle table staged in shared memory by the row kernels -- with
+// the shared-memory carve-out of 4 CTAs per SM there is little L1 left, and
+// __ldg twiddles stalled the butterflies on L2 round trips)
 struct FftRuntime {
-  static LTB_DEV double2* run(const FftDesc& d, double2* a, double2* b, int nseq) {
-    return fft_batched(d, a, b, nseq);
+  static constexpr int kN = 0;
+  static LTB_DEV double2* run(const FftDesc& d, const double2* tw, double2* a, double2* b, int nseq) {
+    return fft_batched(d, a, b, nseq, tw);
   }
 };
 template <int N, int... Rs>
 struct FftFixed {
-  static LTB_DEV double2* run(const FftDesc& d, double2* a, double2* b, int nseq) {
-    return fft_stages_ct<N, 1, Rs...>(d.tw, a, b, nseq);
+  static constexpr int kN = N;
+  static LTB_DEV double2* run(const FftDesc& d, const double2* tw, double2* a, double2* b, int nseq) {
+    return fft_stages_ct<N, 1, Rs...>(tw, a, b, nseq);
   }
 };
 
