@@ -318,6 +318,7 @@ cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long 
                              double2* out, long long ld, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
   if (d.big) return big_rfft_rows(*d.big, src, nt, nrows, out, ld, st);
+  if (reg_fft_supported(d.n)) return reg_rfft_rows(d, src, nt, nrows, out, ld, st);
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
@@ -331,6 +332,7 @@ cudaError_t launch_irfft_rows(const FftDesc& d, const double2* in, long long ld_
                               double scale, double* out, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
   if (d.big) return big_irfft_rows(*d.big, in, ld_f, ld_p, nparts, nt, nrows, scale, out, st);
+  if (reg_fft_supported(d.n)) return reg_irfft_rows(d, in, ld_f, ld_p, nparts, nt, nrows, scale, out, st);
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
   const long long grid = (nrows + 2 * B - 1) / (2 * B);
@@ -347,6 +349,7 @@ cudaError_t launch_c2r_r2c_rows(const FftDesc& d, const double2* in, long long l
     RfftSrc src{mout, 0, 1, 0, 0};
     return big_rfft_rows(*d.big, src, nt, nrows, xout, ld_x, st);
   }
+  if (reg_fft_supported(d.n)) return reg_c2r_r2c_rows(d, in, ld_f, nt, nrows, scale, mout, xout, ld_x, st);
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
   const long long grid = (nrows + 2 * B - 1) / (2 * B);

@@ -43,6 +43,16 @@ cudaError_t launch_c2r_r2c_rows(const FftDesc& d, const double2* in, long long l
 
 size_t fft_smem_bytes(int n, int* pairs_per_cta);
 
+// register-resident two-pass path (ltb_fft_reg.cu) for N in {128, 256, 512,
+// 840, 1024}; same contracts as the three launchers above
+bool reg_fft_supported(int n);
+cudaError_t reg_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long long nrows, double2* out, long long ld,
+                          cudaStream_t st);
+cudaError_t reg_irfft_rows(const FftDesc& d, const double2* in, long long ld_f, long long ld_p, int nparts, int nt,
+                           long long nrows, double scale, double* out, cudaStream_t st);
+cudaError_t reg_c2r_r2c_rows(const FftDesc& d, const double2* in, long long ld_f, int nt, long long nrows,
+                             double scale, double* mout, double2* xout, long long ld_x, cudaStream_t st);
+
 // four-step path (ltb_fft_big.cu): N = n1 n2 with both factors <= max_len
 bool big_fft_split(int n, int max_len, int* n1, int* n2);
 cudaError_t big_rfft_rows(const BigFft& b, const RfftSrc& src, int nt, long long nrows, double2* out, long long ld,

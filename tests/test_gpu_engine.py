@@ -236,3 +236,25 @@ def test_integrate_displacement(ltb):
     assert np.allclose(ltb.InferenceEngine.integrate_displacement(f, dt), ref, rtol=1e-14, atol=1e-14)
     ft = ltb.reindex(f, ltb.Layout.TimeMajorBlocks)
     assert np.allclose(ltb.InferenceEngine.integrate_displacement(ft, dt), ref, rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("nt", [128, 420])
+def test_forecast_round_trip_register_schedule(ltb, nt):
+    """infer_map with forecast at a register-schedule length and an odd N_m:
+    the fused c2r (m) -> r2c (F_q input) pass against the oracle's separate
+    G* and F_q applies."""
+    rng = np.random.default_rng(nt)
+    nd, nm, nq = 2, 2501, 3
+    kg = rng.standard_normal((nd, nm, nt))
+    kq = rng.standard_normal((nq, nm, nt))
+    n = nd * nt
+    lo = np.tril(rng.standard_normal((n, n))) * 0.01 + np.eye(n) * 2.0
+    eng = ltb.InferenceEngine(plan_of(ltb, kg, 2), plan_of(ltb, kq, 1))
+    eng.set_factor(lo)
+    d = rng.standard_normal(n)
+    res = eng.infer_map(obs(ltb, nd, nt, d), with_forecast=True)
+    y = np.linalg.solve(lo.T, np.linalg.solve(lo, d))
+    m_ref = orc.OraclePlan(kg).apply_adjoint(y)
+    assert orc.rel_err(res.m_map.values, m_ref) <= 1e-12
+    q_ref = orc.OraclePlan(kq).apply(res.m_map.values)
+    assert orc.rel_err(res.q_map.values, q_ref) <= 1e-12

@@ -177,6 +177,21 @@ def test_time_lengths_vs_oracle(ltb, nt):
     assert orc.rel_err(fwd(ltb, plan, m), dense_f) <= TOL
 
 
+@pytest.mark.parametrize("nt", [64, 128, 256, 420, 512])
+def test_register_schedules_persistent(ltb, nt):
+    """The register-resident two-pass transforms (2 N_t in {128, 256, 512,
+    840, 1024}) with odd row counts (a half pair at the end) on both sides and
+    more row pairs than resident warps (the persistent loop wraps)."""
+    rng = np.random.default_rng(7 * nt)
+    nd, nm = 3, 2501
+    k = rng.standard_normal((nd, nm, nt))
+    m, d = rng.standard_normal(nm * nt), rng.standard_normal(nd * nt)
+    op = orc.OraclePlan(k)
+    plan = mk_plan(ltb, k)
+    assert orc.rel_err(fwd(ltb, plan, m), op.apply(m)) <= TOL
+    assert orc.rel_err(adj(ltb, plan, d), op.apply_adjoint(d)) <= TOL
+
+
 @pytest.mark.parametrize("nd,nm,nt", [(1, 1, 4), (1, 300, 9), (31, 7, 12), (33, 64, 20),
                                       (64, 2000, 32), (130, 50, 17), (600, 40, 42),
                                       (700, 3, 5), (5000, 2, 3)])
