@@ -318,7 +318,11 @@ cudaError_t launch_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long 
                              double2* out, long long ld, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
   if (d.big) return big_rfft_rows(*d.big, src, nt, nrows, out, ld, st);
-  if (reg_fft_supported(d.n)) return reg_rfft_rows(d, src, nt, nrows, out, ld, st);
+  if (reg_fft_supported(d.n)) {
+    RfftSrc s2 = src;
+    s2.bulk = (src.in && src.P == 1 && src.c0 == 0 && ((uintptr_t)src.in & 15) == 0) ? 1 : 0;
+    return reg_rfft_rows(d, s2, nt, nrows, out, ld, st);
+  }
   const int B = pairs_for(d.n, nrows);
   const size_t smem = smem_for(d.n, B);
   const long long grid = (nrows + 2 * B - 1) / (2 * B);

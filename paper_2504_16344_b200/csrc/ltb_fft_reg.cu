@@ -103,16 +103,30 @@ struct RegFft {
   static LTB_DEV int addr(int n) { return n + n / R1; }
 };
 
-// 8 warps per CTA, one CTA per SM (the register DFTs want ~255 registers;
-// capping them at 168 for 12 warps spills)
-constexpr int kRegWarps = 8;
-constexpr int kRegThreads = 32 * kRegWarps;
-constexpr int kRegMinCtas = 1;
+// One CTA of W warps per SM (the register DFTs want ~255 registers; capping
+// them at 168 for 12 warps spills).  Per warp group: the pass-1/pass-2
+// exchange buffer (SEQ complex) and a staging buffer (STG complex) the NEXT
+// pair's operands are prefetched into with cp.async while the current pair
+// computes.  Staging: r2c rows 2 N_t doubles (N/2 complex); c2r spectra
+// 2 (N_t + 1) complex.
+constexpr size_t kRegSmemMax = 227 * 1024;
 
-template <class F>
-constexpr size_t reg_smem() {
-  return ((size_t)kRegWarps * F::S * F::SEQ + F::N) * sizeof(double2);
+template <class F, bool kSpectra>
+struct RegCfg {
+  static constexpr int STG = kSpectra ? F::N + 2 : F::N / 2;
+  static constexpr size_t per_warp = (size_t)F::S * (F::SEQ + STG) * sizeof(double2);
+  static constexpr size_t tw_bytes = (size_t)F::N * sizeof(double2);
+  static constexpr int W0 = (int)((kRegSmemMax - tw_bytes) / per_warp);
+  static constexpr int W = W0 > 8 ? 8 : W0;
+  static constexpr size_t smem = W * per_warp + tw_bytes;
+  static_assert(W >= 1, "register FFT tile exceeds shared memory");
+};
+
+LTB_DEV void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
+LTB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+LTB_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // stage the pass-2 twiddles tw2[r R1 + i] = W_N^(r i)
 template <class F>
@@ -158,166 +172,264 @@ LTB_DEV void unpack_store(const double2 (&v2)[F::R2], double2* buf, int li, int 
   const bool has_a = g < nrows, has_b = g + 1 < nrows;
   const long long ca = src.oP ? (g / src.oP) * src.oQ + g % src.oP + src.o0 : g;
   const long long cb = src.oP ? ((g + 1) / src.oP) * src.oQ + (g + 1) % src.oP + src.o0 : g + 1;
+  // both columns adjacent and 32-byte aligned: one 256-bit store per frequency
+  const bool wide = has_b && cb == ca + 1 && (((uintptr_t)(out + ca) | (uintptr_t)(ld * 16)) & 31) == 0;
   for (int k = li; k <= nt; k += F::LP) {
     const double2 zk = buf[F::addr(k)];
     const double2 zn = buf[F::addr(k == 0 ? 0 : F::N - k)];
-    if (has_a) out[(long long)k * ld + ca] = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
-    if (has_b) out[(long long)k * ld + cb] = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));
+    const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
+    const double2 B = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));
+    double2* p = out + (long long)k * ld + ca;
+    if (wide) {
+      asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(A.x), "d"(A.y), "d"(B.x), "d"(B.y)
+                   : "memory");
+    } else {
+      if (has_a) *p = A;
+      if (has_b) out[(long long)k * ld + cb] = B;
+    }
   }
   __syncwarp();
 }
 
 LTB_DEV long long in_row(const RfftSrc& s, long long g) { return (g % s.P) * s.Q + g / s.P + s.c0; }
 
+// r2c operands of the pair at row g into v (lane li < R2: x[li + r R2],
+// rows a / b as re / im, zero past N_t): straight from memory or generated
 template <class F>
-__global__ void __launch_bounds__(kRegThreads, kRegMinCtas)
+LTB_DEV void direct_rows(const RfftSrc& src, int nt, long long g, long long nrows, int li, double2 (&v)[F::R1]) {
+  if (li >= F::R2) return;
+  const bool ha = g < nrows, hb = g + 1 < nrows;
+  const long long ra = ha ? in_row(src, g) : 0, rb = hb ? in_row(src, g + 1) : 0;
+#pragma unroll
+  for (int r = 0; r < F::R1; ++r) {
+    const int n = li + r * F::R2;
+    double va = 0.0, vb = 0.0;
+    if (n < nt) {
+      if (src.in) {
+        if (ha) va = __ldg(src.in + ra * nt + n);
+        if (hb) vb = __ldg(src.in + rb * nt + n);
+      } else {
+        if (ha) va = gen_uniform_keyed(src.gen_key, (uint64_t)(ra * nt + n));
+        if (hb) vb = gen_uniform_keyed(src.gen_key, (uint64_t)(rb * nt + n));
+      }
+    }
+    v[r] = make_double2(va, vb);
+  }
+}
+
+// contiguous rows g, g + 1 (16-byte aligned) -> stg as doubles [a | b]
+template <class F>
+LTB_DEV void prefetch_rows(const double* __restrict__ in, int nt, long long g, long long nrows, int li, double2* stg) {
+  if (g >= nrows) return;
+  const int chunks = (g + 1 < nrows ? 2 * nt : nt) / 2;  // N_t even on every register schedule
+  const double* base = in + g * nt;
+  for (int c = li; c < chunks; c += F::LP) cp_async16(stg + c, base + 2 * c);
+}
+
+template <class F>
+LTB_DEV void staged_rows(const double2* stg, int nt, long long g, long long nrows, int li, double2 (&v)[F::R1]) {
+  if (li >= F::R2) return;
+  const double* sd = reinterpret_cast<const double*>(stg);
+  const bool ha = g < nrows, hb = g + 1 < nrows;
+#pragma unroll
+  for (int r = 0; r < F::R1; ++r) {
+    const int n = li + r * F::R2;
+    v[r] = make_double2(n < nt && ha ? sd[n] : 0.0, n < nt && hb ? sd[nt + n] : 0.0);
+  }
+}
+
+// the two half spectra of the pair (rows g, g + 1) -> stg[k] / stg[nf + k]:
+// 32 contiguous bytes per frequency, every element read once
+template <class F>
+LTB_DEV void prefetch_spectra(const double2* __restrict__ in, long long ld_f, int nt, long long g, long long nrows,
+                              int li, double2* stg) {
+  if (g >= nrows) return;
+  const int nf = nt + 1;
+  const bool hb = g + 1 < nrows;
+  for (int k = li; k < nf; k += F::LP) {
+    const double2* p = in + (long long)k * ld_f + g;
+    cp_async16(stg + k, p);
+    if (hb) cp_async16(stg + nf + k, p + 1);
+  }
+}
+
+// synchronous variant summing nparts slabs in a fixed order
+template <class F>
+LTB_DEV void load_spectra(const double2* __restrict__ in, long long ld_f, long long ld_p, int nparts, int nt,
+                          long long g, long long nrows, int li, double2* stg) {
+  if (g >= nrows) return;
+  const int nf = nt + 1;
+  const bool hb = g + 1 < nrows;
+#pragma unroll 4
+  for (int k = li; k < nf; k += F::LP) {
+    const double2* p = in + (long long)k * ld_f + g;
+    double2 a = __ldg(p), b = hb ? __ldg(p + 1) : make_double2(0.0, 0.0);
+    for (int q = 1; q < nparts; ++q) {
+      a = cadd(a, __ldg(p + (long long)q * ld_p));
+      if (hb) b = cadd(b, __ldg(p + (long long)q * ld_p + 1));
+    }
+    stg[k] = a;
+    stg[nf + k] = b;
+  }
+}
+
+// conj of the Hermitian-extended pair spectrum Z = A + i B at the pass-1
+// indices k = li + r R2 (FFTW c2r semantics: Im of DC / Nyquist ignored)
+template <class F>
+LTB_DEV void staged_conj_pair(const double2* stg, int nt, long long g, long long nrows, int li, double2 (&v)[F::R1]) {
+  if (li >= F::R2) return;
+  const int nf = nt + 1;
+  const bool ha = g < nrows, hb = g + 1 < nrows;
+#pragma unroll
+  for (int r = 0; r < F::R1; ++r) {
+    const int k = li + r * F::R2;
+    const bool mirror = k > nt;
+    const int kk = mirror ? F::N - k : k;
+    double2 a = ha ? stg[kk] : make_double2(0.0, 0.0), b = hb ? stg[nf + kk] : make_double2(0.0, 0.0);
+    if (kk == 0 || kk == nt) {
+      a.y = 0.0;
+      b.y = 0.0;
+    }
+    if (mirror) {
+      a.y = -a.y;
+      b.y = -b.y;
+    }
+    v[r] = make_double2(a.x - b.y, -(a.y + b.x));
+  }
+}
+
+// warp-group geometry shared by the kernels
+template <class F, int W>
+struct Lanes {
+  int grp, li;
+  double2* buf;  // SEQ exchange buffer
+  double2* stg;  // staging
+  long long t0, stride, tasks;
+  template <int STG>
+  LTB_DEV void init(double2* smem, long long nrows) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    grp = lane / F::LP;
+    li = lane % F::LP;
+    double2* base = smem + F::N + (size_t)(warp * F::S + grp) * (F::SEQ + STG);
+    buf = base;
+    stg = base + F::SEQ;
+    t0 = (long long)blockIdx.x * W + warp;
+    stride = (long long)gridDim.x * W;
+    tasks = ((nrows + 1) / 2 + F::S - 1) / F::S;
+  }
+  LTB_DEV long long row(long long t) const { return 2 * (t * F::S + grp); }
+};
+
+template <class F, int W>
+__global__ void __launch_bounds__(32 * W, 1)
     rfft_reg_kernel(const double2* __restrict__ tw, const RfftSrc src, int nt, long long nrows, double2* out,
                     long long ld) {
+  using C = RegCfg<F, false>;
   extern __shared__ __align__(16) double2 smem[];
-  double2* tw2 = smem;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / F::LP, li = lane % F::LP;
-  double2* buf = smem + F::N + (size_t)(warp * F::S + grp) * F::SEQ;
-  stage_tw2<F>(tw, tw2);
-  const long long npairs = (nrows + 1) / 2;
-  const long long tasks = (npairs + F::S - 1) / F::S;
-  for (long long t = (long long)blockIdx.x * kRegWarps + warp; t < tasks; t += (long long)gridDim.x * kRegWarps) {
-    const long long g = 2 * (t * F::S + grp);
+  Lanes<F, W> L;
+  L.template init<C::STG>(smem, nrows);
+  stage_tw2<F>(tw, smem);
+  const bool staged = src.bulk && !(src.oP);
+  if (staged && L.t0 < L.tasks) prefetch_rows<F>(src.in, nt, L.row(L.t0), nrows, L.li, L.stg);
+  cp_async_commit();
+  for (long long t = L.t0; t < L.tasks; t += L.stride) {
+    const long long g = L.row(t);
     double2 v[F::R1];
-    if (li < F::R2) {
-      const bool ha = g < nrows, hb = g + 1 < nrows;
-      const long long ra = ha ? in_row(src, g) : 0, rb = hb ? in_row(src, g + 1) : 0;
-#pragma unroll
-      for (int r = 0; r < F::R1; ++r) {
-        const int n = li + r * F::R2;
-        double va = 0.0, vb = 0.0;
-        if (n < nt) {
-          if (src.in) {
-            if (ha) va = __ldg(src.in + ra * nt + n);
-            if (hb) vb = __ldg(src.in + rb * nt + n);
-          } else {
-            if (ha) va = gen_uniform_keyed(src.gen_key, (uint64_t)(ra * nt + n));
-            if (hb) vb = gen_uniform_keyed(src.gen_key, (uint64_t)(rb * nt + n));
-          }
-        }
-        v[r] = make_double2(va, vb);
-      }
+    if (staged) {
+      cp_async_wait_all();
+      __syncwarp();
+      staged_rows<F>(L.stg, nt, g, nrows, L.li, v);
+      __syncwarp();
+      if (t + L.stride < L.tasks) prefetch_rows<F>(src.in, nt, L.row(t + L.stride), nrows, L.li, L.stg);
+      cp_async_commit();
+    } else {
+      direct_rows<F>(src, nt, g, nrows, L.li, v);
     }
     double2 v2[F::R2];
-    two_pass<F>(v, buf, tw2, li, v2);
-    unpack_store<F>(v2, buf, li, nt, g, nrows, src, out, ld);
+    two_pass<F>(v, L.buf, smem, L.li, v2);
+    unpack_store<F>(v2, L.buf, L.li, nt, g, nrows, src, out, ld);
   }
+  cp_async_wait_all();
 }
 
-// the two half spectra of the pair (rows g, g + 1; nparts slabs summed in a
-// fixed order) into buf[k] / buf[nf + k] -- every element read once, 32
-// contiguous bytes per frequency -- then conj of the Hermitian-extended
-// Z = A + i B at the pass-1 indices k = li + r R2 into v (FFTW c2r semantics:
-// Im of DC / Nyquist ignored)
-template <class F>
-LTB_DEV void load_conj_pair(const double2* __restrict__ in, long long ld_f, long long ld_p, int nparts, int nt,
-                            long long g, bool ha, bool hb, double2* buf, int li, double2 (&v)[F::R1]) {
-  const int nf = nt + 1;
-  if (ha) {
-#pragma unroll 4
-    for (int k = li; k < nf; k += F::LP) {
-      const double2* p = in + (long long)k * ld_f + g;
-      double2 a = __ldg(p), b = hb ? __ldg(p + 1) : make_double2(0.0, 0.0);
-      for (int q = 1; q < nparts; ++q) {
-        a = cadd(a, __ldg(p + (long long)q * ld_p));
-        if (hb) b = cadd(b, __ldg(p + (long long)q * ld_p + 1));
-      }
-      if (k == 0 || k == nt) {
-        a.y = 0.0;
-        b.y = 0.0;
-      }
-      buf[k] = a;
-      buf[nf + k] = b;
-    }
-  }
-  __syncwarp();
-  if (li < F::R2) {
-#pragma unroll
-    for (int r = 0; r < F::R1; ++r) {
-      const int k = li + r * F::R2;
-      const bool mirror = k > nt;
-      const int kk = mirror ? F::N - k : k;
-      double2 a = ha ? buf[kk] : make_double2(0.0, 0.0), b = ha ? buf[nf + kk] : make_double2(0.0, 0.0);
-      if (mirror) {
-        a.y = -a.y;
-        b.y = -b.y;
-      }
-      v[r] = make_double2(a.x - b.y, -(a.y + b.x));
-    }
-  }
-  __syncwarp();
-}
-
-template <class F>
-__global__ void __launch_bounds__(kRegThreads, kRegMinCtas)
+template <class F, int W>
+__global__ void __launch_bounds__(32 * W, 1)
     irfft_reg_kernel(const double2* __restrict__ tw, const double2* __restrict__ in, long long ld_f, long long ld_p,
                      int nparts, int nt, long long nrows, double scale, double* __restrict__ out) {
+  using C = RegCfg<F, true>;
   extern __shared__ __align__(16) double2 smem[];
-  double2* tw2 = smem;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / F::LP, li = lane % F::LP;
-  double2* buf = smem + F::N + (size_t)(warp * F::S + grp) * F::SEQ;
-  stage_tw2<F>(tw, tw2);
-  const long long npairs = (nrows + 1) / 2;
-  const long long tasks = (npairs + F::S - 1) / F::S;
-  for (long long t = (long long)blockIdx.x * kRegWarps + warp; t < tasks; t += (long long)gridDim.x * kRegWarps) {
-    const long long g = 2 * (t * F::S + grp);
+  Lanes<F, W> L;
+  L.template init<C::STG>(smem, nrows);
+  stage_tw2<F>(tw, smem);
+  const bool staged = nparts == 1;
+  if (staged && L.t0 < L.tasks) prefetch_spectra<F>(in, ld_f, nt, L.row(L.t0), nrows, L.li, L.stg);
+  cp_async_commit();
+  for (long long t = L.t0; t < L.tasks; t += L.stride) {
+    const long long g = L.row(t);
     const bool ha = g < nrows, hb = g + 1 < nrows;
+    if (staged) {
+      cp_async_wait_all();
+    } else {
+      load_spectra<F>(in, ld_f, ld_p, nparts, nt, g, nrows, L.li, L.stg);
+    }
+    __syncwarp();
     double2 v[F::R1];
-    load_conj_pair<F>(in, ld_f, ld_p, nparts, nt, g, ha, hb, buf, li, v);
+    staged_conj_pair<F>(L.stg, nt, g, nrows, L.li, v);
+    __syncwarp();
+    if (staged && t + L.stride < L.tasks) prefetch_spectra<F>(in, ld_f, nt, L.row(t + L.stride), nrows, L.li, L.stg);
+    cp_async_commit();
     double2 v2[F::R2];
-    two_pass<F>(v, buf, tw2, li, v2);
+    two_pass<F>(v, L.buf, smem, L.li, v2);
     // ifft(Z) = conj(fft(conj Z)): row a = Re Y, row b = -Im Y
-    if (li < F::R1) {
+    if (L.li < F::R1) {
 #pragma unroll
       for (int q = 0; q < F::R2 / 2; ++q) {  // n = li + q R1 < nt = N / 2 exactly for q < R2 / 2
-        const int n = li + q * F::R1;
-        {
-          if (ha) out[g * nt + n] = v2[q].x * scale;
-          if (hb) out[(g + 1) * nt + n] = -v2[q].y * scale;
-        }
+        const int n = L.li + q * F::R1;
+        if (ha) out[g * nt + n] = v2[q].x * scale;
+        if (hb) out[(g + 1) * nt + n] = -v2[q].y * scale;
       }
     }
   }
+  cp_async_wait_all();
 }
 
 // c2r of a pair (rows written to mout) -> zero padded -> r2c into xout
-template <class F>
-__global__ void __launch_bounds__(kRegThreads, kRegMinCtas)
+template <class F, int W>
+__global__ void __launch_bounds__(32 * W, 1)
     c2r_r2c_reg_kernel(const double2* __restrict__ tw, const double2* __restrict__ in, long long ld_f, int nt,
                        long long nrows, double scale, double* __restrict__ mout, double2* __restrict__ xout,
                        long long ld_x) {
+  using C = RegCfg<F, true>;
   extern __shared__ __align__(16) double2 smem[];
-  double2* tw2 = smem;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / F::LP, li = lane % F::LP;
-  double2* buf = smem + F::N + (size_t)(warp * F::S + grp) * F::SEQ;
-  stage_tw2<F>(tw, tw2);
+  Lanes<F, W> L;
+  L.template init<C::STG>(smem, nrows);
+  stage_tw2<F>(tw, smem);
   const RfftSrc ident{nullptr, 0, 1, 0, 0};
-  const long long npairs = (nrows + 1) / 2;
-  const long long tasks = (npairs + F::S - 1) / F::S;
-  for (long long t = (long long)blockIdx.x * kRegWarps + warp; t < tasks; t += (long long)gridDim.x * kRegWarps) {
-    const long long g = 2 * (t * F::S + grp);
+  if (L.t0 < L.tasks) prefetch_spectra<F>(in, ld_f, nt, L.row(L.t0), nrows, L.li, L.stg);
+  cp_async_commit();
+  for (long long t = L.t0; t < L.tasks; t += L.stride) {
+    const long long g = L.row(t);
     const bool ha = g < nrows, hb = g + 1 < nrows;
+    const int li = L.li;
+    cp_async_wait_all();
+    __syncwarp();
     double2 v[F::R1];
-    load_conj_pair<F>(in, ld_f, 0, 1, nt, g, ha, hb, buf, li, v);
+    staged_conj_pair<F>(L.stg, nt, g, nrows, li, v);
+    __syncwarp();
+    if (t + L.stride < L.tasks) prefetch_spectra<F>(in, ld_f, nt, L.row(t + L.stride), nrows, li, L.stg);
+    cp_async_commit();
     double2 v2[F::R2];
-    two_pass<F>(v, buf, tw2, li, v2);
+    two_pass<F>(v, L.buf, smem, li, v2);
     if (li < F::R1) {
 #pragma unroll
       for (int q = 0; q < F::R2; ++q) {
         const int n = li + q * F::R1;
         const double a = v2[q].x * scale, b = -v2[q].y * scale;
-        if (n < nt) {
+        if (q < F::R2 / 2) {  // n < nt
           if (ha) mout[g * nt + n] = a;
           if (hb) mout[(g + 1) * nt + n] = b;
         }
-        buf[q * F::ROW + li] = make_double2(n < nt && ha ? a : 0.0, n < nt && hb ? b : 0.0);
+        L.buf[q * F::ROW + li] = make_double2(q < F::R2 / 2 && ha ? a : 0.0, q < F::R2 / 2 && hb ? b : 0.0);
       }
     }
     __syncwarp();
@@ -325,13 +437,14 @@ __global__ void __launch_bounds__(kRegThreads, kRegMinCtas)
 #pragma unroll
       for (int r = 0; r < F::R1; ++r) {
         const int n = li + r * F::R2;
-        v[r] = n < nt ? buf[F::addr(n)] : make_double2(0.0, 0.0);
+        v[r] = n < nt ? L.buf[F::addr(n)] : make_double2(0.0, 0.0);
       }
     }
     __syncwarp();
-    two_pass<F>(v, buf, tw2, li, v2);
-    unpack_store<F>(v2, buf, li, nt, g, nrows, ident, xout, ld_x);
+    two_pass<F>(v, L.buf, smem, li, v2);
+    unpack_store<F>(v2, L.buf, li, nt, g, nrows, ident, xout, ld_x);
   }
+  cp_async_wait_all();
 }
 
 int sm_count() {
@@ -344,20 +457,19 @@ int sm_count() {
   return n;
 }
 
-template <class F>
+template <class F, int W>
 unsigned reg_grid(long long nrows) {
   const long long tasks = ((nrows + 1) / 2 + F::S - 1) / F::S;
-  const long long ctas = (tasks + kRegWarps - 1) / kRegWarps;
-  return (unsigned)std::max(1ll, std::min(ctas, (long long)kRegMinCtas * sm_count()));
+  const long long ctas = (tasks + W - 1) / W;
+  return (unsigned)std::max(1ll, std::min(ctas, (long long)sm_count()));
 }
 
-template <class F, class K, class... Args>
+template <class F, bool kSpectra, class K, class... Args>
 cudaError_t reg_launch(K kern, long long nrows, cudaStream_t st, Args... args) {
-  constexpr size_t smem = reg_smem<F>();
-  static_assert(smem <= 227 * 1024, "register FFT tile exceeds shared memory");
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  using C = RegCfg<F, kSpectra>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
   if (e != cudaSuccess) return e;
-  kern<<<reg_grid<F>(nrows), kRegThreads, smem, st>>>(args...);
+  kern<<<reg_grid<F, C::W>(nrows), 32 * C::W, C::smem, st>>>(args...);
   return cudaGetLastError();
 }
 
@@ -384,7 +496,7 @@ cudaError_t reg_rfft_rows(const FftDesc& d, const RfftSrc& src, int nt, long lon
                           cudaStream_t st) {
   return reg_dispatch(d.n, [&](auto f) {
     using F = decltype(f);
-    return reg_launch<F>(rfft_reg_kernel<F>, nrows, st, d.tw, src, nt, nrows, out, ld);
+    return reg_launch<F, false>(rfft_reg_kernel<F, RegCfg<F, false>::W>, nrows, st, d.tw, src, nt, nrows, out, ld);
   });
 }
 
@@ -392,7 +504,7 @@ cudaError_t reg_irfft_rows(const FftDesc& d, const double2* in, long long ld_f, 
                            long long nrows, double scale, double* out, cudaStream_t st) {
   return reg_dispatch(d.n, [&](auto f) {
     using F = decltype(f);
-    return reg_launch<F>(irfft_reg_kernel<F>, nrows, st, d.tw, in, ld_f, ld_p, nparts, nt, nrows, scale, out);
+    return reg_launch<F, true>(irfft_reg_kernel<F, RegCfg<F, true>::W>, nrows, st, d.tw, in, ld_f, ld_p, nparts, nt, nrows, scale, out);
   });
 }
 
@@ -400,7 +512,7 @@ cudaError_t reg_c2r_r2c_rows(const FftDesc& d, const double2* in, long long ld_f
                              double scale, double* mout, double2* xout, long long ld_x, cudaStream_t st) {
   return reg_dispatch(d.n, [&](auto f) {
     using F = decltype(f);
-    return reg_launch<F>(c2r_r2c_reg_kernel<F>, nrows, st, d.tw, in, ld_f, nt, nrows, scale, mout, xout, ld_x);
+    return reg_launch<F, true>(c2r_r2c_reg_kernel<F, RegCfg<F, true>::W>, nrows, st, d.tw, in, ld_f, nt, nrows, scale, mout, xout, ld_x);
   });
 }
 
