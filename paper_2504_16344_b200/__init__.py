@@ -12,5 +12,6 @@ from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, ConfigErro
                      NumericalError, ObsSeries, QoISeries, SpaceTimeField, StateError,
                      algorithmic_bytes, reindex)
 from .engine import InferenceEngine, MapResult, QoIPrediction, normal_quantile  # noqa: F401
-from .artifacts import (infer_from_artifacts, read_series, write_dense, write_engine_artifacts,  # noqa: F401
-                        write_kernel, write_series)
+from .artifacts import (Manifest, fnv1a64_file, infer_from_artifacts, read_manifest, read_series,  # noqa: F401
+                        verify_manifest, write_dense, write_engine_artifacts, write_kernel, write_manifest,
+                        write_series)

@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 from . import _lib
-from .matvec import BlockToeplitzKernel, _buffer, check
+from .matvec import BlockToeplitzKernel, IoError, _buffer, check
 
 
 def write_kernel(path, kernel):
@@ -37,11 +37,91 @@ def write_dense(path, m, symmetric=False):
                                      int(bool(symmetric)), 0))
 
 
-def write_engine_artifacts(directory, engine, f_kernel=None, fq_kernel=None, K=None):
+# ---------------------------------------------------------------------------
+# manifest (io.cpp:221-299): "artifact <name> <bytes> <fnv1a64 hex>",
+# "phase <name> <seconds>", "meta <key> <value>" lines after a comment header
+# ---------------------------------------------------------------------------
+def fnv1a64_file(path):
+    """FNV-1a 64 of a file's bytes (io.cpp:198-219), through the native library."""
+    h = C.c_uint64()
+    check(_lib.load().ltb_fnv1a64_file(os.fsencode(str(path)), C.byref(h)))
+    return h.value
+
+
+class Manifest:
+    """ltibayes::Manifest (io.hpp): artifact entries (name, bytes, hash),
+    phase timings and free-form meta key/values, in file order."""
+
+    def __init__(self, artifacts=None, phases=None, meta=None):
+        self.artifacts = list(artifacts or [])  # (name, bytes, hash)
+        self.phases = list(phases or [])        # (name, seconds)
+        self.meta = list(meta or [])            # (key, value)
+
+    def add_artifact(self, directory, name):
+        p = os.path.join(directory, name)
+        self.artifacts.append((name, os.path.getsize(p), fnv1a64_file(p)))
+
+    def find(self, name):
+        for e in self.artifacts:
+            if e[0] == name:
+                return e
+        return None
+
+    def meta_value(self, key):
+        for k, v in self.meta:
+            if k == key:
+                return v
+        raise IoError("manifest: missing meta key " + key)
+
+
+def write_manifest(path, m):
+    """write_manifest (io.cpp:245-263), atomically."""
+    lines = ["# ltibayes artifact manifest"]
+    lines += ["artifact %s %d %016x" % (n, b, h) for n, b, h in m.artifacts]
+    lines += ["phase %s %.6f" % (n, sec) for n, sec in m.phases]
+    lines += ["meta %s %s" % (k, v) for k, v in m.meta]
+    _atomic_bytes(str(path), ("\n".join(lines) + "\n").encode())
+
+
+def read_manifest(path):
+    """read_manifest (io.cpp:265-291); unknown line kinds raise IOError."""
+    m = Manifest()
+    with open(path) as fh:
+        for line in fh.read().split("\n"):
+            if not line or line[0] == "#":
+                continue
+            kind, _, rest = line.partition(" ")
+            if kind == "artifact":
+                name, nbytes, hexv = rest.split()[:3]
+                m.artifacts.append((name, int(nbytes), int(hexv, 16)))
+            elif kind == "phase":
+                name, sec = rest.split()[:2]
+                m.phases.append((name, float(sec)))
+            elif kind == "meta":
+                k, _, v = rest.partition(" ")
+                m.meta.append((k, v))
+            else:
+                raise IoError("unknown manifest line: " + line)
+    return m
+
+
+def verify_manifest(directory, m):
+    """verify_manifest (io.cpp:293-303): the first artifact that is missing,
+    has another size or fails its hash, else None."""
+    for name, nbytes, h in m.artifacts:
+        p = os.path.join(directory, name)
+        if not os.path.exists(p) or os.path.getsize(p) != nbytes or fnv1a64_file(p) != h:
+            return name
+    return None
+
+
+def write_engine_artifacts(directory, engine, f_kernel=None, fq_kernel=None, K=None, meta=None, phases=None):
     """The dense part of the reference's artifact set (workflow.cpp:256-264)
     from an engine after form_K / factorize / form_Q: chol.dnsm, Q.dnsm,
     gamma_post_q.dnsm, prior_qoi_cov.dnsm, plus K.dnsm when the caller kept
-    K (``engine.K()`` before factorize) and f.btpz / fq.btpz when given."""
+    K (``engine.K()`` before factorize) and f.btpz / fq.btpz when given;
+    then manifest.txt with the size and FNV-1a hash of every artifact present
+    (+ the caller's meta / phase entries, e.g. ("sigma2", "0.01"))."""
     os.makedirs(directory, exist_ok=True)
     if f_kernel is not None:
         write_kernel(os.path.join(directory, "f.btpz"), f_kernel)
@@ -53,6 +133,15 @@ def write_engine_artifacts(directory, engine, f_kernel=None, fq_kernel=None, K=N
     write_dense(os.path.join(directory, "Q.dnsm"), engine.Q(), False)
     write_dense(os.path.join(directory, "gamma_post_q.dnsm"), engine.gamma_post_q(), True)
     write_dense(os.path.join(directory, "prior_qoi_cov.dnsm"), engine.prior_qoi_cov(), True)
+    # manifest over what was written, in the reference's artifact order
+    # (workflow.cpp:240-244,266-284); meta / phases as the caller supplies
+    man = Manifest(phases=phases, meta=meta)
+    for name in ("f.btpz", "fq.btpz", "gstar.btpz", "gqstar.btpz", "K.dnsm", "chol.dnsm", "Q.dnsm",
+                 "gamma_post_q.dnsm", "prior_qoi_cov.dnsm"):
+        if os.path.exists(os.path.join(directory, name)):
+            man.add_artifact(directory, name)
+    write_manifest(os.path.join(directory, "manifest.txt"), man)
+    return man
 
 
 # ---------------------------------------------------------------------------
@@ -112,12 +201,25 @@ def infer_from_artifacts(directory, d_obs_path, sigma2, prior, dt_obs, h_x=None,
     -> infer_map + predict_qoi + integrate_displacement on the device; writes
     m_map.f64 (+ .hdr), map_displacement.csv (std = nan: no Hutchinson
     probes), qoi_forecast.csv and latency.txt next to the artifacts.  The
-    manifest / configuration checks of the CLI are out of scope: sigma2, the
-    prior (h_x, gamma, delta) and dt_obs are arguments."""
+    artifacts are checked against manifest.txt when it exists (a missing or
+    altered file raises StateError, as workflow.cpp:317-320); the config
+    digest check of the CLI is out of scope: sigma2 (None: the manifest's
+    "sigma2" meta), the prior (h_x, gamma, delta) and dt_obs are arguments."""
     import time
     from .engine import InferenceEngine
     from .matvec import Layout, MatvecPlan, ObsSeries, reindex
+    from .matvec import StateError
     t0 = time.perf_counter()
+    mpath = os.path.join(directory, "manifest.txt")
+    if os.path.exists(mpath):
+        man = read_manifest(mpath)
+        bad = verify_manifest(directory, man)
+        if bad is not None:
+            raise StateError("stale artifacts: %s is missing or fails its manifest hash; rerun offline" % bad)
+        if sigma2 is None:
+            sigma2 = float(man.meta_value("sigma2"))
+    if sigma2 is None:
+        raise StateError("infer_from_artifacts: sigma2 not given and no manifest to read it from")
     f_plan = MatvecPlan.load(os.path.join(directory, "f.btpz"), device=device)
     gpath = os.path.join(directory, "gstar.btpz")
     g_plan = (MatvecPlan.load(gpath, device=device) if os.path.exists(gpath)

@@ -123,3 +123,59 @@ def test_series_files_roundtrip(tmp_path):
     (tmp_path / "short.f64").write_bytes(b"\0" * 64)
     with pytest.raises(ltb.IoError):
         ltb.read_series(tmp_path / "short.f64", ltb.ObsSeries)
+
+
+def _fnv1a64(data, h=0xcbf29ce484222325):
+    # io.cpp:198-206, restated independently
+    for b in data:
+        h = ((h ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def test_fnv1a64_known_answers(tmp_path):
+    """ltb_fnv1a64_file (io.cpp:208-219) on the published FNV-1a 64 test
+    strings and on a file longer than the reference's 64 KB read buffer."""
+    import paper_2504_16344_b200 as ltb
+    for text, want in ((b"", 0xcbf29ce484222325), (b"a", 0xaf63dc4c8601ec8c), (b"foobar", 0x85944171f73967e8)):
+        (tmp_path / "t").write_bytes(text)
+        assert ltb.fnv1a64_file(tmp_path / "t") == want
+    blob = np.random.default_rng(3).integers(0, 256, 70000, dtype=np.uint8).tobytes()
+    (tmp_path / "b").write_bytes(blob)
+    assert ltb.fnv1a64_file(tmp_path / "b") == _fnv1a64(blob)
+    with pytest.raises(ltb.IoError):
+        ltb.fnv1a64_file(tmp_path / "missing")
+
+
+def test_manifest_roundtrip_and_verify(tmp_path):
+    """io.cpp:221-303: write_manifest's line format, read_manifest (meta values
+    with spaces, unknown kinds rejected), verify_manifest reporting the first
+    missing / resized / altered artifact."""
+    import paper_2504_16344_b200 as ltb
+    rng = np.random.default_rng(5)
+    ltb.write_dense(tmp_path / "Q.dnsm", rng.standard_normal((4, 3)))
+    ltb.write_kernel(tmp_path / "f.btpz", ltb.BlockToeplitzKernel(2, 3, 4, data=rng.standard_normal((2, 3, 4))))
+    m = ltb.Manifest(phases=[("phase2_form_K", 1.25)], meta=[("sigma2", "0.01"), ("note", "two words")])
+    for name in ("f.btpz", "Q.dnsm"):
+        m.add_artifact(tmp_path, name)
+    ltb.write_manifest(tmp_path / "manifest.txt", m)
+    lines = (tmp_path / "manifest.txt").read_text().splitlines()
+    fb = (tmp_path / "f.btpz").read_bytes()
+    assert lines[0] == "# ltibayes artifact manifest"
+    assert lines[1] == "artifact f.btpz %d %016x" % (len(fb), _fnv1a64(fb))
+    assert lines[3] == "phase phase2_form_K 1.250000"
+    assert lines[5] == "meta note two words"
+    r = ltb.read_manifest(tmp_path / "manifest.txt")
+    assert r.artifacts == m.artifacts and r.phases == m.phases and r.meta == m.meta
+    assert r.meta_value("sigma2") == "0.01" and r.find("Q.dnsm")[1] == (tmp_path / "Q.dnsm").stat().st_size
+    assert ltb.verify_manifest(tmp_path, r) is None
+    q = bytearray((tmp_path / "Q.dnsm").read_bytes())
+    q[40] ^= 1  # same size, different bytes
+    (tmp_path / "Q.dnsm").write_bytes(bytes(q))
+    assert ltb.verify_manifest(tmp_path, r) == "Q.dnsm"
+    (tmp_path / "f.btpz").unlink()
+    assert ltb.verify_manifest(tmp_path, r) == "f.btpz"
+    (tmp_path / "bad.txt").write_text("# x\nbogus line\n")
+    with pytest.raises(ltb.IoError):
+        ltb.read_manifest(tmp_path / "bad.txt")
+    with pytest.raises(ltb.IoError):
+        r.meta_value("missing")

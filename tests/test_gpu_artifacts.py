@@ -171,7 +171,12 @@ def test_device_built_artifacts_roundtrip(ltb, tmp_path):
     eng.form_Q(f, fq, prior=prior)
     ltb.write_engine_artifacts(tmp_path, eng, f_kernel=kf, fq_kernel=kq, K=K)
     assert sorted(p.name for p in tmp_path.iterdir()) == sorted(
-        ["K.dnsm", "chol.dnsm", "Q.dnsm", "gamma_post_q.dnsm", "prior_qoi_cov.dnsm", "f.btpz", "fq.btpz"])
+        ["K.dnsm", "chol.dnsm", "Q.dnsm", "gamma_post_q.dnsm", "prior_qoi_cov.dnsm", "f.btpz", "fq.btpz",
+         "manifest.txt"])
+    man = ltb.read_manifest(tmp_path / "manifest.txt")
+    assert [e[0] for e in man.artifacts] == ["f.btpz", "fq.btpz", "K.dnsm", "chol.dnsm", "Q.dnsm",
+                                             "gamma_post_q.dnsm", "prior_qoi_cov.dnsm"]
+    assert ltb.verify_manifest(tmp_path, man) is None
     eng2 = ltb.InferenceEngine(ltb.MatvecPlan.load(tmp_path / "f.btpz", prior=prior),
                                ltb.MatvecPlan.load(tmp_path / "fq.btpz"))
     eng2.load_factor(tmp_path / "chol.dnsm")
@@ -200,10 +205,10 @@ def test_infer_from_artifacts_like_cmd_infer(ltb, tmp_path):
     eng.form_K(f, prior=prior, sigma2=s2)
     eng.factorize()
     eng.form_Q(f, fq, prior=prior)
-    ltb.write_engine_artifacts(tmp_path, eng, f_kernel=kf, fq_kernel=kq)
+    ltb.write_engine_artifacts(tmp_path, eng, f_kernel=kf, fq_kernel=kq, meta=[("sigma2", repr(s2))])
     d = ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, rng.standard_normal(nd * nt))
     ltb.write_series(tmp_path / "d_obs.f64", ltb.reindex(d, ltb.Layout.TimeMajorBlocks))
-    out = ltb.infer_from_artifacts(str(tmp_path), tmp_path / "d_obs.f64", s2, prior, dt)
+    out = ltb.infer_from_artifacts(str(tmp_path), tmp_path / "d_obs.f64", None, prior, dt)  # sigma2 from meta
     ref = eng.infer_map(d)
     assert np.array_equal(out["m_map"].values, ref.m_map.values)
     m = ltb.read_series(tmp_path / "m_map.f64", ltb.SpaceTimeField)
@@ -215,3 +220,9 @@ def test_infer_from_artifacts_like_cmd_infer(ltb, tmp_path):
     assert qcsv.shape == (nq * nt, 5)
     assert np.allclose(qcsv[:, 2], eng.predict_qoi(d).q_map.values, rtol=1e-15, atol=0)
     assert "smw_rel_residual" in (tmp_path / "latency.txt").read_text()
+    # an artifact altered after the manifest was written: stale, as cmd_infer
+    q = bytearray((tmp_path / "Q.dnsm").read_bytes())
+    q[-1] ^= 0x10
+    (tmp_path / "Q.dnsm").write_bytes(bytes(q))
+    with pytest.raises(ltb.StateError, match="Q.dnsm"):
+        ltb.infer_from_artifacts(str(tmp_path), tmp_path / "d_obs.f64", s2, prior, dt)
