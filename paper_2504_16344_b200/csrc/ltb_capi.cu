@@ -311,13 +311,48 @@ using DevFn = ltb_status (*)(const ltb_plan*, ltb_scratch*, const double*, doubl
 // chunk order, so the result is deterministic).  Returns LTB_OK after the
 // results are on the host.
 constexpr size_t kPipeMinBytes = 16u << 20;
-constexpr int kPipeChunks = 8;
+constexpr int kPipeGeo = 3, kPipeEven = 8, kPipeMaxChunks = 8;
 
 ltb_status pipe_setup(ltb_scratch* s) {
   if (!s->copy_stream) LTB_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
   for (cudaEvent_t& e : s->pipe_ev)
     if (!e) LTB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return LTB_OK;
+}
+
+// Column chunk boundaries b[0..K] of the host-pointer pipelines, in whole
+// GEMV work units.  A column costs 16 Nf rows bytes of F-hat streaming and
+// 8 N_t bytes of PCIe copy, so the copy runs g ~ rows / 65 times faster
+// than the GEMV consumes / produces columns (HBM ~6.5 TB/s, PCIe ~50 GB/s).
+// g >= 2 (Cascadia: ~9): three chunks growing by ~0.6 g from the end whose
+// copy cannot overlap anything -- first for the H2D of F m, last for the D2H
+// of F* d -- so each copy hides under the neighbouring chunk's GEMV, the
+// short end chunk's copy is the only exposed one, and there are few GEMV
+// windows (each launch has a wave tail).  g < 2 (config 2's G*: the copy is
+// the critical path): kPipeEven even chunks, so the copies start early.
+int pipe_bounds(const ltb_plan* p, bool short_first, long long* b) {
+  // even boundaries too: the transforms pair rows (2j, 2j+1), so chunking
+  // keeps the device path's pairs and its bits
+  const long long cols = p->cols, u = p->shape.unit_cols * (p->shape.unit_cols % 2 ? 2 : 1);
+  const double g = std::min(6.0, 0.6 * p->rows / 65.0);
+  const int n = g >= 2.0 ? kPipeGeo : kPipeEven;
+  const double grow = g >= 2.0 ? g : 1.0;
+  long long sz[kPipeMaxChunks];
+  double w = 1.0, tot = 0.0;
+  for (int k = 0; k < n; ++k, w *= grow) tot += w;
+  long long used = 0;
+  int K = 0;
+  w = 1.0;
+  for (int k = 0; k < n && used < cols; ++k, w *= grow) {
+    long long c = (long long)(cols * (w / tot));
+    c = std::max(u, (c + u - 1) / u * u);
+    if (k == n - 1 || used + c > cols) c = cols - used;
+    sz[K++] = c;
+    used += c;
+  }
+  b[0] = 0;
+  for (int k = 0; k < K; ++k) b[k + 1] = b[k] + sz[short_first ? k : K - 1 - k];
+  return K;
 }
 
 // F* of a device-resident d into dev_out (n_cols x N_t), GEMV-H / c2r in
@@ -330,13 +365,12 @@ ltb_status adjoint_chunks_to_host(const ltb_plan* p, ltb_scratch* s, const doubl
   if (st != LTB_OK) return st;
   const cudaStream_t cs = s->stream, xs = s->copy_stream;
   const long long cols = p->cols, nt = p->nt;
-  long long cc = (cols + kPipeChunks - 1) / kPipeChunks;
-  cc = (cc + p->shape.unit_cols - 1) / p->shape.unit_cols * p->shape.unit_cols;
-  const int K = (int)((cols + cc - 1) / cc);
+  long long b[kPipeMaxChunks + 1];
+  const int K = pipe_bounds(p, false, b);
   RfftSrc src{d_dev, 0, 1, 0, 0};
   LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, p->rows, s->dhat, p->rows, cs), 1);
   for (int k = 0; k < K; ++k) {
-    const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+    const long long c0 = b[k], nc = b[k + 1] - b[k];
     LTB_LAUNCH(launch_gemv_h(gemv_window(p->shape, c0, nc, 0), p->fhat, s->dhat, s->xhat, cs), 1);
     LTB_LAUNCH(launch_irfft_rows(p->fft, s->xhat + c0, cols, 0, 1, p->nt, nc, 1.0 / p->npad, dev_out + c0 * nt, cs),
                1);
@@ -356,21 +390,20 @@ ltb_status apply_host_pipelined(const ltb_plan* p, ltb_scratch* s, const double*
   if (st != LTB_OK) return st;
   const cudaStream_t cs = s->stream, xs = s->copy_stream;
   const long long cols = p->cols, nt = p->nt;
-  long long cc = (cols + kPipeChunks - 1) / kPipeChunks;
-  cc = (cc + p->shape.unit_cols - 1) / p->shape.unit_cols * p->shape.unit_cols;  // whole GEMV units
-  const int K = (int)((cols + cc - 1) / cc);
+  long long b[kPipeMaxChunks + 1];
+  const int K = pipe_bounds(p, !adjoint, b);
   // order the copy stream after everything already queued on the compute stream
   LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[16], cs));
   LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[16], 0));
   if (!adjoint) {
     for (int k = 0; k < K; ++k) {
-      const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+      const long long c0 = b[k], nc = b[k + 1] - b[k];
       LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in + c0 * nt, in + c0 * nt, sizeof(double) * nc * nt,
                                    cudaMemcpyHostToDevice, xs));
       LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], xs));
     }
     for (int k = 0; k < K; ++k) {
-      const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+      const long long c0 = b[k], nc = b[k + 1] - b[k];
       LTB_CUDA_TRY(cudaStreamWaitEvent(cs, s->pipe_ev[k], 0));
       RfftSrc src{s->stage_in + c0 * nt, 0, 1, 0, 0};
       LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, nc, s->xhat + c0, cols, cs), 1);
@@ -701,16 +734,14 @@ ltb_status gstar_then_fq(const ltb_plan* g, ltb_scratch* sg, const ltb_plan* fq,
   LTB_LAUNCH(launch_rfft_rows(g->fft, src, g->nt, g->rows, sg->dhat, g->rows, cs), 1);
   const bool chunked = m_host && !sg->timing && (size_t)cols * nt * sizeof(double) >= kPipeMinBytes;
   int K = 1;
-  long long cc = cols;
+  long long b[kPipeMaxChunks + 1] = {0, cols};
   if (chunked) {
     ltb_status st = pipe_setup(sg);
     if (st != LTB_OK) return st;
-    cc = (cols + kPipeChunks - 1) / kPipeChunks;
-    cc = (cc + g->shape.unit_cols - 1) / g->shape.unit_cols * g->shape.unit_cols;
-    K = (int)((cols + cc - 1) / cc);
+    K = pipe_bounds(g, false, b);
   }
   for (int k = 0; k < K; ++k) {
-    const long long c0 = k * cc, nc = std::min(cc, cols - c0);
+    const long long c0 = b[k], nc = b[k + 1] - b[k];
     LTB_LAUNCH(launch_gemv_h(gemv_window(g->shape, c0, nc, 0), g->fhat, sg->dhat, sg->xhat, cs), 1);
     LTB_LAUNCH(launch_c2r_r2c_rows(g->fft, sg->xhat + c0, cols, g->nt, nc, 1.0 / g->npad, m_dev + c0 * nt,
                                    sq->xhat + c0, cols, cs),
