@@ -226,13 +226,22 @@ __host__ __device__ inline size_t chain_idx(int I, int k, int row, int col) {
   return ((size_t)(I * 2 + (row >> 5)) * kLook + k) * kHalfTile + (size_t)col * kHalf + (row & 31);
 }
 
-LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int u, int I, unsigned h) {
-  if (threadIdx.x == 0) {
+// issued by the first thread of warp 1: warp 0 carries the step's critical
+// hand-off / reduction / push right after the barrier.  Also pulls the tiles
+// of block I + 2 (dir: +-2) into L2, so the bulk copy two steps later
+// streams from L2 rather than HBM (64 KB per step per chain CTA).
+LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int u, int I, unsigned h, int I_pf = -1) {
+  if (threadIdx.x == 32) {
     const int s = u & 1;
     constexpr unsigned kBytes = kLook * kHalfTile * sizeof(double);
     mbar_arrive_expect_tx(cr.full + s, kBytes);
     bulk_g2s(cr.stage + (size_t)s * kLook * kHalfTile, mtiles + ((size_t)I * 2 + h) * kLook * kHalfTile, kBytes,
              cr.full + s, policy_evict_first());
+    if (I_pf >= 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mtiles + ((size_t)I_pf * 2 + h) * kLook *
+                                                                                   kHalfTile),
+                   "r"(kBytes)
+                   : "memory");
   }
 }
 
@@ -304,12 +313,13 @@ LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, c
   }
   mbar_wait_bounded(cr.full + (u & 1), (unsigned)(u >> 1) & 1, a.status);  // this step's tiles
   if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
-  if (u >= 1)  // the peer's half of the previous block (older ones were waited for earlier)
-    mbar_wait_bounded(&sm.ybar[(u - 1) & (kYSlots - 1)], (unsigned)((u - 1) >> kYShift) & 1, a.status);
   const double* ms = cr.stage + (size_t)(u & 1) * kLook * kHalfTile;
   double p = 0.0;
+  // older blocks first: every half of them is already here (a thread only
+  // ever reads the columns of group q, and waited for them when they were
+  // the newest block), so this part is off the step-to-step critical path
 #pragma unroll
-  for (int k = 0; k < kLook; ++k) {
+  for (int k = kLook - 1; k >= 1; --k) {
     if (k < nvalid) {
       const double* v = sm.ring[(u - k - 1) & (kYSlots - 1)] + kCC * q;
       const double* M = ms + (size_t)k * kHalfTile + (size_t)kCC * q * kHalf + i;
@@ -317,10 +327,22 @@ LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, c
       for (int kk = 0; kk < kCC; ++kk) p = fma(M[kk * kHalf], v[kk], p);
     }
   }
+  if (nvalid > 0) {
+    // block u - 1: this CTA's half is local; only the column groups of the
+    // peer's half wait for its st.async
+    if ((q / (kCQ / kChainCtas)) != (int)cx.h)
+      mbar_wait_bounded(&sm.ybar[(u - 1) & (kYSlots - 1)], (unsigned)((u - 1) >> kYShift) & 1, a.status);
+    const double* v = sm.ring[(u - 1) & (kYSlots - 1)] + kCC * q;
+    const double* M = ms + (size_t)kCC * q * kHalf + i;
+#pragma unroll
+    for (int kk = 0; kk < kCC; ++kk) p = fma(M[kk * kHalf], v[kk], p);
+  }
   sm.red[q][i] = p;
   __syncthreads();  // also: every thread is done with stage u & 1
   if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
-  if (u + 2 < nb) chain_issue(cr, kForward ? a.mf : a.mb, u + 2, kForward ? I + 2 : I - 2, cx.h);
+  if (u + 2 < nb)
+    chain_issue(cr, kForward ? a.mf : a.mb, u + 2, kForward ? I + 2 : I - 2, cx.h,
+                u + 4 < nb ? (kForward ? I + 4 : I - 4) : -1);
   if (tid < kHalf) {
     unsigned long long raw[kMaxRanks];
     for (int hh = 1; hh < P; ++hh) raw[hh] = ld_relaxed_u64(cbuf + ((size_t)hh * nb + I) * kTB + row0 + tid);
@@ -330,10 +352,15 @@ LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, c
       c += raw[hh] != kSentinel ? __longlong_as_double((long long)raw[hh])
                                 : poll_value<false>(cbuf + ((size_t)hh * nb + I) * kTB + row0 + tid, a.status);
     if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
-    double s = 0.0;
+    // pairwise tree over the column groups (4 dependent adds, not 16)
+    double t[kCQ];
 #pragma unroll
-    for (int g = 0; g < kCQ; ++g) s += sm.red[g][tid];
-    const double v = c - s;
+    for (int g = 0; g < kCQ; ++g) t[g] = sm.red[g][tid];
+#pragma unroll
+    for (int w = kCQ / 2; w >= 1; w /= 2)
+#pragma unroll
+      for (int g = 0; g < w; ++g) t[g] += t[g + w];
+    const double v = c - t[0];
     const int e = slot * kTB + row0 + tid;
     sm.ring[slot][row0 + tid] = v;
     st_async_f64(cx.peer_ring + (uint32_t)e * 8u, v, cx.peer_bar + (uint32_t)slot * 8u);
@@ -367,8 +394,8 @@ template <bool kForward>
 LTB_DEV void chain_sweep(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx) {
   const int nb = a.nb;
   const double* mt = kForward ? a.mf : a.mb;
-  chain_issue(cr, mt, 0, kForward ? 0 : nb - 1, cx.h);
-  if (nb > 1) chain_issue(cr, mt, 1, kForward ? 1 : nb - 2, cx.h);
+  chain_issue(cr, mt, 0, kForward ? 0 : nb - 1, cx.h, nb > 2 ? (kForward ? 2 : nb - 3) : -1);
+  if (nb > 1) chain_issue(cr, mt, 1, kForward ? 1 : nb - 2, cx.h, nb > 3 ? (kForward ? 3 : nb - 4) : -1);
   auto nvalid = [&](int u) { return u < kLook ? u : kLook; };
   // three hand-off registers in rotating roles (no moves of pending loads)
   unsigned long long cA = kSentinel, cB = kSentinel, cC = kSentinel;
