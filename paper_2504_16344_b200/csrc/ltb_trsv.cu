@@ -163,23 +163,32 @@ LTB_DEV double red_sum(const double (&red)[kQ][kTB], int r) {
   return s;
 }
 
-// The chain is a cluster of two CTAs (CTAs 0 and 1 of rank 0): CTA h owns
-// rows [32 h, 32 h + 32) of every 64-block, so each ingests half of the chain
-// tiles per step; the two halves of each solution block are exchanged through
-// distributed shared memory (st.async completing on the peer's mbarrier).
-constexpr int kChainCtas = 2;
-constexpr int kHalf = kTB / kChainCtas;   // 32 rows per chain CTA
-constexpr int kCQ = kThreads / kHalf;     // 16 column groups
-constexpr int kCC = kTB / kCQ;            // 4 columns per thread
+// The chain is a cluster of kLook = 4 CTAs (CTAs 0-3 of rank 0), CTA k
+// owning the chain term of distance k:
+//   HEAD (CTA 0): x_u = c_u - M_{u,0} x_{u-1} - sum_{k=1..3} P^k_u, with
+//     x_{u-1} its own previous output (local shared memory) -- the
+//     step-to-step critical path has no cross-CTA exchange and one tile;
+//   TAIL k (CTAs 1-3): P^k_u = M_{u,k} x_{u-1-k}, needing x only k steps
+//     after the head produced it; the partial sums arrive (st.async into the
+//     head's shared memory, all three completing one mbarrier) before the
+//     head needs them.
+// The head pushes every x_u to the tails the same way.  Each CTA ingests one
+// 32 KB tile per step.
+constexpr int kChainCtas = kLook;
+constexpr int kHalf = kTB / 2;            // tile storage split in row halves (chain_idx)
 constexpr int kHalfTile = kTB * kHalf;    // 2048 doubles
 constexpr int kYShift = 3;
 constexpr int kYSlots = 1 << kYShift;
-static_assert(kLook + 1 < kYSlots, "y ring too short");
+constexpr int kCStages = 4;               // chain tile copies issued four steps ahead
+static_assert((kChainCtas & (kChainCtas - 1)) == 0, "cluster size must be a power of two");
+static_assert(kLook + 1 < kYSlots, "x ring too short");
 
 struct ChainSmem {
-  double ring[kYSlots][kTB];  // solution blocks: own half written locally, peer half by st.async
-  double red[kCQ][kHalf];
-  uint64_t ybar[kYSlots];     // completes when the peer's half of a slot has arrived
+  double xr[kYSlots][kTB];                  // solution blocks (head: written locally; tails: received)
+  double pr[kChainCtas - 1][kYSlots][kTB];  // head: the tails' partial sums
+  double red[kQ][kTB];
+  uint64_t xbar[kYSlots];                   // tail: slot of x_u arrived
+  uint64_t pbar[kYSlots];                   // head: all tails' P_u arrived
 };
 
 struct WorkerSmem {
@@ -211,37 +220,35 @@ LTB_DEV void grid_barrier(unsigned* gsync) {
 // ---------------- chain ------------------------------------------------------
 // Chain tiles are stored split by half: step I, half h, tile k, column c,
 // row ii (< 32) at ((I * 2 + h) * kLook + k) * kHalfTile + c * kHalf + ii, so
-// the kLook tiles a chain CTA needs per step are one contiguous 32 KB run,
-// brought in by one bulk async copy (TMA 1-D) into a two-stage shared buffer
-// a full step ahead.  (Register prefetches of the same data stalled every
-// step on the scoreboard of the next step's loads; one SM's bulk-copy intake
-// (~36 B/cycle from HBM, tools/probes/tma_latency.cu) is why the tiles are
-// split over two SMs.)
-struct ChainRing {
-  double* stage;   // 2 stages x kLook half tiles (dynamic shared memory)
-  uint64_t* full;  // 2 mbarriers
-};
-
+// tile k of a step is two contiguous 16 KB runs (rows 0-31 and 32-63),
+// brought in by bulk async copies (TMA 1-D) into a kCStages-deep shared ring
+// kCStages steps ahead, and pulled into L2 two steps before that.
 __host__ __device__ inline size_t chain_idx(int I, int k, int row, int col) {
   return ((size_t)(I * 2 + (row >> 5)) * kLook + k) * kHalfTile + (size_t)col * kHalf + (row & 31);
 }
 
-// issued by the first thread of warp 1: warp 0 carries the step's critical
-// hand-off / reduction / push right after the barrier.  Also pulls the tiles
-// of block I + 2 (dir: +-2) into L2, so the bulk copy two steps later
-// streams from L2 rather than HBM (64 KB per step per chain CTA).
-LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int u, int I, unsigned h, int I_pf = -1) {
-  if (threadIdx.x == 32) {
-    const int s = u & 1;
-    constexpr unsigned kBytes = kLook * kHalfTile * sizeof(double);
-    mbar_arrive_expect_tx(cr.full + s, kBytes);
-    bulk_g2s(cr.stage + (size_t)s * kLook * kHalfTile, mtiles + ((size_t)I * 2 + h) * kLook * kHalfTile, kBytes,
-             cr.full + s, policy_evict_first());
-    if (I_pf >= 0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mtiles + ((size_t)I_pf * 2 + h) * kLook *
-                                                                                   kHalfTile),
-                   "r"(kBytes)
-                   : "memory");
+struct ChainRing {
+  double* stage;   // kCStages stages x 1 tile, [half][col][row & 31] (dynamic shared memory)
+  uint64_t* full;  // kCStages mbarriers
+};
+
+// tile k of block I for step u; issued by a thread of warp 2 (warps 0-1
+// carry the head's hand-off / reduction / push right after the barrier)
+LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int u, int I, int k, int I_pf) {
+  if (threadIdx.x == 64) {
+    const int s = u % kCStages;
+    constexpr unsigned kRun = kHalfTile * sizeof(double);  // 16 KB: one row half of the tile
+    mbar_arrive_expect_tx(cr.full + s, 2 * kRun);
+    double* dst = cr.stage + (size_t)s * 2 * kHalfTile;
+    for (int hh = 0; hh < 2; ++hh) {
+      bulk_g2s(dst + (size_t)hh * kHalfTile, mtiles + ((size_t)(I * 2 + hh) * kLook + k) * kHalfTile, kRun,
+               cr.full + s, policy_evict_first());
+      if (I_pf >= 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         mtiles + ((size_t)(I_pf * 2 + hh) * kLook + k) * kHalfTile),
+                     "r"(kRun)
+                     : "memory");
+    }
   }
 }
 
@@ -282,108 +289,137 @@ LTB_DEV void cluster_sync_all() {
 }
 
 struct ChainCtx {
-  unsigned h;          // this CTA's half
-  uint32_t peer_ring;  // &ring[0][0] in the peer CTA (cluster address)
-  uint32_t peer_bar;   // &ybar[0] in the peer CTA
+  unsigned h;                      // 0 = head, k = tail of chain term k
+  uint32_t peer_v[kChainCtas];     // head: &tail_k.xr[0][0]; tail: [0] = &head.pr[h - 1][0][0]
+  uint32_t peer_bar[kChainCtas];   // head: &tail_k.xbar[0]; tail: [0] = &head.pbar[0]
 };
 
-// Step u of a sweep (block I = u forward, nb - 1 - u transposed).  `cur` is
-// this step's hand-off prefetched one step ago; `nxt` receives the next one.
+LTB_DEV unsigned slot_parity(int u) { return (unsigned)(u >> kYShift) & 1; }
+
+// M v for this thread's row i and column group q (8 columns)
+LTB_DEV double chain_fma(const double* st, const double* v, int i, int q) {
+  const double* M = st + (size_t)(i >> 5) * kHalfTile + (size_t)kCPT * q * kHalf + (i & 31);
+  double p = 0.0;
+#pragma unroll
+  for (int cc = 0; cc < kCPT; ++cc) p = fma(M[cc * kHalf], v[kCPT * q + cc], p);
+  return p;
+}
+
+// pairwise tree over the kQ column groups of row r
+LTB_DEV double red_tree(const double (&red)[kQ][kTB], int r) {
+  double t[kQ];
+#pragma unroll
+  for (int g = 0; g < kQ; ++g) t[g] = red[g][r];
+#pragma unroll
+  for (int w = kQ / 2; w >= 1; w /= 2)
+#pragma unroll
+    for (int g = 0; g < w; ++g) t[g] += t[g + w];
+  return t[0];
+}
+
+LTB_DEV void chain_wait_tiles(const ChainRing& cr, int u, int* status) {
+  mbar_wait_bounded(cr.full + u % kCStages, (unsigned)(u / kCStages) & 1, status);
+}
+LTB_DEV void chain_next_tiles(const DistArgs& a, const ChainRing& cr, const double* mt, int u, int k,
+                              bool fwd) {
+  const int nb = a.nb, un = u + kCStages;
+  if (un < nb) chain_issue(cr, mt, un, fwd ? un : nb - 1 - un, k, un + 2 < nb ? (fwd ? un + 2 : nb - 3 - un) : -1);
+}
+
+// Head step u (block I = u forward, nb - 1 - u transposed).  `cur` is this
+// step's hand-off prefetched earlier; `nxt` / `nxt2` the next two.
 // Hand-off: forward = cf[I] (one worker); transposed = sum over the P ranks'
-// cb[h][I].
+// cb[h][I], in rank order.
 template <bool kForward>
-LTB_DEV void chain_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u,
-                        int nvalid, unsigned long long cur, unsigned long long& nxt,
-                        unsigned long long& nxt2) {
-  const int tid = threadIdx.x, i = tid & (kHalf - 1), q = tid / kHalf;
+LTB_DEV void head_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u,
+                       unsigned long long cur, unsigned long long& nxt, unsigned long long& nxt2) {
+  const int tid = threadIdx.x, i = tid & (kTB - 1), q = tid / kTB;
   const int nb = a.nb, P = kForward ? 1 : a.P;
   const int I = kForward ? u : nb - 1 - u;
-  const int row0 = (int)cx.h * kHalf;
   double* recv0 = a.loc[0].recv;  // the chain runs on rank 0 = local rank 0
   const double* cbuf = recv0 + (kForward ? off_cf(nb) : off_cb(nb));
   const int In = kForward ? I + 1 : I - 1, In2 = kForward ? I + 2 : I - 2;
   const int slot = u & (kYSlots - 1);
-  if (tid == 0) mbar_arrive_expect_tx(&sm.ybar[slot], kHalf * sizeof(double));  // the peer's half of step u
-  if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I] = clock64();
+  if (tid == 0)  // the tails' P_u
+    mbar_arrive_expect_tx(&sm.pbar[slot], (kChainCtas - 1) * kTB * sizeof(double));
+  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I] = clock64();
   // rank 0's hand-offs are prefetched two steps ahead and re-read a step
   // ahead while still unpublished, so the wait below is rarely a round trip
-  if (tid < kHalf) {
-    if (In2 >= 0 && In2 < nb) nxt2 = ld_relaxed_u64(cbuf + (size_t)In2 * kTB + row0 + tid);
-    if (In >= 0 && In < nb && nxt == kSentinel) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + row0 + tid);
+  if (tid < kTB) {
+    if (In2 >= 0 && In2 < nb) nxt2 = ld_relaxed_u64(cbuf + (size_t)In2 * kTB + tid);
+    if (In >= 0 && In < nb && nxt == kSentinel) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
   }
-  mbar_wait_bounded(cr.full + (u & 1), (unsigned)(u >> 1) & 1, a.status);  // this step's tiles
-  if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
-  const double* ms = cr.stage + (size_t)(u & 1) * kLook * kHalfTile;
-  double p = 0.0;
-  // older blocks first: every half of them is already here (a thread only
-  // ever reads the columns of group q, and waited for them when they were
-  // the newest block), so this part is off the step-to-step critical path
-#pragma unroll
-  for (int k = kLook - 1; k >= 1; --k) {
-    if (k < nvalid) {
-      const double* v = sm.ring[(u - k - 1) & (kYSlots - 1)] + kCC * q;
-      const double* M = ms + (size_t)k * kHalfTile + (size_t)kCC * q * kHalf + i;
-#pragma unroll
-      for (int kk = 0; kk < kCC; ++kk) p = fma(M[kk * kHalf], v[kk], p);
-    }
-  }
-  if (nvalid > 0) {
-    // block u - 1: this CTA's half is local; only the column groups of the
-    // peer's half wait for its st.async
-    if ((q / (kCQ / kChainCtas)) != (int)cx.h)
-      mbar_wait_bounded(&sm.ybar[(u - 1) & (kYSlots - 1)], (unsigned)((u - 1) >> kYShift) & 1, a.status);
-    const double* v = sm.ring[(u - 1) & (kYSlots - 1)] + kCC * q;
-    const double* M = ms + (size_t)kCC * q * kHalf + i;
-#pragma unroll
-    for (int kk = 0; kk < kCC; ++kk) p = fma(M[kk * kHalf], v[kk], p);
-  }
-  sm.red[q][i] = p;
-  __syncthreads();  // also: every thread is done with stage u & 1
-  if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
-  if (u + 2 < nb)
-    chain_issue(cr, kForward ? a.mf : a.mb, u + 2, kForward ? I + 2 : I - 2, cx.h,
-                u + 4 < nb ? (kForward ? I + 4 : I - 4) : -1);
-  if (tid < kHalf) {
+  chain_wait_tiles(cr, u, a.status);
+  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
+  sm.red[q][i] = u >= 1 ? chain_fma(cr.stage + (size_t)(u % kCStages) * 2 * kHalfTile,
+                                    sm.xr[(u - 1) & (kYSlots - 1)], i, q)
+                        : 0.0;
+  __syncthreads();  // also: every thread is done with this tile stage
+  if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
+  chain_next_tiles(a, cr, kForward ? a.mf : a.mb, u, 0, kForward);
+  if (tid < kTB) {
     unsigned long long raw[kMaxRanks];
-    for (int hh = 1; hh < P; ++hh) raw[hh] = ld_relaxed_u64(cbuf + ((size_t)hh * nb + I) * kTB + row0 + tid);
+    for (int hh = 1; hh < P; ++hh) raw[hh] = ld_relaxed_u64(cbuf + ((size_t)hh * nb + I) * kTB + tid);
     double c = cur != kSentinel ? __longlong_as_double((long long)cur)
-                                : poll_value<false>(cbuf + (size_t)I * kTB + row0 + tid, a.status);
+                                : poll_value<false>(cbuf + (size_t)I * kTB + tid, a.status);
     for (int hh = 1; hh < P; ++hh)  // fixed order h = 0, 1, ..., P-1
       c += raw[hh] != kSentinel ? __longlong_as_double((long long)raw[hh])
-                                : poll_value<false>(cbuf + ((size_t)hh * nb + I) * kTB + row0 + tid, a.status);
-    if (kForward && a.trace && tid == 0 && cx.h == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
-    // pairwise tree over the column groups (4 dependent adds, not 16)
-    double t[kCQ];
+                                : poll_value<false>(cbuf + ((size_t)hh * nb + I) * kTB + tid, a.status);
+    if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
+    const double s = red_tree(sm.red, tid);
+    mbar_wait_bounded(&sm.pbar[slot], slot_parity(u), a.status);  // normally long complete
+    double v = c - s;
 #pragma unroll
-    for (int g = 0; g < kCQ; ++g) t[g] = sm.red[g][tid];
+    for (int k = 0; k < kChainCtas - 1; ++k) v -= sm.pr[k][slot][tid];
+    sm.xr[slot][tid] = v;
 #pragma unroll
-    for (int w = kCQ / 2; w >= 1; w /= 2)
-#pragma unroll
-      for (int g = 0; g < w; ++g) t[g] += t[g + w];
-    const double v = c - t[0];
-    const int e = slot * kTB + row0 + tid;
-    sm.ring[slot][row0 + tid] = v;
-    st_async_f64(cx.peer_ring + (uint32_t)e * 8u, v, cx.peer_bar + (uint32_t)slot * 8u);
-    const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + row0 + tid;
+    for (int k = 1; k < kChainCtas; ++k)
+      st_async_f64(cx.peer_v[k] + (uint32_t)(slot * kTB + tid) * 8u, v, cx.peer_bar[k] + (uint32_t)slot * 8u);
+    const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + tid;
     for (int r = 0; r < a.P; ++r) a.peer[r][o] = v;  // push to every rank
   }
   __syncthreads();
-  if (a.trace && threadIdx.x == 0 && cx.h == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
+  if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
 }
 
-// fresh barriers for a sweep; both chain CTAs must be past their previous
-// sweep (all of its peer data received) before either starts sending
+// Tail k, step u: P^k_u = M_{u,k} x_{u-1-k} -> the head's pr[k - 1] slot
+template <bool kForward>
+LTB_DEV void tail_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u) {
+  const int tid = threadIdx.x, i = tid & (kTB - 1), q = tid / kTB;
+  const int k = (int)cx.h;
+  const int slot = u & (kYSlots - 1);
+  if (tid == 0) mbar_arrive_expect_tx(&sm.xbar[slot], kTB * sizeof(double));  // x_u from the head
+  chain_wait_tiles(cr, u, a.status);
+  const int src = u - 1 - k;
+  if (src >= 0) mbar_wait_bounded(&sm.xbar[src & (kYSlots - 1)], slot_parity(src), a.status);
+  sm.red[q][i] = src >= 0 ? chain_fma(cr.stage + (size_t)(u % kCStages) * 2 * kHalfTile,
+                                      sm.xr[src & (kYSlots - 1)], i, q)
+                          : 0.0;
+  __syncthreads();
+  chain_next_tiles(a, cr, kForward ? a.mf : a.mb, u, k, kForward);
+  if (tid < kTB)
+    st_async_f64(cx.peer_v[0] + (uint32_t)(slot * kTB + tid) * 8u, red_tree(sm.red, tid),
+                 cx.peer_bar[0] + (uint32_t)slot * 8u);
+  __syncthreads();
+}
+
+// fresh barriers for a sweep; every chain CTA must be past its previous
+// sweep (all of its peer data received) before any starts sending
 LTB_DEV void chain_sweep_init(const ChainRing& cr, ChainSmem& sm, bool reinit) {
   if (threadIdx.x == 0) {
     if (reinit) {
-      for (int s = 0; s < 2; ++s)
+      for (int s = 0; s < kCStages; ++s)
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(cr.full + s)) : "memory");
-      for (int s = 0; s < kYSlots; ++s)
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.ybar[s])) : "memory");
+      for (int s = 0; s < kYSlots; ++s) {
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.xbar[s])) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.pbar[s])) : "memory");
+      }
     }
-    mbar_init(cr.full, 1);
-    mbar_init(cr.full + 1, 1);
-    for (int s = 0; s < kYSlots; ++s) mbar_init(&sm.ybar[s], 1);
+    for (int s = 0; s < kCStages; ++s) mbar_init(cr.full + s, 1);
+    for (int s = 0; s < kYSlots; ++s) {
+      mbar_init(&sm.xbar[s], 1);
+      mbar_init(&sm.pbar[s], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -394,21 +430,29 @@ template <bool kForward>
 LTB_DEV void chain_sweep(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx) {
   const int nb = a.nb;
   const double* mt = kForward ? a.mf : a.mb;
-  chain_issue(cr, mt, 0, kForward ? 0 : nb - 1, cx.h, nb > 2 ? (kForward ? 2 : nb - 3) : -1);
-  if (nb > 1) chain_issue(cr, mt, 1, kForward ? 1 : nb - 2, cx.h, nb > 3 ? (kForward ? 3 : nb - 4) : -1);
-  auto nvalid = [&](int u) { return u < kLook ? u : kLook; };
-  // three hand-off registers in rotating roles (no moves of pending loads)
-  unsigned long long cA = kSentinel, cB = kSentinel, cC = kSentinel;
-  for (int u = 0; u < nb; u += 3) {
-    chain_step<kForward>(a, sm, cr, cx, u, nvalid(u), cA, cB, cC);
-    cA = kSentinel;
-    if (u + 1 < nb) chain_step<kForward>(a, sm, cr, cx, u + 1, nvalid(u + 1), cB, cC, cA);
-    cB = kSentinel;
-    if (u + 2 < nb) chain_step<kForward>(a, sm, cr, cx, u + 2, nvalid(u + 2), cC, cA, cB);
-    cC = kSentinel;
+  const int k = (int)cx.h;
+  for (int u = 0; u < kCStages && u < nb; ++u) {
+    const int pf = u + kCStages < nb ? u + kCStages : -1;  // pulled into L2 for the copy issued at step u
+    chain_issue(cr, mt, u, kForward ? u : nb - 1 - u, k, pf < 0 ? -1 : (kForward ? pf : nb - 1 - pf));
   }
-  // the peer's half of the last block is never read by a later step: wait for it
-  mbar_wait_bounded(&sm.ybar[(nb - 1) & (kYSlots - 1)], (unsigned)((nb - 1) >> kYShift) & 1, a.status);
+  if (k == 0) {
+    // three hand-off registers in rotating roles (no moves of pending loads)
+    unsigned long long cA = kSentinel, cB = kSentinel, cC = kSentinel;
+    for (int u = 0; u < nb; u += 3) {
+      head_step<kForward>(a, sm, cr, cx, u, cA, cB, cC);
+      cA = kSentinel;
+      if (u + 1 < nb) head_step<kForward>(a, sm, cr, cx, u + 1, cB, cC, cA);
+      cB = kSentinel;
+      if (u + 2 < nb) head_step<kForward>(a, sm, cr, cx, u + 2, cC, cA, cB);
+      cC = kSentinel;
+    }
+  } else {
+    for (int u = 0; u < nb; ++u) tail_step<kForward>(a, sm, cr, cx, u);
+    // the x_u this tail never reads (the last k + 1): wait for them before the
+    // barriers are re-initialised
+    for (int u = nb - 1 - k > 0 ? nb - 1 - k : 0; u < nb; ++u)
+      mbar_wait_bounded(&sm.xbar[u & (kYSlots - 1)], slot_parity(u), a.status);
+  }
   __syncthreads();
   cluster_sync_all();
 }
@@ -416,8 +460,15 @@ LTB_DEV void chain_sweep(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, 
 LTB_DEV void chain_run(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, unsigned h) {
   ChainCtx cx;
   cx.h = h;
-  cx.peer_ring = mapa_rank(&sm.ring[0][0], h ^ 1u);
-  cx.peer_bar = mapa_rank(&sm.ybar[0], h ^ 1u);
+  if (h == 0) {
+    for (int k = 1; k < kChainCtas; ++k) {
+      cx.peer_v[k] = mapa_rank(&sm.xr[0][0], (unsigned)k);
+      cx.peer_bar[k] = mapa_rank(&sm.xbar[0], (unsigned)k);
+    }
+  } else {
+    cx.peer_v[0] = mapa_rank(&sm.pr[h - 1][0][0], 0u);
+    cx.peer_bar[0] = mapa_rank(&sm.pbar[0], 0u);
+  }
   chain_sweep_init(cr, sm, false);
   chain_sweep<true>(a, sm, cr, cx);
   chain_sweep_init(cr, sm, true);
@@ -648,7 +699,8 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
 }
 
 constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
-static_assert(2 * kLook * kHalfTile <= kRing * kTile, "the chain's two tile stages live in the worker ring's space");
+static_assert(kCStages * 2 * kHalfTile <= kRing * kTile && kCStages <= kRing,
+              "the chain's tile stages live in the worker ring's space");
 
 // ---------------- setup kernels ----------------------------------------------
 // local tile index t of rank r -> (I, J)
