@@ -199,9 +199,14 @@ ltb_status solve_dev(const ltb_engine* e_, const double* in, double* out, cudaSt
                      cudaMemcpyKind kind = cudaMemcpyDeviceToDevice) {
   ltb_engine* e = const_cast<ltb_engine*>(e_);
   const size_t n = (size_t)e->factor.n;
-  ENG_CUDA(cudaMemcpyAsync(e->ypad, in, n * sizeof(double),
-                           kind == cudaMemcpyDeviceToHost ? cudaMemcpyHostToDevice : kind, st));
-  ENG_CUDA(trsv_solve(e->factor, e->ypad, st));
+  // the kernel only reads b: a device input of whole 64-blocks is used in
+  // place (no staging copy on the online path); else staged into the padded
+  // buffer
+  const bool direct = kind == cudaMemcpyDeviceToDevice && n == (size_t)e->factor.nb * kTB;
+  if (!direct)
+    ENG_CUDA(cudaMemcpyAsync(e->ypad, in, n * sizeof(double),
+                             kind == cudaMemcpyDeviceToHost ? cudaMemcpyHostToDevice : kind, st));
+  ENG_CUDA(trsv_solve(e->factor, direct ? in : e->ypad, st));
   count_launches(1);
   if (out)
     ENG_CUDA(cudaMemcpyAsync(out, trsv_result(e->factor), n * sizeof(double),
