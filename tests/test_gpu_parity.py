@@ -194,7 +194,8 @@ def test_register_schedules_persistent(ltb, nt):
 
 @pytest.mark.parametrize("nd,nm,nt", [(1, 1, 4), (1, 300, 9), (31, 7, 12), (33, 64, 20),
                                       (64, 2000, 32), (130, 50, 17), (600, 40, 42),
-                                      (700, 3, 5), (5000, 2, 3)])
+                                      (700, 3, 5), (5000, 2, 3), (1, 1, 64), (1, 7, 420), (2, 1, 512),
+                                      (3, 3, 128)])
 def test_shapes_vs_oracle(ltb, nd, nm, nt):
     """Ragged row / column counts across the GEMV thread mappings (GS lanes,
     RPT rows per thread, column lanes, row tiles)."""
