@@ -389,6 +389,26 @@ class MatvecPlan:
         return m
 
 
+def dense_apply(kernel, v, adjoint=False, mem_cap_bytes=2 << 30):
+    """fft_matvec.hpp:80-87 / fft_matvec.cpp:267-315: the FFT-free time-domain
+    block-Toeplitz product on the device (the reference's test oracle, kept for
+    the drop-in).  ``kernel`` is a BlockToeplitzKernel (host data); ``v`` has
+    n_cols*N_t values (rows_out*N_t for the adjoint) on the host; the result
+    is a new host array.  CapacityError when the implied dense operator
+    exceeds ``mem_cap_bytes`` (0: no cap)."""
+    k = kernel
+    kp, _kk, _a = _buffer(k.data.ravel(), k.rows_out * k.n_cols * k.n_time, "dense_apply kernel")
+    nin = (k.rows_out if adjoint else k.n_cols) * k.n_time
+    nout = (k.n_cols if adjoint else k.rows_out) * k.n_time
+    if type(v).__module__.startswith("torch"):
+        raise ValueError("dense_apply: host arrays only (the kernel is host data)")
+    vp, vk, _b = _buffer(v, nin, "dense_apply input")
+    out = np.empty(nout)
+    check(_lib.load().ltb_dense_apply(kp, k.rows_out, k.n_cols, k.n_time, vp, int(bool(adjoint)),
+                                      int(mem_cap_bytes), C.c_void_p(out.ctypes.data), vk))
+    return out
+
+
 def algorithmic_bytes(rows, cols, nt):
     """Bytes one F or F* matvec must move: F-hat once plus
     the input and output series."""

@@ -258,3 +258,24 @@ def test_forecast_round_trip_register_schedule(ltb, nt):
     assert orc.rel_err(res.m_map.values, m_ref) <= 1e-12
     q_ref = orc.OraclePlan(kq).apply(res.m_map.values)
     assert orc.rel_err(res.q_map.values, q_ref) <= 1e-12
+
+
+def test_online_latency_acceptance_11(ltb):
+    """acceptance_main.cpp:496-516: at Nm=256, Nd=16, Nq=4, Nt=128 the online
+    inversion + forecast touches only the precomputed operators and finishes
+    well under 1 s; its results match the oracle's separate applies."""
+    rng = np.random.default_rng(11)
+    nd, nm, nq, nt = 16, 256, 4, 128
+    kg = rng.standard_normal((nd, nm, nt)) * 0.9 ** np.arange(nt)
+    kq = rng.standard_normal((nq, nm, nt)) * 0.9 ** np.arange(nt)
+    n = nd * nt
+    lo = np.tril(rng.standard_normal((n, n))) * 0.3 / np.sqrt(n) + np.eye(n) * 1.5
+    eng = ltb.InferenceEngine(plan_of(ltb, kg, 2), plan_of(ltb, kq, 1))
+    eng.set_factor(lo)
+    d = rng.standard_normal(n)
+    eng.infer_map(obs(ltb, nd, nt, d), with_forecast=True)  # warm-up
+    res = eng.infer_map(obs(ltb, nd, nt, d), with_forecast=True)
+    assert res.seconds < 1.0
+    y = np.linalg.solve(lo.T, np.linalg.solve(lo, d))
+    assert orc.rel_err(res.m_map.values, orc.OraclePlan(kg).apply_adjoint(y)) <= 1e-12
+    assert orc.rel_err(res.q_map.values, orc.OraclePlan(kq).apply(res.m_map.values)) <= 1e-12

@@ -340,3 +340,26 @@ def test_asymptotic_scaling_fft(ltb):
         if factor <= 2.6:
             break
     assert factor <= 2.6, factor
+
+
+# --- test_fft_matvec.cpp:164-179 (dense_apply contract, on the device) ------
+def test_dense_apply_device(ltb):
+    """ltb_dense_apply (the drop-in's FFT-free oracle): zero kernel -> exact
+    zeros, identity -> reinterpretation, random vs the oracle's dense_apply
+    both ways, CapacityError above the implied-operator cap."""
+    rng = np.random.default_rng(164)
+    k = ltb.BlockToeplitzKernel(3, 4, 9, data=np.zeros((3, 4, 9)))
+    assert np.all(ltb.dense_apply(k, rng.standard_normal(36)) == 0.0)
+    ident = np.zeros((3, 3, 9))
+    for i in range(3):
+        ident[i, i, 0] = 1.0
+    m = rng.standard_normal(27)
+    assert orc.rel_err(ltb.dense_apply(ltb.BlockToeplitzKernel(3, 3, 9, data=ident), m), m) <= 1e-15
+    kr = rng.standard_normal((5, 7, 33))
+    m, d = rng.standard_normal(7 * 33), rng.standard_normal(5 * 33)
+    kb = ltb.BlockToeplitzKernel(5, 7, 33, data=kr)
+    assert orc.rel_err(ltb.dense_apply(kb, m), orc.dense_apply(kr, m, False)) <= TOL
+    assert orc.rel_err(ltb.dense_apply(kb, d, adjoint=True), orc.dense_apply(kr, d, True)) <= TOL
+    assert orc.rel_err(ltb.dense_apply(kb, m), fwd(ltb, mk_plan(ltb, kr), m)) <= TOL
+    with pytest.raises(ltb.CapacityError):
+        ltb.dense_apply(kb, m, mem_cap_bytes=1000)
