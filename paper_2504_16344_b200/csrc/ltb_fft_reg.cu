@@ -14,11 +14,16 @@
 //     as a + i b), groups synchronise with __syncwarp only, and warps loop
 //     persistently over row pairs: no CTA barriers in the steady state and
 //     the pass-2 twiddle table is staged once per CTA;
-//   * pass-1 operands come straight from global memory (row loads
-//     coalesced across the lanes; the zero padding is never stored) and the
-//     c2r output leaves from registers; only the r2c unpack (Z[k] with
-//     Z[N-k]) goes back through shared memory to write the transposed
-//     spectra out[f * ld + row].
+//   * the next pair's operands are prefetched by cp.async into a per-warp
+//     staging buffer while the current pair computes (r2c: the two
+//     contiguous rows; c2r: the pair's two half spectra, 32 contiguous bytes
+//     per frequency, each element read once); strided / generated rows (plan
+//     build) and summed partial slabs load directly; the zero padding is
+//     never stored;
+//   * the c2r rows leave from registers (coalesced across the lanes); the
+//     r2c unpack (Z[k] with Z[N-k]) goes back through shared memory and
+//     writes the transposed spectra out[f * ld + row] with one 256-bit store
+//     per frequency for the pair.
 //
 // Shared layout per sequence: R2 rows of R1 complex padded to R1 + 1
 // (natural index n at n + n / R1): the pass-1 scatter (stride R1 + 1) and the
