@@ -165,7 +165,7 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
   const size_t nb = (size_t)(n + kTB - 1) / kTB;
   const size_t rows = e->rank < (int)nb ? (nb - 1 - e->rank) / e->world + 1 : 0;
   const size_t mine = rows * (e->rank + 1) + (size_t)e->world * rows * (rows - 1) / 2;  // tiles
-  const size_t need = (mine + nb + (e->rank == 0 ? 2 * nb * kLook : 0)) * kTB * kTB * sizeof(double);
+  const size_t need = (mine + nb + (e->rank == 0 ? 2 * nb * (size_t)trsv_look_for((int)nb) : 0)) * kTB * kTB * sizeof(double);
   if (need + (64u << 20) > free_b)
     return efail(LTB_CAPACITY, "set_factor: packed factor needs %zu bytes, %zu free", need, free_b);
   ENG_CUDA(trsv_alloc(e->factor, n, e->world, e->rank));

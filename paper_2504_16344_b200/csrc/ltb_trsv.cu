@@ -11,15 +11,15 @@
 //   * rank 0's CTA 0 is the CHAIN; every other CTA is a WORKER of its rank;
 //   * forward sweep: a worker owns whole block rows of its rank, streams the
 //     row's panel tiles through a TMA ring as soon as the needed y blocks
-//     exist, stops kLook tiles short of the diagonal and hands the chain
-//     c_I = L_II^{-1} (b_I - sum_{J<I-kLook} L_IJ y_J);
-//   * the chain finishes y_I = c_I - sum_{k<=kLook} M_{I,k} y_{I-k}
+//     exist, stops look (4 or 8) tiles short of the diagonal and hands the chain
+//     c_I = L_II^{-1} (b_I - sum_{J<I-look} L_IJ y_J);
+//   * the chain finishes y_I = c_I - sum_{k<=look} M_{I,k} y_{I-k}
 //     (M_{I,k} = L_II^{-1} L_{I,I-k} precomputed, streamed by bulk async
-//     copies into a two-stage shared buffer, last kLook blocks of y kept in
+//     copies into a two-stage shared buffer, last look blocks of y kept in
 //     shared memory) and pushes
 //     y_I to every rank;
 //   * transposed sweep: block column I is spread over the ranks, so every
-//     rank's workers reduce their share s_h = sum_{J=h mod P, J>I+kLook}
+//     rank's workers reduce their share s_h = sum_{J=h mod P, J>I+look}
 //     L_JI^T x_J and push q_h = L_II^{-T} (delta y_I - s_h) to the chain, which
 //     sums the P hand-offs and finishes x_I with M'_{I,k} = L_II^{-T}
 //     L_{I+k,I}^T; x_I is pushed to every rank;
@@ -145,6 +145,7 @@ struct RankView {
 
 struct DistArgs {
   int P, r0, nloc, nb, gper;      // ranks, first local rank, local ranks, blocks, CTAs per rank
+  int look;                       // chain depth = chain CTAs (one cluster)
   RankView loc[kMaxRanks];        // local ranks (index rank - r0)
   double* peer[kMaxRanks];        // recv of EVERY rank, addressable from this launch
   const double* mf;               // chain tiles (rank 0 local)
@@ -163,29 +164,28 @@ LTB_DEV double red_sum(const double (&red)[kQ][kTB], int r) {
   return s;
 }
 
-// The chain is a cluster of kLook = 4 CTAs (CTAs 0-3 of rank 0), CTA k
+// The chain is a cluster of look = 8 or 4 CTAs (trsv_look_for) on rank 0, CTA k
 // owning the chain term of distance k:
-//   HEAD (CTA 0): x_u = c_u - M_{u,0} x_{u-1} - sum_{k=1..3} P^k_u, with
-//     x_{u-1} its own previous output (local shared memory) -- the
-//     step-to-step critical path has no cross-CTA exchange and one tile;
-//   TAIL k (CTAs 1-3): P^k_u = M_{u,k} x_{u-1-k}, needing x only k steps
+//   HEAD (CTA 0): x_u = -(M_{u,0} x_{u-1} + sum_{k>=1} P^k_u), with x_{u-1}
+//     its own previous output (local shared memory) -- the step-to-step
+//     critical path has no cross-CTA exchange and one tile;
+//   TAIL k (CTAs 1..look-1): P^k_u = M_{u,k} x_{u-1-k}, needing x only k steps
 //     after the head produced it; the partial sums arrive (st.async into the
-//     head's shared memory, all three completing one mbarrier) before the
-//     head needs them.
+//     head's shared memory, all completing one mbarrier) before the
+//     head needs them.  The last tail also folds in the workers' hand-off
+//     c_u (P^{look-1}_u - c_u), so the head never polls global memory; the
+//     workers hand off look steps before c_u is needed.
 // The head pushes every x_u to the tails the same way.  Each CTA ingests one
-// 32 KB tile per step.
-constexpr int kChainCtas = kLook;
+// 32 KB tile per step.  (Clusters of 8 cost co-residency: 120 of 148 SMs.)
 constexpr int kHalf = kTB / 2;            // tile storage split in row halves (chain_idx)
 constexpr int kHalfTile = kTB * kHalf;    // 2048 doubles
-constexpr int kYShift = 3;
+constexpr int kYShift = 4;
 constexpr int kYSlots = 1 << kYShift;
-constexpr int kCStages = 4;               // chain tile copies issued four steps ahead
-static_assert((kChainCtas & (kChainCtas - 1)) == 0, "cluster size must be a power of two");
-static_assert(kLook + 1 < kYSlots, "x ring too short");
+constexpr int kCStages = 2;               // chain tile copies issued two steps ahead
+static_assert(kMaxLook + 1 < kYSlots, "x ring too short");
 
 struct ChainSmem {
   double xr[kYSlots][kTB];                  // solution blocks (head: written locally; tails: received)
-  double pr[kChainCtas - 1][kYSlots][kTB];  // head: the tails' partial sums
   double red[kQ][kTB];
   uint64_t xbar[kYSlots];                   // tail: slot of x_u arrived
   uint64_t pbar[kYSlots];                   // head: all tails' P_u arrived
@@ -219,33 +219,34 @@ LTB_DEV void grid_barrier(unsigned* gsync) {
 
 // ---------------- chain ------------------------------------------------------
 // Chain tiles are stored split by half: step I, half h, tile k, column c,
-// row ii (< 32) at ((I * 2 + h) * kLook + k) * kHalfTile + c * kHalf + ii, so
+// row ii (< 32) at ((I * 2 + h) * look + k) * kHalfTile + c * kHalf + ii, so
 // tile k of a step is two contiguous 16 KB runs (rows 0-31 and 32-63),
 // brought in by bulk async copies (TMA 1-D) into a kCStages-deep shared ring
 // kCStages steps ahead, and pulled into L2 two steps before that.
-__host__ __device__ inline size_t chain_idx(int I, int k, int row, int col) {
-  return ((size_t)(I * 2 + (row >> 5)) * kLook + k) * kHalfTile + (size_t)col * kHalf + (row & 31);
+__host__ __device__ inline size_t chain_idx(int look, int I, int k, int row, int col) {
+  return ((size_t)(I * 2 + (row >> 5)) * look + k) * kHalfTile + (size_t)col * kHalf + (row & 31);
 }
 
 struct ChainRing {
   double* stage;   // kCStages stages x 1 tile, [half][col][row & 31] (dynamic shared memory)
+  double* pr;      // head: the tails' partial sums [k - 1][slot][row] (dynamic shared memory)
   uint64_t* full;  // kCStages mbarriers
 };
 
 // tile k of block I for step u; issued by a thread of warp 2 (warps 0-1
 // carry the head's hand-off / reduction / push right after the barrier)
-LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int u, int I, int k, int I_pf) {
+LTB_DEV void chain_issue(const ChainRing& cr, const double* mtiles, int look, int u, int I, int k, int I_pf) {
   if (threadIdx.x == 64) {
     const int s = u % kCStages;
     constexpr unsigned kRun = kHalfTile * sizeof(double);  // 16 KB: one row half of the tile
     mbar_arrive_expect_tx(cr.full + s, 2 * kRun);
     double* dst = cr.stage + (size_t)s * 2 * kHalfTile;
     for (int hh = 0; hh < 2; ++hh) {
-      bulk_g2s(dst + (size_t)hh * kHalfTile, mtiles + ((size_t)(I * 2 + hh) * kLook + k) * kHalfTile, kRun,
+      bulk_g2s(dst + (size_t)hh * kHalfTile, mtiles + ((size_t)(I * 2 + hh) * look + k) * kHalfTile, kRun,
                cr.full + s, policy_evict_first());
       if (I_pf >= 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                         mtiles + ((size_t)(I_pf * 2 + hh) * kLook + k) * kHalfTile),
+                         mtiles + ((size_t)(I_pf * 2 + hh) * look + k) * kHalfTile),
                      "r"(kRun)
                      : "memory");
     }
@@ -290,8 +291,8 @@ LTB_DEV void cluster_sync_all() {
 
 struct ChainCtx {
   unsigned h;                      // 0 = head, k = tail of chain term k
-  uint32_t peer_v[kChainCtas];     // head: &tail_k.xr[0][0]; tail: [0] = &head.pr[h - 1][0][0]
-  uint32_t peer_bar[kChainCtas];   // head: &tail_k.xbar[0]; tail: [0] = &head.pbar[0]
+  uint32_t peer_v[kMaxLook];     // head: &tail_k.xr[0][0]; tail: [0] = &head.pr[h - 1][0][0]
+  uint32_t peer_bar[kMaxLook];   // head: &tail_k.xbar[0]; tail: [0] = &head.pbar[0]
 };
 
 LTB_DEV unsigned slot_parity(int u) { return (unsigned)(u >> kYShift) & 1; }
@@ -320,35 +321,26 @@ LTB_DEV double red_tree(const double (&red)[kQ][kTB], int r) {
 LTB_DEV void chain_wait_tiles(const ChainRing& cr, int u, int* status) {
   mbar_wait_bounded(cr.full + u % kCStages, (unsigned)(u / kCStages) & 1, status);
 }
+template <int L>
 LTB_DEV void chain_next_tiles(const DistArgs& a, const ChainRing& cr, const double* mt, int u, int k,
                               bool fwd) {
   const int nb = a.nb, un = u + kCStages;
-  if (un < nb) chain_issue(cr, mt, un, fwd ? un : nb - 1 - un, k, un + 2 < nb ? (fwd ? un + 2 : nb - 3 - un) : -1);
+  if (un < nb)
+    chain_issue(cr, mt, L, un, fwd ? un : nb - 1 - un, k, un + 2 < nb ? (fwd ? un + 2 : nb - 3 - un) : -1);
 }
 
-// Head step u (block I = u forward, nb - 1 - u transposed).  `cur` is this
-// step's hand-off prefetched earlier; `nxt` / `nxt2` the next two.
-// Hand-off: forward = cf[I] (one worker); transposed = sum over the P ranks'
-// cb[h][I], in rank order.
-template <bool kForward>
-LTB_DEV void head_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u,
-                       unsigned long long cur, unsigned long long& nxt, unsigned long long& nxt2) {
+// Head step u (block I = u forward, nb - 1 - u transposed):
+// x_u = -(M_{u,0} x_{u-1} + P^1_u + P^2_u + P^3_u), the worker hand-off c_u
+// already folded into P^3_u by the last tail (off the critical path).
+template <bool kForward, int L>
+LTB_DEV void head_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u) {
   const int tid = threadIdx.x, i = tid & (kTB - 1), q = tid / kTB;
-  const int nb = a.nb, P = kForward ? 1 : a.P;
+  const int nb = a.nb;
   const int I = kForward ? u : nb - 1 - u;
-  double* recv0 = a.loc[0].recv;  // the chain runs on rank 0 = local rank 0
-  const double* cbuf = recv0 + (kForward ? off_cf(nb) : off_cb(nb));
-  const int In = kForward ? I + 1 : I - 1, In2 = kForward ? I + 2 : I - 2;
   const int slot = u & (kYSlots - 1);
   if (tid == 0)  // the tails' P_u
-    mbar_arrive_expect_tx(&sm.pbar[slot], (kChainCtas - 1) * kTB * sizeof(double));
+    mbar_arrive_expect_tx(&sm.pbar[slot], (L - 1) * kTB * sizeof(double));
   if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I] = clock64();
-  // rank 0's hand-offs are prefetched two steps ahead and re-read a step
-  // ahead while still unpublished, so the wait below is rarely a round trip
-  if (tid < kTB) {
-    if (In2 >= 0 && In2 < nb) nxt2 = ld_relaxed_u64(cbuf + (size_t)In2 * kTB + tid);
-    if (In >= 0 && In < nb && nxt == kSentinel) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
-  }
   chain_wait_tiles(cr, u, a.status);
   if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 1] = clock64();
   sm.red[q][i] = u >= 1 ? chain_fma(cr.stage + (size_t)(u % kCStages) * 2 * kHalfTile,
@@ -356,25 +348,23 @@ LTB_DEV void head_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, co
                         : 0.0;
   __syncthreads();  // also: every thread is done with this tile stage
   if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 2] = clock64();
-  chain_next_tiles(a, cr, kForward ? a.mf : a.mb, u, 0, kForward);
+  chain_next_tiles<L>(a, cr, kForward ? a.mf : a.mb, u, 0, kForward);
   if (tid < kTB) {
-    unsigned long long raw[kMaxRanks];
-    for (int hh = 1; hh < P; ++hh) raw[hh] = ld_relaxed_u64(cbuf + ((size_t)hh * nb + I) * kTB + tid);
-    double c = cur != kSentinel ? __longlong_as_double((long long)cur)
-                                : poll_value<false>(cbuf + (size_t)I * kTB + tid, a.status);
-    for (int hh = 1; hh < P; ++hh)  // fixed order h = 0, 1, ..., P-1
-      c += raw[hh] != kSentinel ? __longlong_as_double((long long)raw[hh])
-                                : poll_value<false>(cbuf + ((size_t)hh * nb + I) * kTB + tid, a.status);
-    if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
-    const double s = red_tree(sm.red, tid);
+    double s = red_tree(sm.red, tid);
     mbar_wait_bounded(&sm.pbar[slot], slot_parity(u), a.status);  // normally long complete
-    double v = c - s;
+    if (kForward && a.trace && tid == 0) a.trace[4 * nb + 1 + 4 * I + 3] = clock64();
+    double pk[kMaxLook - 1];  // all partials loaded at once (compile-time slots), then summed in order
 #pragma unroll
-    for (int k = 0; k < kChainCtas - 1; ++k) v -= sm.pr[k][slot][tid];
+    for (int k = 0; k < kMaxLook - 1; ++k) pk[k] = k < L - 1 ? cr.pr[((size_t)k * kYSlots + slot) * kTB + tid] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxLook - 1; ++k)
+      if (k < L - 1) s += pk[k];
+    const double v = -s;
     sm.xr[slot][tid] = v;
 #pragma unroll
-    for (int k = 1; k < kChainCtas; ++k)
-      st_async_f64(cx.peer_v[k] + (uint32_t)(slot * kTB + tid) * 8u, v, cx.peer_bar[k] + (uint32_t)slot * 8u);
+    for (int k = 1; k < kMaxLook; ++k)
+      if (k < L)
+        st_async_f64(cx.peer_v[k] + (uint32_t)(slot * kTB + tid) * 8u, v, cx.peer_bar[k] + (uint32_t)slot * 8u);
     const size_t o = (kForward ? off_yf(nb) : off_xb(nb)) + (size_t)I * kTB + tid;
     for (int r = 0; r < a.P; ++r) a.peer[r][o] = v;  // push to every rank
   }
@@ -382,13 +372,26 @@ LTB_DEV void head_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, co
   if (a.trace && threadIdx.x == 0) a.trace[(kForward ? 0 : nb) + I] = globaltimer();
 }
 
-// Tail k, step u: P^k_u = M_{u,k} x_{u-1-k} -> the head's pr[k - 1] slot
-template <bool kForward>
-LTB_DEV void tail_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u) {
+// Tail k, step u: P^k_u = M_{u,k} x_{u-1-k} -> the head's pr[k - 1] slot.
+// The last tail also resolves the worker hand-off c_u (forward: cf[I] of
+// one worker; transposed: the P ranks' cb[h][I] summed in rank order) and
+// sends P^3_u - c_u; `cur` is c_u's raw value prefetched earlier, `nxt` /
+// `nxt2` receive the next two.
+template <bool kForward, int L>
+LTB_DEV void tail_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx, int u,
+                       unsigned long long cur, unsigned long long& nxt, unsigned long long& nxt2) {
   const int tid = threadIdx.x, i = tid & (kTB - 1), q = tid / kTB;
-  const int k = (int)cx.h;
+  const int k = (int)cx.h, nb = a.nb, P = kForward ? 1 : a.P;
+  const int I = kForward ? u : nb - 1 - u;
+  const bool last = k == L - 1;
+  const double* cbuf = a.loc[0].recv + (kForward ? off_cf(nb) : off_cb(nb));  // rank 0 = local rank 0
   const int slot = u & (kYSlots - 1);
   if (tid == 0) mbar_arrive_expect_tx(&sm.xbar[slot], kTB * sizeof(double));  // x_u from the head
+  if (last && tid < kTB) {  // hand-offs prefetched two steps ahead, re-read a step ahead while unpublished
+    const int In = kForward ? I + 1 : I - 1, In2 = kForward ? I + 2 : I - 2;
+    if (In2 >= 0 && In2 < nb) nxt2 = ld_relaxed_u64(cbuf + (size_t)In2 * kTB + tid);
+    if (In >= 0 && In < nb && nxt == kSentinel) nxt = ld_relaxed_u64(cbuf + (size_t)In * kTB + tid);
+  }
   chain_wait_tiles(cr, u, a.status);
   const int src = u - 1 - k;
   if (src >= 0) mbar_wait_bounded(&sm.xbar[src & (kYSlots - 1)], slot_parity(src), a.status);
@@ -396,10 +399,21 @@ LTB_DEV void tail_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, co
                                       sm.xr[src & (kYSlots - 1)], i, q)
                           : 0.0;
   __syncthreads();
-  chain_next_tiles(a, cr, kForward ? a.mf : a.mb, u, k, kForward);
-  if (tid < kTB)
-    st_async_f64(cx.peer_v[0] + (uint32_t)(slot * kTB + tid) * 8u, red_tree(sm.red, tid),
-                 cx.peer_bar[0] + (uint32_t)slot * 8u);
+  chain_next_tiles<L>(a, cr, kForward ? a.mf : a.mb, u, k, kForward);
+  if (tid < kTB) {
+    double pv = red_tree(sm.red, tid);
+    if (last) {
+      unsigned long long raw[kMaxRanks];
+      for (int hh = 1; hh < P; ++hh) raw[hh] = ld_relaxed_u64(cbuf + ((size_t)hh * nb + I) * kTB + tid);
+      double c = cur != kSentinel ? __longlong_as_double((long long)cur)
+                                  : poll_value<false>(cbuf + (size_t)I * kTB + tid, a.status);
+      for (int hh = 1; hh < P; ++hh)  // fixed order h = 0, 1, ..., P-1
+        c += raw[hh] != kSentinel ? __longlong_as_double((long long)raw[hh])
+                                  : poll_value<false>(cbuf + ((size_t)hh * nb + I) * kTB + tid, a.status);
+      pv -= c;
+    }
+    st_async_f64(cx.peer_v[0] + (uint32_t)(slot * kTB + tid) * 8u, pv, cx.peer_bar[0] + (uint32_t)slot * 8u);
+  }
   __syncthreads();
 }
 
@@ -426,28 +440,28 @@ LTB_DEV void chain_sweep_init(const ChainRing& cr, ChainSmem& sm, bool reinit) {
   cluster_sync_all();
 }
 
-template <bool kForward>
+template <bool kForward, int L>
 LTB_DEV void chain_sweep(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, const ChainCtx& cx) {
   const int nb = a.nb;
   const double* mt = kForward ? a.mf : a.mb;
   const int k = (int)cx.h;
   for (int u = 0; u < kCStages && u < nb; ++u) {
     const int pf = u + kCStages < nb ? u + kCStages : -1;  // pulled into L2 for the copy issued at step u
-    chain_issue(cr, mt, u, kForward ? u : nb - 1 - u, k, pf < 0 ? -1 : (kForward ? pf : nb - 1 - pf));
+    chain_issue(cr, mt, L, u, kForward ? u : nb - 1 - u, k, pf < 0 ? -1 : (kForward ? pf : nb - 1 - pf));
   }
   if (k == 0) {
+    for (int u = 0; u < nb; ++u) head_step<kForward, L>(a, sm, cr, cx, u);
+  } else {
     // three hand-off registers in rotating roles (no moves of pending loads)
     unsigned long long cA = kSentinel, cB = kSentinel, cC = kSentinel;
     for (int u = 0; u < nb; u += 3) {
-      head_step<kForward>(a, sm, cr, cx, u, cA, cB, cC);
+      tail_step<kForward, L>(a, sm, cr, cx, u, cA, cB, cC);
       cA = kSentinel;
-      if (u + 1 < nb) head_step<kForward>(a, sm, cr, cx, u + 1, cB, cC, cA);
+      if (u + 1 < nb) tail_step<kForward, L>(a, sm, cr, cx, u + 1, cB, cC, cA);
       cB = kSentinel;
-      if (u + 2 < nb) head_step<kForward>(a, sm, cr, cx, u + 2, cC, cA, cB);
+      if (u + 2 < nb) tail_step<kForward, L>(a, sm, cr, cx, u + 2, cC, cA, cB);
       cC = kSentinel;
     }
-  } else {
-    for (int u = 0; u < nb; ++u) tail_step<kForward>(a, sm, cr, cx, u);
     // the x_u this tail never reads (the last k + 1): wait for them before the
     // barriers are re-initialised
     for (int u = nb - 1 - k > 0 ? nb - 1 - k : 0; u < nb; ++u)
@@ -457,22 +471,24 @@ LTB_DEV void chain_sweep(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, 
   cluster_sync_all();
 }
 
+template <int L>
 LTB_DEV void chain_run(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, unsigned h) {
   ChainCtx cx;
   cx.h = h;
   if (h == 0) {
-    for (int k = 1; k < kChainCtas; ++k) {
-      cx.peer_v[k] = mapa_rank(&sm.xr[0][0], (unsigned)k);
-      cx.peer_bar[k] = mapa_rank(&sm.xbar[0], (unsigned)k);
+#pragma unroll
+    for (int k = 1; k < kMaxLook; ++k) {  // compile-time slots: cx stays in registers
+      cx.peer_v[k] = k < L ? mapa_rank(&sm.xr[0][0], (unsigned)k) : 0u;
+      cx.peer_bar[k] = k < L ? mapa_rank(&sm.xbar[0], (unsigned)k) : 0u;
     }
   } else {
-    cx.peer_v[0] = mapa_rank(&sm.pr[h - 1][0][0], 0u);
+    cx.peer_v[0] = mapa_rank(cr.pr + (size_t)(h - 1) * kYSlots * kTB, 0u);
     cx.peer_bar[0] = mapa_rank(&sm.pbar[0], 0u);
   }
   chain_sweep_init(cr, sm, false);
-  chain_sweep<true>(a, sm, cr, cx);
+  chain_sweep<true, L>(a, sm, cr, cx);
   chain_sweep_init(cr, sm, true);
-  chain_sweep<false>(a, sm, cr, cx);
+  chain_sweep<false, L>(a, sm, cr, cx);
 }
 
 // ---------------- workers: TMA tile ring ------------------------------------
@@ -494,13 +510,14 @@ LTB_DEV void ring_issue(TileRing& r, unsigned g, const double* src, uint64_t pol
 }
 
 // forward row I of rank r: thread (i = tid & 63, q = tid >> 6) owns row i,
-// columns [8q, 8q+8) of each tile L_IJ, J < I - kLook (contiguous in memory)
+// columns [8q, 8q+8) of each tile L_IJ, J < I - look (contiguous in memory)
+template <int L>
 LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSmem& sm,
                                 TileRing& ring, int I, const double* row, uint64_t policy) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
   const int nb = a.nb;
   const double* yf = rv.recv + off_yf(nb);
-  const int jmax = I - kLook;  // panel tiles J < jmax; the chain does the rest
+  const int jmax = I - L;  // panel tiles J < jmax; the chain does the rest
   const unsigned g0 = ring.next;
   if (tid == 0)
     for (int J = 0; J < jmax && J < kRing; ++J) ring_issue(ring, g0 + J, row + (size_t)J * kTile, policy);
@@ -547,17 +564,18 @@ LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSme
 }
 
 // transposed column I, rank r's share: thread (j = tid & 63, q = tid >> 6)
-// reads row j of tile L_JI for J = r (mod P), J > I + kLook (descending),
+// reads row j of tile L_JI for J = r (mod P), J > I + look (descending),
 // columns [8q, 8q+8), keeping 8 partial sums of (L_JI^T x_J); hands the
 // chain q_r = L_II^{-T} (delta_{r, I mod P} y_I - s_r)
+template <int L>
 LTB_DEV void worker_transposed_col(const DistArgs& a, const RankView& rv, int r, WorkerSmem& sm,
                                    TileRing& ring, int I, uint64_t policy) {
   const int tid = threadIdx.x, j = tid & 63, q = tid >> 6;
   const int nb = a.nb, P = a.P;
   const double* xb = rv.recv + off_xb(nb);
   const double* yf = rv.recv + off_yf(nb);
-  // this rank's rows J > I + kLook, descending from the largest J = r (mod P)
-  const int jmin = I + kLook;
+  // this rank's rows J > I + look, descending from the largest J = r (mod P)
+  const int jmin = I + L;
   const int Jtop = nb - 1 - ((nb - 1 - r) % P + P) % P;
   const int ntile = Jtop > jmin ? (Jtop - jmin - 1) / P + 1 : 0;
   auto tile_of = [&](int J) {
@@ -620,6 +638,7 @@ LTB_DEV void worker_transposed_col(const DistArgs& a, const RankView& rv, int r,
   if (a.trace && tid == 0 && a.r0 == 0 && r == 0) a.trace[3 * nb + I] = globaltimer();
 }
 
+template <int L>
 __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
   __shared__ union {
     ChainSmem chain;
@@ -665,11 +684,12 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && a.r0 == 0) a.trace[4 * nb] = globaltimer();
 
-  if (r == 0 && lc < kChainCtas) {
+  if (r == 0 && lc < L) {
     ChainRing cr;
     cr.stage = reinterpret_cast<double*>(ring_smem);
+    cr.pr = cr.stage + (size_t)kCStages * 2 * kHalfTile;
     cr.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kRing * kTile * sizeof(double));
-    chain_run(a, sm.chain, cr, (unsigned)lc);
+    chain_run<L>(a, sm.chain, cr, (unsigned)lc);
   } else {
     TileRing ring;
     ring.stage = reinterpret_cast<double*>(ring_smem);
@@ -682,13 +702,13 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
       policy = policy_evict_first();
     }
     __syncthreads();
-    const int w = r == 0 ? lc - kChainCtas : lc, W = r == 0 ? a.gper - kChainCtas : a.gper;
+    const int w = r == 0 ? lc - L : lc, W = r == 0 ? a.gper - L : a.gper;
     // forward: this rank's rows I = r + P li
     const int nrows = r < nb ? (nb - 1 - r) / a.P + 1 : 0;
     for (int li = w; li < nrows; li += W)
-      worker_forward_row(a, rv, sm.worker, ring, r + a.P * li, rv.tiles + row_off(li, r, a.P) * kTile, policy);
+      worker_forward_row<L>(a, rv, sm.worker, ring, r + a.P * li, rv.tiles + row_off(li, r, a.P) * kTile, policy);
     // transposed: every column, this rank's share
-    for (int I = nb - 1 - w; I >= 0; I -= W) worker_transposed_col(a, rv, r, sm.worker, ring, I, policy);
+    for (int I = nb - 1 - w; I >= 0; I -= W) worker_transposed_col<L>(a, rv, r, sm.worker, ring, I, policy);
   }
   // (3) leave only once this rank's copy of x is complete
   {
@@ -699,8 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
 }
 
 constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
-static_assert(kCStages * 2 * kHalfTile <= kRing * kTile && kCStages <= kRing,
-              "the chain's tile stages live in the worker ring's space");
+static_assert(kCStages * 2 * kHalfTile + (kMaxLook - 1) * kYSlots * kTB <= kRing * kTile && kCStages <= kRing,
+              "the chain's tile stages and partial sums live in the worker ring's space");
 
 // ---------------- setup kernels ----------------------------------------------
 // local tile index t of rank r -> (I, J)
@@ -784,7 +804,7 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
                                                           uint64_t key, double scale, int n,
                                                           const double* __restrict__ dinv,
                                                           double* __restrict__ mf,
-                                                          double* __restrict__ mb, int nb) {
+                                                          double* __restrict__ mb, int nb, int look) {
   extern __shared__ double ct_smem[];
   double* sA = ct_smem;               // Dinv_II, sA[col * kPad + row]
   double* sB = ct_smem + kTB * kPad;  // panel tile, same layout
@@ -793,7 +813,7 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
   const int J = dir == 0 ? I - k : I + k;
   if (J < 0 || J >= nb) {
-    for (int e = tid; e < kTile; e += blockDim.x) C[chain_idx(I, k - 1, e & 63, e >> 6)] = 0.0;
+    for (int e = tid; e < kTile; e += blockDim.x) C[chain_idx(look, I, k - 1, e & 63, e >> 6)] = 0.0;
     return;
   }
   const double* A = dinv + (size_t)I * kTile;
@@ -808,46 +828,48 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
     } else {
       for (int l = 0; l < kTB; ++l) s = fma(sA[i * kPad + l], sB[l * kPad + jj], s);
     }
-    C[chain_idx(I, k - 1, i, jj)] = s;
+    C[chain_idx(look, I, k - 1, i, jj)] = s;
   }
 }
 
-int g_coop_blocks = -1;  // co-resident CTAs of trsv_kernel on this device
+int g_coop_blocks[kMaxLook + 1] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // per cluster size
 
-cudaError_t coop_blocks(int* out) {
-  if (g_coop_blocks < 0) {
+cudaError_t coop_blocks(int look, int* out) {
+  int& cb = g_coop_blocks[look];
+  if (cb < 0) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const void* fn = look == 8 ? (const void*)trsv_kernel<8> : (const void*)trsv_kernel<4>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRingSmem);
     if (e != cudaSuccess) return e;
     // clusters of two co-resident CTAs (the chain pair); workers come in pairs too
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kChainCtas * 16);
+    cfg.gridDim = dim3(look * 16);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = kRingSmem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kChainCtas;
+    at[0].val.clusterDim.x = look;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, (void*)trsv_kernel, &cfg) != cudaSuccess) clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) clusters = 0;
     cudaGetLastError();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_kernel, kThreads, kRingSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, kRingSmem);
     // (some tools report no cluster occupancy: fall back to the per-SM count;
     // the grid never exceeds what one SM per CTA can hold)
     const int by_sm = sms * per;
-    g_coop_blocks = (clusters > 0 ? std::min(by_sm, clusters * kChainCtas) : by_sm) & ~(kChainCtas - 1);
-    g_coop_blocks = std::max(g_coop_blocks, 2 * kChainCtas);
+    cb = (clusters > 0 ? std::min(by_sm, clusters * look) : by_sm) & ~(look - 1);
+    cb = std::max(cb, 2 * look);
     if (getenv("LTB_DEBUG"))
       fprintf(stderr, "ltb trsv: sms=%d blocks/SM=%d clusters=%d -> %d co-resident CTAs\n", sms, per, clusters,
-              g_coop_blocks);
+              cb);
   }
-  *out = g_coop_blocks;
+  *out = cb;
   return cudaSuccess;
 }
 
@@ -857,8 +879,8 @@ cudaError_t prepare(TriFactor& t, bool gen, uint64_t key, double scale, cudaStre
   cudaFuncSetAttribute(chain_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   invert_diag_kernel<<<t.nb, kTB, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv, t.status);
   if (t.rank == 0)
-    chain_tiles_kernel<<<dim3(t.nb, kLook, 2), 256, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv,
-                                                                  t.mf, t.mb, t.nb);
+    chain_tiles_kernel<<<dim3(t.nb, t.look, 2), 256, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv,
+                                                                   t.mf, t.mb, t.nb, t.look);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int h = 0;
@@ -880,6 +902,7 @@ DistArgs make_args(TriFactor* const* ts, const double* const* bs, int nloc, int 
   a.nloc = nloc;
   a.nb = t0.nb;
   a.gper = gper;
+  a.look = t0.look;
   for (int g = 0; g < nloc; ++g) a.loc[g] = RankView{ts[g]->tiles, ts[g]->dinv, bs[g], ts[g]->recv};
   for (int p = 0; p < a.P; ++p) a.peer[p] = nloc == a.P ? ts[p]->recv : t0.peer_recv[p];
   a.mf = t0.mf;
@@ -905,12 +928,12 @@ cudaError_t launch(const DistArgs& a, cudaStream_t st) {
   // out into a status error rather than hanging if residency ever fails.
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kChainCtas;
+  at[0].val.clusterDim.x = a.look;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, trsv_kernel, a);
+  return a.look == 8 ? cudaLaunchKernelEx(&cfg, trsv_kernel<8>, a) : cudaLaunchKernelEx(&cfg, trsv_kernel<4>, a);
 }
 
 }  // namespace
@@ -923,7 +946,8 @@ cudaError_t trsv_alloc(TriFactor& t, int n, int P, int rank) {
   t.P = P;
   t.rank = rank;
   const size_t ntiles = rank_tiles(t.nb, rank, P);
-  const size_t chain = rank == 0 ? (size_t)t.nb * kLook * kTile : 0;
+  t.look = trsv_look_for(t.nb);
+  const size_t chain = rank == 0 ? (size_t)t.nb * t.look * kTile : 0;
   const size_t rl = recv_len(t.nb, P);
   t.bytes = (ntiles + t.nb) * kTile * sizeof(double) + 2 * chain * sizeof(double) + rl * sizeof(double);
   cudaError_t e;
@@ -1002,10 +1026,11 @@ cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
   for (int p = 0; p < t.P; ++p)
     if (!t.peer_recv[p]) return cudaErrorInvalidValue;  // not connected
   int blocks = 0;
-  cudaError_t e = coop_blocks(&blocks);
+  cudaError_t e = coop_blocks(t.look, &blocks);
   if (e != cudaSuccess) return e;
-  // the chain pair + up to one worker per block row, in whole clusters
-  const int gper = std::min(blocks, std::max(2 * kChainCtas, (t.nb + kChainCtas + 1) & ~(kChainCtas - 1)));
+  // the chain cluster + up to one worker per block row, in whole clusters
+  const int L = t.look;
+  const int gper = std::min(blocks, std::max(2 * L, (t.nb + L + L - 1) / L * L));
   TriFactor* ts[1] = {&t};
   const double* bs[1] = {b};
   return launch(make_args(ts, bs, 1, gper), st);
@@ -1014,10 +1039,11 @@ cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
 cudaError_t trsv_solve_emulated(TriFactor* const* ts, const double* const* bs, int P, cudaStream_t st) {
   if (P < 1 || P > kMaxRanks || ts[0]->P != P) return cudaErrorInvalidValue;
   int blocks = 0;
-  cudaError_t e = coop_blocks(&blocks);
+  const int L = ts[0]->look;
+  cudaError_t e = coop_blocks(L, &blocks);
   if (e != cudaSuccess) return e;
-  const int gper = (blocks / P) & ~(kChainCtas - 1);
-  if (gper < 2 * kChainCtas) return cudaErrorInvalidValue;
+  const int gper = (blocks / P) / L * L;
+  if (gper < 2 * L) return cudaErrorInvalidValue;
   return launch(make_args(ts, bs, P, gper), st);
 }
 

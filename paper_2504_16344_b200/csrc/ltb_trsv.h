@@ -10,7 +10,12 @@
 namespace ltb {
 
 constexpr int kTB = 64;        // factor tile edge
-constexpr int kLook = 4;       // diagonal-chain lookahead depth (tiles per chain step)
+constexpr int kMaxLook = 8;    // diagonal-chain lookahead depth bound (chain terms = chain CTAs)
+// Chain depth for nb blocks: 8 terms (a cluster of 8 chain CTAs) where the
+// sequential chain dominates (small n: the workers get 8 steps of slack), 4
+// where panel streaming dominates (clusters of 8 leave only 120 of 148 SMs
+// co-resident).  Every rank of a distributed factor picks the same depth.
+inline int trsv_look_for(int nb) { return nb <= 256 ? 8 : 4; }
 constexpr int kMaxRanks = 8;
 
 // Row-cyclic block distribution over P ranks: rank r holds the 64-row block
@@ -27,6 +32,7 @@ constexpr int kMaxRanks = 8;
 // [ yf | xb | ready (8 doubles) | cf | cb (P blocks) ], each vector nb*64.
 struct TriFactor {
   int n = 0, nb = 0, P = 1, rank = 0;
+  int look = 4;  // chain depth (trsv_look_for)
   double* tiles = nullptr;
   double* dinv = nullptr;
   double* mf = nullptr;
