@@ -8,16 +8,17 @@
 //
 //   * the factor is distributed row-cyclically (block row I on rank I mod P;
 //     P = 1 is the single-GPU packed triangle);
-//   * rank 0's CTA 0 is the CHAIN; every other CTA is a WORKER of its rank;
+//   * rank 0's first `look` CTAs (one cluster, look = 8 for nb <= 256 else
+//     4) are the CHAIN; every other CTA is a WORKER of its rank;
 //   * forward sweep: a worker owns whole block rows of its rank, streams the
 //     row's panel tiles through a TMA ring as soon as the needed y blocks
-//     exist, stops look (4 or 8) tiles short of the diagonal and hands the chain
+//     exist, stops `look` tiles short of the diagonal and hands the chain
 //     c_I = L_II^{-1} (b_I - sum_{J<I-look} L_IJ y_J);
-//   * the chain finishes y_I = c_I - sum_{k<=look} M_{I,k} y_{I-k}
-//     (M_{I,k} = L_II^{-1} L_{I,I-k} precomputed, streamed by bulk async
-//     copies into a two-stage shared buffer, last look blocks of y kept in
-//     shared memory) and pushes
-//     y_I to every rank;
+//   * the chain finishes y_I = c_I - sum_{k<look} M_{I,k} y_{I-1-k}
+//     (M_{I,k} = L_II^{-1} L_{I,I-1-k} precomputed): chain CTA k owns term k,
+//     the head (k = 0) adds the other CTAs' partial sums (sent ahead through
+//     distributed shared memory; the last one carries c_I) to its own term
+//     and pushes y_I to every rank (see "chain" below);
 //   * transposed sweep: block column I is spread over the ranks, so every
 //     rank's workers reduce their share s_h = sum_{J=h mod P, J>I+look}
 //     L_JI^T x_J and push q_h = L_II^{-T} (delta y_I - s_h) to the chain, which
