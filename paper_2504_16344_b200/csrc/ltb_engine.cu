@@ -636,20 +636,116 @@ extern "C" ltb_status ltb_debug_dtrsv_emulated(int n, int P, uint64_t seed, cons
 // ---------------------------------------------------------------------------
 // Q d forecast with credible intervals (predict_qoi, bayes_engine.cpp:340-362)
 //
-// Q (Nq*Nt x Nd*Nt, column-major) is the one dense operator of the online
-// phase (17.8 GB at Cascadia).  Its GEMV is the same HBM-streaming problem as
-// GEMV-N, so it reuses that kernel: a column of Q with an even number of rows
-// read as complex pairs (q_2i, q_2i+1) times the real d_j embedded as (d_j, 0)
-// gives complex partial sums whose real / imaginary parts are exactly
-// sum_j Q_2i,j d_j and sum_j Q_2i+1,j d_j.
+// Q (Nq*Nt x Nd*Nt, column-major, rows padded to even) is the one dense
+// operator of the online phase (17.8 GB at Cascadia): a tall column-major
+// GEMV streamed once from HBM.  qd_gemv_kernel: one CTA per SM, each owning
+// a contiguous column range (and a row tile of <= 72 KB per column, the
+// whole column at Cascadia), so its share of Q is one contiguous run that
+// arrives by bulk async copies (TMA 1-D, one per column segment) into a
+// 3-deep shared-memory ring; thread t accumulates row pairs (2p, 2p+1),
+// p = t + 512 k, in registers over its columns in order.  qd_finish_kernel
+// sums the per-range partials in range order (deterministic) and writes
+// q and the credible bounds in the same pass.
 // ---------------------------------------------------------------------------
 namespace {
 
-__global__ void real_to_complex_kernel(const double* __restrict__ d, long long n,
-                                       double2* __restrict__ out) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    out[i] = make_double2(d[i], 0.0);
+constexpr int kQdThreads = 512;
+constexpr long long kQdSegMax = 9216;               // rows per column segment (72 KB)
+constexpr int kQdMaxPairs = (int)((kQdSegMax / 2 + kQdThreads - 1) / kQdThreads);  // 9
+constexpr size_t kQdSmem = 216 * 1024;              // staging ring (+ barriers)
+constexpr int kQdMaxStages = 4;
+
+struct QdShape {
+  long long ldp = 0, cols = 0;
+  int rt = 0, nrt = 0;      // row tile (even) and tiles
+  int cb = 0, ns = 0;       // columns per stage, stages
+  int ncr = 0;              // column ranges
+};
+
+QdShape qd_shape(long long ldp, long long cols, int sms) {
+  QdShape q;
+  q.ldp = ldp;
+  q.cols = cols;
+  q.rt = (int)std::min(ldp, kQdSegMax);
+  q.nrt = (int)((ldp + q.rt - 1) / q.rt);
+  const size_t seg = (size_t)q.rt * sizeof(double);
+  q.cb = (int)std::max<size_t>(1, (size_t)(kQdSegMax * sizeof(double)) / seg);
+  q.ns = (int)std::min<size_t>(kQdMaxStages, (kQdSmem - 64) / (q.cb * seg));
+  q.ncr = (int)std::max<long long>(1, std::min<long long>(cols, std::max(1, sms / q.nrt)));
+  return q;
+}
+
+__global__ void __launch_bounds__(kQdThreads, 1)
+    qd_gemv_kernel(const double* __restrict__ Q, long long ldp, long long cols, int rt, int cb, int ns,
+                   const double* __restrict__ d, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char qsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(qsm);
+  double* ring = reinterpret_cast<double*>(qsm + 64);
+  const int tid = threadIdx.x;
+  const long long r0 = (long long)blockIdx.y * rt;
+  const int rlen = (int)min((long long)rt, ldp - r0);  // even
+  const long long cr = blockIdx.x, ncr = gridDim.x;
+  const long long c0 = cols * cr / ncr, c1 = cols * (cr + 1) / ncr;
+  const long long nchunks = (c1 - c0 + cb - 1) / cb;
+  const size_t seg = (size_t)rlen * sizeof(double);
+  auto issue = [&](long long k) {
+    const int s = (int)(k % ns);
+    const long long j0 = c0 + k * cb, j1 = min(c1, j0 + cb);
+    mbar_arrive_expect_tx(bar + s, (unsigned)(seg * (j1 - j0)));
+    for (long long j = j0; j < j1; ++j)
+      bulk_g2s(ring + ((size_t)s * cb + (j - j0)) * rt, Q + (size_t)j * ldp + r0, (unsigned)seg, bar + s,
+               policy_evict_first());
+  };
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) mbar_init(bar + s, 1);
+    fence_mbar_init();
+    for (long long k = 0; k < ns && k < nchunks; ++k) issue(k);
+  }
+  __syncthreads();
+  double2 acc[kQdMaxPairs];
+#pragma unroll
+  for (int k = 0; k < kQdMaxPairs; ++k) acc[k] = make_double2(0.0, 0.0);
+  for (long long k = 0; k < nchunks; ++k) {
+    const int s = (int)(k % ns);
+    mbar_wait(bar + s, (unsigned)(k / ns) & 1);
+    const long long j0 = c0 + k * cb, j1 = min(c1, j0 + cb);
+    for (long long j = j0; j < j1; ++j) {
+      const double dj = __ldg(d + j);
+      const double2* col = reinterpret_cast<const double2*>(ring + ((size_t)s * cb + (j - j0)) * rt);
+#pragma unroll
+      for (int kp = 0; kp < kQdMaxPairs; ++kp) {
+        const int p = tid + kQdThreads * kp;
+        if (2 * p < rlen) {
+          const double2 v = col[p];
+          acc[kp].x = fma(v.x, dj, acc[kp].x);
+          acc[kp].y = fma(v.y, dj, acc[kp].y);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0 && k + ns < nchunks) issue(k + ns);
+  }
+  double* out = partials + (size_t)cr * ldp + r0;
+#pragma unroll
+  for (int kp = 0; kp < kQdMaxPairs; ++kp) {
+    const int p = tid + kQdThreads * kp;
+    if (2 * p < rlen) reinterpret_cast<double2*>(out)[p] = acc[kp];
+  }
+}
+
+// q = sum over column ranges (in order) of the partials; credible bounds
+__global__ void qd_finish_kernel(const double* __restrict__ partials, long long ldp, int ncr, long long rows,
+                                 const double* __restrict__ gdiag, double z, double* __restrict__ q,
+                                 double* __restrict__ lo, double* __restrict__ hi) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < ncr; ++c) acc += partials[(size_t)c * ldp + r];
+    const double half = z * sqrt(fmax(gdiag[r], 0.0));
+    q[r] = acc;
+    lo[r] = acc - half;
+    hi[r] = acc + half;
+  }
 }
 
 __global__ void pad_columns_kernel(const double* __restrict__ Q, size_t ldq, long long rows,
@@ -659,17 +755,6 @@ __global__ void pad_columns_kernel(const double* __restrict__ Q, size_t ldq, lon
        e += (long long)gridDim.x * blockDim.x) {
     const long long c = e / ldp, r = e - c * ldp;
     out[e] = r < rows ? Q[(size_t)c * ldq + r] : 0.0;
-  }
-}
-
-__global__ void credible_kernel(const double* __restrict__ q, const double* __restrict__ gdiag,
-                                long long n, double z, double* __restrict__ lo,
-                                double* __restrict__ hi) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double half = z * sqrt(fmax(gdiag[i], 0.0));
-    lo[i] = q[i] - half;
-    hi[i] = q[i] + half;
   }
 }
 
@@ -710,24 +795,20 @@ struct QoIOperator {
   long long rows = 0, cols = 0, ldp = 0;  // Nq*Nt, Nd*Nt, rows padded to even
   double* Q = nullptr;                    // ldp x cols, column-major
   double* gdiag = nullptr;
-  double2* x = nullptr;                   // d as complex
-  double2* partials = nullptr;
-  unsigned* tickets = nullptr;
-  double* y = nullptr;                    // ldp reals (= ldp/2 complex)
+  double* partials = nullptr;             // qd.ncr x ldp
+  double* y = nullptr;                    // ldp
   double* lo = nullptr;
   double* hi = nullptr;
   double* stage = nullptr;                // host-pointer staging for d
   double* gpost = nullptr;                // full Gamma_post_q (form_Q only), m x m
   double* prior_cov = nullptr;            // Fq Gq* (form_Q only), m x m
-  GemvShape shape{};
+  QdShape qd{};
   void release() {
     cudaFree(gpost);
     cudaFree(prior_cov);
     cudaFree(Q);
     cudaFree(gdiag);
-    cudaFree(x);
     cudaFree(partials);
-    cudaFree(tickets);
     cudaFree(y);
     cudaFree(lo);
     cudaFree(hi);
@@ -763,13 +844,15 @@ ltb_status ltb_engine_set_phase3(ltb_engine* e, const double* Q, size_t ldq,
   op.rows = rows;
   op.cols = cols;
   op.ldp = rows + (rows & 1);
-  op.shape = gemv_shape((int)(op.ldp / 2), cols, 1, 0);
-  const int tiles = gemv_n_row_tiles(op.shape);
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    op.qd = qd_shape(op.ldp, cols, sms);
+  }
   ENG_CUDA(cudaMalloc(&op.Q, sizeof(double) * op.ldp * cols));
   ENG_CUDA(cudaMalloc(&op.gdiag, sizeof(double) * rows));
-  ENG_CUDA(cudaMalloc(&op.x, sizeof(double2) * cols));
-  ENG_CUDA(cudaMalloc(&op.partials, sizeof(double2) * gemv_n_partials(op.shape)));
-  ENG_CUDA(cudaMalloc(&op.tickets, sizeof(unsigned) * tiles));
+  ENG_CUDA(cudaMalloc(&op.partials, sizeof(double) * op.ldp * op.qd.ncr));
   ENG_CUDA(cudaMalloc(&op.y, sizeof(double) * op.ldp));
   ENG_CUDA(cudaMalloc(&op.lo, sizeof(double) * rows));
   ENG_CUDA(cudaMalloc(&op.hi, sizeof(double) * rows));
@@ -815,14 +898,16 @@ ltb_status ltb_engine_predict_qoi(const ltb_engine* e, ltb_scratch* s, const dou
     ENG_CUDA(cudaMemcpyAsync(op.stage, d, sizeof(double) * op.cols, cudaMemcpyHostToDevice, st));
     din = op.stage;
   }
-  real_to_complex_kernel<<<148 * 4, 256, 0, st>>>(din, op.cols, op.x);
+  const QdShape& qs = op.qd;
+  const size_t smem = 64 + (size_t)qs.ns * qs.cb * qs.rt * sizeof(double);
+  ENG_CUDA(cudaFuncSetAttribute(qd_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  qd_gemv_kernel<<<dim3((unsigned)qs.ncr, (unsigned)qs.nrt), kQdThreads, smem, st>>>(
+      op.Q, op.ldp, op.cols, qs.rt, qs.cb, qs.ns, din, op.partials);
   ENG_CUDA(cudaGetLastError());
-  ENG_CUDA(launch_gemv_n(op.shape, reinterpret_cast<const double2*>(op.Q), op.x, op.partials,
-                         reinterpret_cast<double2*>(op.y), op.tickets, st));
-  credible_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 4, (op.rows + 255) / 256)), 256, 0, st>>>(
-      op.y, op.gdiag, op.rows, z, op.lo, op.hi);
+  qd_finish_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 4, (op.rows + 255) / 256)), 256, 0, st>>>(
+      op.partials, op.ldp, qs.ncr, op.rows, op.gdiag, z, op.y, op.lo, op.hi);
   ENG_CUDA(cudaGetLastError());
-  count_launches(3);
+  count_launches(2);
   const cudaMemcpyKind k = ptr_kind == LTB_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   ENG_CUDA(cudaMemcpyAsync(q, op.y, sizeof(double) * op.rows, k, st));
   if (lo) ENG_CUDA(cudaMemcpyAsync(lo, op.lo, sizeof(double) * op.rows, k, st));

@@ -194,7 +194,9 @@ def test_predict_qoi_with_credible_intervals(ltb):
     and q -/+ z sqrt(max(diag, 0)); z = 1.96 at 0.95, normal quantile else;
     odd Nq*Nt (padding path) and ConfigError on a bad level."""
     rng = np.random.default_rng(8)
-    for nd, nq, nm, nt in [(3, 2, 5, 7), (4, 3, 6, 9), (64, 8, 16, 128)]:
+    # the last case has Nq*Nt = 9603 > 9216 rows: two row tiles per column
+    # segment in the Q d kernel, odd (padded) row count
+    for nd, nq, nm, nt in [(3, 2, 5, 7), (4, 3, 6, 9), (64, 8, 16, 128), (2, 97, 4, 99)]:
         g = ltb.MatvecPlan.generated(nd, nm, nt, seed=1, tag=ltb.KernelTag.Gstar)
         fq = ltb.MatvecPlan.generated(nq, nm, nt, seed=1, tag=ltb.KernelTag.Fq)
         eng = ltb.InferenceEngine(g, fq)
