@@ -170,7 +170,7 @@ def test_generated_factor_small_inversion_config(ltb):
     assert np.array_equal(qd.cpu().numpy(), res.q_map.values)
 
 
-@pytest.mark.parametrize("n,P", [(64, 1), (200, 2), (1000, 2), (3000, 3), (8192, 4), (777, 4), (5000, 7), (300, 6)])
+@pytest.mark.parametrize("n,P", [(64, 1), (200, 2), (1000, 2), (3000, 3), (8192, 4), (777, 4), (5000, 7), (300, 6), (20000, 8), (17000, 3)])
 def test_distributed_solve_emulated(ltb, n, P):
     """The P-rank distributed K^{-1} apply (row-cyclic factor, chain on rank 0,
     peer pushes) emulated by one launch on one GPU matches the oracle's TRSV
