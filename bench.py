@@ -271,7 +271,7 @@ def bench_online(ltb, torch, reps=20, cpu=True):
         g.apply_adjoint_raw(d, m, sg)
         fq.apply_raw(m, q, sq)
     gst, fqt = sg.stage_ms(), sq.stage_ms()
-    dh = d.cpu().numpy()
+    dh = d.cpu().pin_memory().numpy()  # pinned host input, as the e2e contract has it
     mh = torch.empty(nm * nt, dtype=torch.float64).pin_memory().numpy()
     qh = torch.empty(nq * nt, dtype=torch.float64).pin_memory().numpy()
     e2e = []
