@@ -43,6 +43,40 @@ def test_matvec_random_shapes(ltb, nd, nm, nt, seed):
     assert orc.rel_err(fd, op.apply_adjoint(d)) <= TOL
 
 
+def reg_shapes(seed, count):
+    rng = np.random.default_rng(seed)
+    return [(int(rng.integers(1, 24)), int(rng.integers(1, 3000)), int(rng.choice([64, 128, 256, 420, 512])),
+             int(rng.integers(0, 2**31))) for _ in range(count)]
+
+
+@pytest.mark.parametrize("nd,nm,nt,seed", reg_shapes(303, 12))
+def test_register_fft_random_shapes(ltb, nd, nm, nt, seed):
+    """The register two-pass transforms (2 N_t in {128, 256, 512, 840, 1024})
+    on random row counts, unit sizes and both pointer kinds."""
+    import torch
+    rng = np.random.default_rng(seed)
+    k = rng.standard_normal((nd, nm, nt))
+    plan = ltb.MatvecPlan(ltb.BlockToeplitzKernel(nd, nm, nt, data=k),
+                          unit_cols=int(rng.choice([0, 1, 7, 64])))
+    op = orc.OraclePlan(k)
+    m = rng.standard_normal(nm * nt)
+    d = rng.standard_normal(nd * nt)
+    s = ltb.MatvecPlan.Scratch(plan, stream=torch.cuda.current_stream())
+    if rng.integers(0, 2):
+        fm, fd = np.empty(nd * nt), np.empty(nm * nt)
+        plan.apply_raw(m, fm, s)
+        plan.apply_adjoint_raw(d, fd, s)
+    else:
+        fm_t = torch.empty(nd * nt, dtype=torch.float64, device="cuda")
+        fd_t = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
+        plan.apply_raw(torch.from_numpy(m).cuda(), fm_t, s)
+        plan.apply_adjoint_raw(torch.from_numpy(d).cuda(), fd_t, s)
+        torch.cuda.synchronize()
+        fm, fd = fm_t.cpu().numpy(), fd_t.cpu().numpy()
+    assert orc.rel_err(fm, op.apply(m)) <= TOL
+    assert orc.rel_err(fd, op.apply_adjoint(d)) <= TOL
+
+
 @pytest.mark.parametrize("nd,nm,nt,seed", shapes(202, 8, 9, 90, 40))
 def test_offline_random_shapes(ltb, nd, nm, nt, seed):
     rng = np.random.default_rng(seed)
