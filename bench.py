@@ -229,9 +229,121 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# parity of the timed outputs (checker; runs after the timed region)
+# ---------------------------------------------------------------------------
+def gemv_unit_cols(nd):
+    # csrc/ltb_gemv.cu: kUnitElems (2^18 complex values) / Nd columns per work unit
+    return max(1, (1 << 18) // nd)
+
+
+def sample_columns(n_local, nd):
+    uc = gemv_unit_cols(nd)
+    cand = [0, 1, uc - 1, uc, uc + 1, n_local // 2, n_local - 2, n_local - 1]
+    return sorted({c for c in cand if 0 <= c < n_local})
+
+
+def matvec_parity(torch, dist, sm, step, seed, nd, nt, m, d, d_out, m_out, world, rank):
+    """Checks the outputs of the LAST timed step against the oracle (the C
+    restatement pinned bit-for-bit to the reference build), at the full
+    workload size, mirroring tests/test_gpu_cascadia.py:
+      * F* d column-exact on sampled columns of every rank's shard (first,
+        last, GEMV work-unit boundaries) -- F* is separable in c;
+      * <F m, d> == <m, F* d> over the full timed vectors (all ranks);
+      * F m with m supported on 3 columns per rank vs the oracle on exactly
+        those columns (one extra apply + all-reduce);
+      * a repeated step reproduces the timed outputs bit for bit."""
+    import numpy as np
+    from oracle import oracle as orc  # checker only
+    from paper_2504_16344_b200.dist import shard_range
+    nm_total = sm.nm_total
+    fm, ftd = d_out.clone(), m_out.clone()
+    dh = d.cpu().numpy()
+    ftd_h = ftd.cpu().numpy().reshape(sm.n_local, nt)
+    cols = sample_columns(sm.n_local, nd)
+    e_fstar = 0.0
+    for c in cols:
+        op = orc.OraclePlan(orc.gen_kernel(seed, nd, nm_total, nt, c0=sm.c0 + c, cols=1))
+        e_fstar = max(e_fstar, orc.rel_err(ftd_h[c], op.apply_adjoint(dh)))
+    # adjointness of the timed pair
+    dots = torch.tensor([float(torch.dot(m, ftd))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(dots)
+    fmd = float(torch.dot(fm, d))
+    adj = abs(fmd - float(dots.item())) / float(torch.linalg.norm(fm) * torch.linalg.norm(d))
+    # column-supported F m
+    def sub_of(n_local):
+        return sorted({2 % n_local, min(gemv_unit_cols(nd) + 3, n_local - 1), n_local - 3 if n_local > 3 else 0})
+
+    def vals(gc):
+        return np.random.default_rng(gc).uniform(-1, 1, nt)
+
+    msub = torch.zeros_like(m).view(sm.n_local, nt)
+    for c in sub_of(sm.n_local):
+        msub[c] = torch.from_numpy(vals(sm.c0 + c)).cuda()
+    dchk = torch.empty_like(d_out)
+    sm.apply(msub.view(-1), dchk)
+    torch.cuda.synchronize()
+    gcols = []
+    for r in range(world):
+        c0, c1 = shard_range(nm_total, world, r)
+        gcols += [c0 + c for c in sub_of(c1 - c0)]
+    e_fm = None
+    if rank == 0:
+        ker = np.concatenate([orc.gen_kernel(seed, nd, nm_total, nt, c0=g, cols=1) for g in gcols], axis=1)
+        ref = orc.OraclePlan(ker).apply(np.concatenate([vals(g) for g in gcols]))
+        e_fm = orc.rel_err(dchk.cpu().numpy(), ref)
+    # repeat: bit-identical
+    step()
+    torch.cuda.synchronize()
+    same = torch.tensor([1.0 if (torch.equal(fm, d_out) and torch.equal(ftd, m_out)) else 0.0],
+                        dtype=torch.float64, device="cuda")
+    ef = torch.tensor([e_fstar], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        dist.all_reduce(ef, op=dist.ReduceOp.MAX)
+    if rank != 0:
+        return None
+    worst = max(float(ef.item()), e_fm, adj)
+    return {"max_rel_err": worst, "tol": 1e-12, "ok": bool(worst <= 1e-12 and same.item() == 1.0),
+            "fstar_cols_checked": len(cols) * world, "fstar_max_rel_err": float(ef.item()),
+            "fm_cols_supported": len(gcols), "fm_rel_err": e_fm, "adjointness": adj,
+            "adjointness_terms": [fmd, float(dots.item())],
+            "repeat_bit_identical": bool(same.item() == 1.0),
+            "oracle": "oracle/ltb_oracle.c (C restatement, bit-identical to the reference build on the golden vectors)",
+            "what": "timed outputs of the last step: F* d on sampled columns (incl. GEMV unit boundaries), "
+                    "<Fm,d> vs <m,F*d> full vectors, F m on column-supported m, bitwise repeat"}
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def bench_online(ltb, torch, reps=20, cpu=True):
+def online_parity(eng, nd, nm, nt, nq, seed, prior, d_dev, m_dev, q_dev):
+    """Checker for the config-2 timed outputs (after the timed region), full
+    vectors: y = K^{-1} d (oracle substitution with the device-made factor),
+    m_map = G* y (oracle plan of the prior-premultiplied generated kernel --
+    Gamma_x couples columns, so the whole G is rebuilt on the host), and
+    q = F_q m_map."""
+    from oracle import oracle as orc  # checker only
+    t0 = time.time()
+    dh = d_dev.cpu().numpy()
+    L = eng.chol_lower()
+    y = orc.solve_k(L, dh)
+    del L
+    e_y = orc.rel_err(eng.solve_k_inplace(dh.copy()), y)
+    g = orc.prior_premultiply(orc.gen_kernel(seed, nd, nm, nt, stream=1), *prior)
+    m_ref = orc.OraclePlan(g).apply_adjoint(y)
+    del g
+    q_ref = orc.OraclePlan(orc.gen_kernel(seed, nq, nm, nt, stream=2)).apply(m_ref)
+    e_m = orc.rel_err(m_dev.cpu().numpy(), m_ref)
+    e_q = orc.rel_err(q_dev.cpu().numpy(), q_ref)
+    worst = max(e_y, e_m, e_q)
+    return {"max_rel_err": worst, "tol": 1e-12, "ok": bool(worst <= 1e-12), "solve_k": e_y, "m_map": e_m,
+            "q": e_q, "check_s": time.time() - t0,
+            "what": "full vectors of the last timed infer + forecast vs the oracle (device-made Cholesky "
+                    "factor, host-rebuilt prior-premultiplied G, F_q)"}
+
+
+def bench_online(ltb, torch, reps=20, cpu=True, parity=True):
     """BASELINE config 2: posterior mean + forecast latency (device time)."""
     nd, nm, nt, seed = WORKLOADS["small"]
     nq = 8
@@ -254,6 +366,7 @@ def bench_online(ltb, torch, reps=20, cpu=True):
     for _ in range(3):
         eng.infer_raw(d, m, q)
     dev = sorted(eng.infer_raw(d, m, q) for _ in range(reps))
+    m_timed, q_timed = m.clone(), q.clone()
     # stage breakdown: K^{-1} alone (wall, includes one sync), G* and F_q alone
     y = d.clone()
     solve = []
@@ -296,6 +409,7 @@ def bench_online(ltb, torch, reps=20, cpu=True):
            "predict_qoi_ms": pq[len(pq) // 2] * 1e3,
            "paper_online_s": 0.2,
            "cpu_reference": cpu_reference_online(eng, nd, nm, nt, nq, seed, d) if cpu else None,
+           "parity": online_parity(eng, nd, nm, nt, nq, seed, prior, d, m_timed, q_timed) if parity else None,
            "offline": {"form_k_ms": fk_ms, "form_k_tflops": n * n * nm / (fk_ms * 1e-3) / 1e12,
                        "form_k_flops": n * n * nm,
                        "factorize_ms": fz_ms, "factorize_tflops": n ** 3 / 3 / (fz_ms * 1e-3) / 1e12,
@@ -307,7 +421,43 @@ def bench_online(ltb, torch, reps=20, cpu=True):
     return out
 
 
-def bench_online_dist(ltb, torch, dist, rank, world, reps=5):
+def online_dist_parity(torch, dist, m, d, nd, nm, nt, seed, world, rank):
+    """Checker for the config-5 timed outputs (after the timed region):
+    m_map = G* K^{-1} d on 3 sampled columns of every rank's shard vs the
+    oracle -- K^{-1} d by the oracle's blocked multi-threaded substitution
+    with the same synthetic factor (n = 252,000, rank 0's host cores), G* by
+    the oracle plan of each single generated column (G* is separable in c)."""
+    from oracle import oracle as orc  # checker only
+    from paper_2504_16344_b200.dist import shard_range
+
+    def picks(n_local):
+        return sorted({0, n_local // 2, n_local - 1})
+
+    c0, c1 = shard_range(nm, world, rank)
+    mine = m.view(c1 - c0, nt)[picks(c1 - c0)].contiguous()
+    got = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(got, mine)
+    out = None
+    if rank == 0:
+        t0 = time.time()
+        y = orc.solve_k_gen(seed, d.cpu().numpy())
+        t_solve = time.time() - t0
+        err, ncol = 0.0, 0
+        for r in range(world):
+            a, b = shard_range(nm, world, r)
+            for k, c in enumerate(picks(b - a)):
+                op = orc.OraclePlan(orc.gen_kernel(seed, nd, nm, nt, c0=a + c, cols=1, stream=3))
+                err = max(err, orc.rel_err(got[r][k].cpu().numpy(), op.apply_adjoint(y)))
+                ncol += 1
+        out = {"max_rel_err": err, "tol": 1e-12, "ok": bool(err <= 1e-12), "m_map_cols_checked": ncol,
+               "oracle_solve_s": t_solve, "oracle_threads": os.cpu_count(),
+               "what": "m_map columns of the last timed infer vs oracle G* column (K^{-1} d by the "
+                       "oracle's threaded substitution with the same synthetic factor, n = 252000)"}
+    dist.barrier()
+    return out
+
+
+def bench_online_dist(ltb, torch, dist, rank, world, reps=5, parity=True):
     """BASELINE config 5 (end-to-end online phase, Nd=600, Nt=420, Nq=21,
     n = 252,000): K^{-1} through the row-cyclic factor distributed over the
     ranks (254 GB packed: no single-GPU point), G* and F_q column-sharded
@@ -346,9 +496,10 @@ def bench_online_dist(ltb, torch, dist, rank, world, reps=5):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         lat.append(float(t.item()))
     lat.sort()
+    check = online_dist_parity(torch, dist, m, d, nd, nm, nt, seed, world, rank) if parity else None
     n = nd * nt
     byts = 2 * 8 * (n * (n + 1) // 2) + algorithmic_bytes(nd, nm, nt) + algorithmic_bytes(nq, nm, nt)
-    out = {"config": "end-to-end online phase (Nd=600, Nt=420, Nq=21, n=252000, Nm=16384 sharded, "
+    out = {"parity": check, "config": "end-to-end online phase (Nd=600, Nt=420, Nq=21, n=252000, Nm=16384 sharded, "
                      "synthetic factor row-cyclic over %d GPUs)" % world,
            "latency_ms": lat[len(lat) // 2], "latency_min_ms": lat[0],
            "bytes": byts, "achieved_gbs": byts / (lat[len(lat) // 2] * 1e-3) / 1e9,
@@ -369,6 +520,7 @@ def run_ours(args):
     # one dedicated stream for our kernels, the copies and the collectives
     torch.cuda.set_stream(torch.cuda.Stream())
     if world > 1:
+        nccl_env()
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nd, nm, nt, seed = WORKLOADS[args.workload]
     t_build = time.time()
@@ -420,6 +572,9 @@ def run_ours(args):
     ms = float(t.item())
     step_bytes = 2 * algorithmic_bytes(nd, nm, nt)
     value = world * step_bytes / (ms * 1e-3) / 1e9
+    parity = None
+    if not args.no_parity:
+        parity = matvec_parity(torch, dist, sm, step, seed, nd, nt, m, d, d_out, m_out, world, rank)
 
     # ---- e2e: the C-ABI host-pointer applies (ltb_apply / ltb_apply_adjoint
     # with pinned host buffers: the library copies in and out inside the
@@ -505,9 +660,9 @@ def run_ours(args):
     online = None
     if not args.no_online:
         if world == 1:
-            online = bench_online(ltb, torch, cpu=not args.no_cpu_baseline)
+            online = bench_online(ltb, torch, cpu=not args.no_cpu_baseline, parity=not args.no_parity)
         else:
-            online = bench_online_dist(ltb, torch, dist, rank, world)
+            online = bench_online_dist(ltb, torch, dist, rank, world, parity=not args.no_parity)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -536,6 +691,10 @@ def run_ours(args):
             "roofline": roof,
             "gpu_launches": int(launches),
             "clocks": clk,
+            "parity": parity,
+            "comm": {"backend": "nccl", "world_size": world,
+                     "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+                    if world > 1 else None,
             "online": online,
             "cpu_baseline": cpu,
             "plan_build_s": t_build,
@@ -544,6 +703,27 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def nccl_env():
+    """Communicator init lines (NCCL_DEBUG=INFO, subsystem INIT: nranks,
+    rings / NVLS) go to stderr, so stdout stays the one JSON line."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
+def relaunch(n):
+    """`python bench.py --gpus N` without a launcher: re-exec under
+    torch.distributed.run, one rank per GPU (rank 0 prints the line)."""
+    import socket
+    nccl_env()
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -555,8 +735,16 @@ def main():
     ap.add_argument("--workload", default="cascadia", choices=sorted(WORKLOADS))
     ap.add_argument("--no-online", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle checks")
     ap.add_argument("--cpu-sample-cols", type=int, default=2048)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d (launch one rank per GPU)" % (args.gpus, world),
+              file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

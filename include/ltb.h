@@ -64,6 +64,8 @@ typedef enum { LTB_TIME_MAJOR_BLOCKS = 0, LTB_SPACE_MAJOR_ROWS = 1 } ltb_layout;
 typedef struct ltb_plan ltb_plan;
 typedef struct ltb_scratch ltb_scratch;
 typedef struct ltb_engine ltb_engine;
+typedef struct ltb_splan ltb_splan;       /* MatvecPlan sharded over GPUs */
+typedef struct ltb_sscratch ltb_sscratch; /* its Scratch */
 
 typedef struct {
   int device;    /* CUDA ordinal; -1 = current device */
@@ -164,6 +166,41 @@ ltb_status ltb_apply_series(const ltb_plan* plan, ltb_scratch* s, const double* 
 ltb_status ltb_apply_adjoint_series(const ltb_plan* plan, ltb_scratch* s, const double* in,
                                     int n_rows, int n_time, int layout, double* out,
                                     int ptr_kind);
+
+/* ---- MatvecPlan sharded over the GPUs of one process ----
+ * The same MatvecPlan (fft_matvec.hpp:29-78) with its N_m columns cut into
+ * ndev contiguous ranges, shard k on device devs[k] (devices may repeat).
+ * F m: each shard applies its columns, the home device devs[0] sums the
+ * N_d x N_t partials in shard order (one kernel reading the peers' buffers
+ * over NVLink); F* d: d reaches every shard, each writes its columns of m.
+ * ltb_apply_sharded / ltb_apply_adjoint_sharded have the semantics of
+ * ltb_apply / ltb_apply_adjoint (= apply_raw / apply_adjoint_raw,
+ * fft_matvec.cpp:139-217): host pointers synchronous; device pointers on the
+ * home device, asynchronous on the scratch's home stream.  A multi-GPU
+ * replacement for the single-device plan behind the C++ drop-in
+ * (cpp/fft_matvec_b200.cpp selects it with LTB_DEVICES=0,1,...). */
+ltb_status ltb_plan_create_sharded(const double* kernel_rck, int rows, int cols, int nt, int tag,
+                                   int ndev, const int* devs, const ltb_opts* opts, ltb_splan** out);
+ltb_status ltb_plan_create_generated_sharded(int rows, int cols, int nt, int tag, uint64_t seed,
+                                             uint64_t stream, int ndev, const int* devs,
+                                             const ltb_opts* opts, ltb_splan** out);
+ltb_status ltb_splan_destroy(ltb_splan* plan);
+ltb_status ltb_splan_dims(const ltb_splan* plan, int* rows_out, int* n_cols, int* n_time,
+                          int* n_shards);
+/* shard k: device, column range [c0, c1), peer = 1 if the home device reads it over P2P */
+ltb_status ltb_splan_shard(const ltb_splan* plan, int k, int* device, long long* c0,
+                           long long* c1, int* peer);
+ltb_status ltb_splan_kernel_hat_sqnorm(const ltb_splan* plan, double* out);
+/* home_stream: cudaStream_t on devs[0] for shard 0 (NULL: private); the
+ * other shards get private streams on their devices */
+ltb_status ltb_sscratch_create(const ltb_splan* plan, void* home_stream, ltb_sscratch** out);
+ltb_status ltb_sscratch_destroy(ltb_sscratch* s);
+ltb_status ltb_sscratch_sync(ltb_sscratch* s);
+void* ltb_sscratch_stream(ltb_sscratch* s);
+ltb_status ltb_apply_sharded(const ltb_splan* plan, ltb_sscratch* s, const double* in, double* out,
+                             int ptr_kind);
+ltb_status ltb_apply_adjoint_sharded(const ltb_splan* plan, ltb_sscratch* s, const double* in,
+                                     double* out, int ptr_kind);
 
 /* ---- dense_apply (fft_matvec.hpp:80-87, fft_matvec.cpp:267-315) ----
  * FFT-free time-domain block-Toeplitz product (the reference's test oracle,

@@ -6,6 +6,7 @@
  * rounded IEEE operation, in the same order as the reference loops it
  * restates.  Reference paths are relative to /root/reference/proj.
  */
+#define _POSIX_C_SOURCE 200809L /* pthread barriers under -std=c11 */
 #include "ltb_oracle.h"
 
 #include <math.h>
@@ -492,6 +493,109 @@ void orc_solve_k_gen(uint64_t seed, int n, double* y) {
     y[j] = acc / col[j];
   }
   free(col);
+}
+
+/* The same two substitutions for the synthetic factor at config-5 scale
+ * (n = 252,000: 3.2e10 regenerated entries per sweep), blocked by 256
+ * columns with the off-diagonal updates split over `threads` POSIX threads.
+ * Forward: y_J = L_JJ^{-1} y_J (one thread), then y_I -= L_IJ y_J for every
+ * row below (rows split over the threads).  Transposed: every thread sums
+ * its rows' share L_IJ^T x_I into a private partial, the partials are added
+ * in thread order (deterministic), then x_J = L_JJ^{-T} (y_J - sum).  Same
+ * algebra as orc_solve_k_gen / bayes_engine.cpp:236-240; only the summation
+ * order of the off-diagonal products differs.  Checker for the distributed
+ * K^{-1} at full size (bench config 5, tests/dist_online_check.py). */
+#include <pthread.h>
+
+#define ORC_SB 256
+
+typedef struct {
+  uint64_t key; /* splitmix64(seed ^ splitmix64(stream * ...)) of the factor stream */
+  double offs;  /* 0.5 / sqrt(n) */
+  int n, threads;
+  double* y;
+  double* part; /* threads x ORC_SB */
+  pthread_barrier_t* bar;
+} orc_solve_ctx;
+
+typedef struct {
+  orc_solve_ctx* c;
+  int t;
+} orc_solve_arg;
+
+/* orc_gen_factor_entry for j <= i with the stream key hoisted (bit-identical) */
+static inline double fac_entry(const orc_solve_ctx* c, long i, long j) {
+  const uint64_t h = splitmix64(c->key ^ (((uint64_t)i * (uint64_t)c->n + (uint64_t)j) * 0xC2B2AE3D27D4EB4Full));
+  const double u = 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
+  return i == j ? 1.0 + 0.5 * (u + 1.0) : u * c->offs;
+}
+
+static void* orc_solve_worker(void* p) {
+  orc_solve_arg* a = (orc_solve_arg*)p;
+  orc_solve_ctx* c = a->c;
+  const int n = c->n, t = a->t, T = c->threads;
+  double* y = c->y;
+  for (int jb = 0; jb < n; jb += ORC_SB) { /* forward sweep */
+    const int je = jb + ORC_SB < n ? jb + ORC_SB : n;
+    if (t == 0)
+      for (int j = jb; j < je; ++j) {
+        y[j] = y[j] / fac_entry(c, j, j);
+        const double yj = y[j];
+        for (int i = j + 1; i < je; ++i) y[i] -= fac_entry(c, i, j) * yj;
+      }
+    pthread_barrier_wait(c->bar);
+    const long rows = n - je, i0 = je + rows * t / T, i1 = je + rows * (t + 1) / T;
+    for (long i = i0; i < i1; ++i) {
+      double acc = 0.0;
+      for (int j = jb; j < je; ++j) acc += fac_entry(c, i, j) * y[j];
+      y[i] -= acc;
+    }
+    pthread_barrier_wait(c->bar);
+  }
+  const int nblk = (n + ORC_SB - 1) / ORC_SB;
+  for (int b = nblk - 1; b >= 0; --b) { /* transposed sweep */
+    const int jb = b * ORC_SB, je = jb + ORC_SB < n ? jb + ORC_SB : n;
+    double* part = c->part + (size_t)t * ORC_SB;
+    for (int j = 0; j < ORC_SB; ++j) part[j] = 0.0;
+    const long rows = n - je, i0 = je + rows * t / T, i1 = je + rows * (t + 1) / T;
+    for (long i = i0; i < i1; ++i) {
+      const double xi = y[i];
+      for (int j = jb; j < je; ++j) part[j - jb] += fac_entry(c, i, j) * xi;
+    }
+    pthread_barrier_wait(c->bar);
+    if (t == 0)
+      for (int j = je - 1; j >= jb; --j) {
+        double s = 0.0;
+        for (int q = 0; q < T; ++q) s += c->part[(size_t)q * ORC_SB + (j - jb)];
+        double acc = y[j] - s;
+        for (int i = j + 1; i < je; ++i) acc -= fac_entry(c, i, j) * y[i];
+        y[j] = acc / fac_entry(c, j, j);
+      }
+    pthread_barrier_wait(c->bar);
+  }
+  return NULL;
+}
+
+int orc_solve_k_gen_mt(uint64_t seed, int n, double* y, int threads) {
+  if (n < 1) return 0;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_barrier_t bar;
+  pthread_barrier_init(&bar, NULL, (unsigned)threads);
+  orc_solve_ctx c = {splitmix64(seed ^ splitmix64(0x4C4Full * 0xD1B54A32D192ED03ull)), 0.5 / sqrt((double)n), n,
+                     threads, y, (double*)malloc(sizeof(double) * ORC_SB * (size_t)threads), &bar};
+  orc_solve_arg args[256];
+  pthread_t tid[256];
+  for (int t = 0; t < threads; ++t) {
+    args[t].c = &c;
+    args[t].t = t;
+    if (t > 0) pthread_create(&tid[t], NULL, orc_solve_worker, &args[t]);
+  }
+  orc_solve_worker(&args[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+  pthread_barrier_destroy(&bar);
+  free(c.part);
+  return 0;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -99,6 +99,8 @@ void orc_trsv_lower_t(const double* L, int n, size_t ld, double* y);
 void orc_solve_k(const double* L, int n, size_t ld, double* y);
 /* same, factor regenerated on the fly from orc_gen_factor_entry */
 void orc_solve_k_gen(uint64_t seed, int n, double* y);
+/* same, blocked and split over `threads` POSIX threads (config-5 scale) */
+int orc_solve_k_gen_mt(uint64_t seed, int n, double* y, int threads);
 
 /* ---- prior (prior.cpp:9-39,45-48,82-92,108-134) ---- */
 /* Gamma_x = A_x^{-2}, A_x = delta I - gamma L (Neumann); premultiply each

@@ -64,6 +64,7 @@ def lib():
         L.orc_trsv_lower_t.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
         L.orc_solve_k.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
         L.orc_solve_k_gen.argtypes = [C.c_uint64, C.c_int, _dp]
+        L.orc_solve_k_gen_mt.argtypes = [C.c_uint64, C.c_int, _dp, C.c_int]
         L.orc_prior_premultiply.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double,
                                             C.c_double, C.c_double, _dp]
         L.orc_prior_apply_precision.argtypes = [_dp, C.c_int, C.c_int, C.c_double,
@@ -230,9 +231,16 @@ def solve_k(L, y):
     return y
 
 
-def solve_k_gen(seed, y):
+def solve_k_gen(seed, y, threads=None):
+    """K^{-1} y with the synthetic factor; threads > 1 (default: all host
+    cores for n >= 20000) runs the blocked multi-threaded sweeps."""
     y = np.array(y, dtype=np.float64, copy=True)
-    lib().orc_solve_k_gen(seed, y.size, _ptr(y))
+    if threads is None:
+        threads = (os.cpu_count() or 1) if y.size >= 20000 else 1
+    if threads > 1:
+        lib().orc_solve_k_gen_mt(seed, y.size, _ptr(y), int(threads))
+    else:
+        lib().orc_solve_k_gen(seed, y.size, _ptr(y))
     return y
 
 

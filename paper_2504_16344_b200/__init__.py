@@ -9,7 +9,7 @@ from ._lib import build, kernel_launches, last_error, load  # noqa: F401
 from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, ConfigError,  # noqa: F401
                      CudaError, IoError,
                      DimensionError, KernelTag, Layout, LayoutError, LtbError, MatvecPlan,
-                     NumericalError, ObsSeries, QoISeries, SpaceTimeField, StateError,
+                     NumericalError, ObsSeries, QoISeries, ShardedMatvecPlan, SpaceTimeField, StateError,
                      algorithmic_bytes, dense_apply, reindex)
 from .engine import InferenceEngine, MapResult, QoIPrediction, normal_quantile  # noqa: F401
 from .artifacts import (Manifest, fnv1a64_file, infer_from_artifacts, read_manifest, read_series,  # noqa: F401

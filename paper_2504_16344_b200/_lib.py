@@ -79,6 +79,21 @@ SIGNATURES = {
     "ltb_engine_load_factor_dnsm": ([_vp, C.c_char_p], C.c_int),
     "ltb_engine_load_phase3_dnsm": ([_vp, C.c_char_p, C.c_char_p], C.c_int),
     "ltb_engine_infer_and_forecast": ([_vp, _vp, _vp, _vp, _vp, _dp, C.c_int], C.c_int),
+    "ltb_plan_create_sharded": ([_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), _vp,
+                                 C.POINTER(_vp)], C.c_int),
+    "ltb_plan_create_generated_sharded": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                           C.POINTER(C.c_int), _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_splan_destroy": ([_vp], C.c_int),
+    "ltb_splan_dims": ([_vp] + [C.POINTER(C.c_int)] * 4, C.c_int),
+    "ltb_splan_shard": ([_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                         C.POINTER(C.c_int)], C.c_int),
+    "ltb_splan_kernel_hat_sqnorm": ([_vp, _dp], C.c_int),
+    "ltb_sscratch_create": ([_vp, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_sscratch_destroy": ([_vp], C.c_int),
+    "ltb_sscratch_sync": ([_vp], C.c_int),
+    "ltb_sscratch_stream": ([_vp], _vp),
+    "ltb_apply_sharded": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_apply_adjoint_sharded": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
 }
 
 _lib = None

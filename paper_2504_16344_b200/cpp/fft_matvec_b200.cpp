@@ -18,9 +18,18 @@
 //   * kernel_hat_sqnorm (:124-137); dense_apply with CapacityError (:267-315).
 // CUDA failures surface as NumericalError with the driver's message (the
 // reference taxonomy has no device errors).
+//
+// Multi-GPU: with LTB_DEVICES=0,1,... (two or more ordinals, repeats allowed)
+// every plan is built sharded over those GPUs by column ranges
+// (ltb_plan_create_sharded: F m sums the shards' partial outputs on the
+// first device over NVLink, F* d hands d to every shard) -- same interface,
+// same results to rounding, so the engine's four plans (bayes_engine.cpp:
+// 110-113) and every other caller shard without a code change.
 #include "ltibayes/fft_matvec.hpp"
 
+#include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "ltb.h"
 
@@ -43,6 +52,24 @@ inline void check(ltb_status st, const char* where) {
   if (st != LTB_OK) raise_status(st, where);
 }
 
+// LTB_DEVICES="0,1,2,3" -> {0,1,2,3}; fewer than two entries: single device
+std::vector<int> shard_devices() {
+  std::vector<int> devs;
+  const char* env = std::getenv("LTB_DEVICES");
+  if (!env) return devs;
+  std::string s(env);
+  size_t pos = 0;
+  while (pos < s.size()) {
+    const size_t end = s.find(',', pos);
+    const std::string tok = s.substr(pos, end == std::string::npos ? std::string::npos : end - pos);
+    if (!tok.empty()) devs.push_back(std::stoi(tok));
+    if (end == std::string::npos) break;
+    pos = end + 1;
+  }
+  if (devs.size() < 2) devs.clear();
+  return devs;
+}
+
 void check_series(const BlockSeries& v, const char* what) {
   v.check_consistent(what);
   if (v.layout != Layout::SpaceMajorRows) {
@@ -54,32 +81,46 @@ void check_series(const BlockSeries& v, const char* what) {
 }  // namespace
 
 struct MatvecPlan::Impl {
-  ltb_plan* plan = nullptr;
+  ltb_plan* plan = nullptr;      // single device
+  ltb_splan* splan = nullptr;    // sharded over LTB_DEVICES
   int rows = 0, cols = 0, nt = 0;
   KernelTag tag = KernelTag::F;
   ~Impl() {
     if (plan) ltb_plan_destroy(plan);
+    if (splan) ltb_splan_destroy(splan);
   }
 };
 
 struct MatvecPlan::Scratch::Impl {
   ltb_scratch* s = nullptr;
+  ltb_sscratch* ss = nullptr;
   ~Impl() {
     if (s) ltb_scratch_destroy(s);
+    if (ss) ltb_sscratch_destroy(ss);
   }
 };
 
 MatvecPlan::Scratch::Scratch(const MatvecPlan& plan) : impl_(std::make_unique<Impl>()) {
-  check(ltb_scratch_create(plan.impl_->plan, nullptr, &impl_->s), "MatvecPlan::Scratch");
+  if (plan.impl_->splan)
+    check(ltb_sscratch_create(plan.impl_->splan, nullptr, &impl_->ss), "MatvecPlan::Scratch");
+  else
+    check(ltb_scratch_create(plan.impl_->plan, nullptr, &impl_->s), "MatvecPlan::Scratch");
 }
 MatvecPlan::Scratch::~Scratch() = default;
 MatvecPlan::Scratch::Scratch(Scratch&&) noexcept = default;
 
 MatvecPlan::MatvecPlan(const BlockToeplitzKernel& kernel) : impl_(std::make_unique<Impl>()) {
   kernel.check_consistent("MatvecPlan");
-  check(ltb_plan_create(kernel.data.data(), kernel.rows_out, kernel.n_cols, kernel.n_time,
-                        static_cast<int>(kernel.tag), LTB_PTR_HOST, nullptr, &impl_->plan),
-        "MatvecPlan");
+  const std::vector<int> devs = shard_devices();
+  if (!devs.empty() && kernel.n_cols >= static_cast<int>(devs.size()))
+    check(ltb_plan_create_sharded(kernel.data.data(), kernel.rows_out, kernel.n_cols, kernel.n_time,
+                                  static_cast<int>(kernel.tag), static_cast<int>(devs.size()), devs.data(),
+                                  nullptr, &impl_->splan),
+          "MatvecPlan");
+  else
+    check(ltb_plan_create(kernel.data.data(), kernel.rows_out, kernel.n_cols, kernel.n_time,
+                          static_cast<int>(kernel.tag), LTB_PTR_HOST, nullptr, &impl_->plan),
+          "MatvecPlan");
   impl_->rows = kernel.rows_out;
   impl_->cols = kernel.n_cols;
   impl_->nt = kernel.n_time;
@@ -99,17 +140,27 @@ KernelTag MatvecPlan::tag() const { return impl_->tag; }
 
 double MatvecPlan::kernel_hat_sqnorm() const {
   double out = 0;
-  check(ltb_kernel_hat_sqnorm(impl_->plan, &out), "MatvecPlan::kernel_hat_sqnorm");
+  if (impl_->splan)
+    check(ltb_splan_kernel_hat_sqnorm(impl_->splan, &out), "MatvecPlan::kernel_hat_sqnorm");
+  else
+    check(ltb_kernel_hat_sqnorm(impl_->plan, &out), "MatvecPlan::kernel_hat_sqnorm");
   return out;
 }
 
 void MatvecPlan::apply_raw(const double* in, double* out, Scratch& scratch) const {
-  check(ltb_apply(impl_->plan, scratch.impl_->s, in, out, LTB_PTR_HOST), "MatvecPlan::apply_raw");
+  if (impl_->splan)
+    check(ltb_apply_sharded(impl_->splan, scratch.impl_->ss, in, out, LTB_PTR_HOST), "MatvecPlan::apply_raw");
+  else
+    check(ltb_apply(impl_->plan, scratch.impl_->s, in, out, LTB_PTR_HOST), "MatvecPlan::apply_raw");
 }
 
 void MatvecPlan::apply_adjoint_raw(const double* in, double* out, Scratch& scratch) const {
-  check(ltb_apply_adjoint(impl_->plan, scratch.impl_->s, in, out, LTB_PTR_HOST),
-        "MatvecPlan::apply_adjoint_raw");
+  if (impl_->splan)
+    check(ltb_apply_adjoint_sharded(impl_->splan, scratch.impl_->ss, in, out, LTB_PTR_HOST),
+          "MatvecPlan::apply_adjoint_raw");
+  else
+    check(ltb_apply_adjoint(impl_->plan, scratch.impl_->s, in, out, LTB_PTR_HOST),
+          "MatvecPlan::apply_adjoint_raw");
 }
 
 ObsSeries MatvecPlan::apply(const SpaceTimeField& m) const {

@@ -384,36 +384,53 @@ ltb_status adjoint_chunks_to_host(const ltb_plan* p, ltb_scratch* s, const doubl
   return LTB_OK;
 }
 
+// d_dev = F m of a HOST m, enqueued on s->stream (nothing synchronized):
+// the pipelined column chunks above 16 MB of field, else one copy + the
+// device path.  The copy stream is joined back into the compute stream.
+ltb_status fm_host_enqueue(const ltb_plan* p, ltb_scratch* s, const double* in, double* d_dev) {
+  const cudaStream_t cs = s->stream;
+  const long long cols = p->cols, nt = p->nt;
+  ltb_status st = ensure_stage(s, (size_t)std::max(cols, (long long)p->rows) * nt,
+                               (size_t)std::max(cols, (long long)p->rows) * nt);
+  if (st != LTB_OK) return st;
+  if (s->timing || (size_t)cols * nt * sizeof(double) < kPipeMinBytes) {
+    LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in, in, sizeof(double) * cols * nt, cudaMemcpyHostToDevice, cs));
+    return apply_dev(p, s, s->stage_in, d_dev);
+  }
+  if ((st = pipe_setup(s)) != LTB_OK) return st;
+  const cudaStream_t xs = s->copy_stream;
+  long long b[kPipeMaxChunks + 1];
+  const int K = pipe_bounds(p, true, b);
+  // order the copy stream after everything already queued on the compute stream
+  LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[16], cs));
+  LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[16], 0));
+  for (int k = 0; k < K; ++k) {
+    const long long c0 = b[k], nc = b[k + 1] - b[k];
+    LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in + c0 * nt, in + c0 * nt, sizeof(double) * nc * nt,
+                                 cudaMemcpyHostToDevice, xs));
+    LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], xs));
+  }
+  for (int k = 0; k < K; ++k) {
+    const long long c0 = b[k], nc = b[k + 1] - b[k];
+    LTB_CUDA_TRY(cudaStreamWaitEvent(cs, s->pipe_ev[k], 0));
+    RfftSrc src{s->stage_in + c0 * nt, 0, 1, 0, 0};
+    LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, nc, s->xhat + c0, cols, cs), 1);
+    LTB_LAUNCH(launch_gemv_n(gemv_window(p->shape, c0, nc, k > 0), p->fhat, s->xhat, s->partials, s->dhat,
+                             s->tickets, cs),
+               1);
+  }
+  LTB_LAUNCH(launch_irfft_rows(p->fft, s->dhat, p->rows, 0, 1, p->nt, p->rows, 1.0 / p->npad, d_dev, cs), 1);
+  return LTB_OK;
+}
+
 ltb_status apply_host_pipelined(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
                                 bool adjoint) {
   ltb_status st = pipe_setup(s);
   if (st != LTB_OK) return st;
   const cudaStream_t cs = s->stream, xs = s->copy_stream;
-  const long long cols = p->cols, nt = p->nt;
-  long long b[kPipeMaxChunks + 1];
-  const int K = pipe_bounds(p, !adjoint, b);
-  // order the copy stream after everything already queued on the compute stream
-  LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[16], cs));
-  LTB_CUDA_TRY(cudaStreamWaitEvent(xs, s->pipe_ev[16], 0));
+  const long long nt = p->nt;
   if (!adjoint) {
-    for (int k = 0; k < K; ++k) {
-      const long long c0 = b[k], nc = b[k + 1] - b[k];
-      LTB_CUDA_TRY(cudaMemcpyAsync(s->stage_in + c0 * nt, in + c0 * nt, sizeof(double) * nc * nt,
-                                   cudaMemcpyHostToDevice, xs));
-      LTB_CUDA_TRY(cudaEventRecord(s->pipe_ev[k], xs));
-    }
-    for (int k = 0; k < K; ++k) {
-      const long long c0 = b[k], nc = b[k + 1] - b[k];
-      LTB_CUDA_TRY(cudaStreamWaitEvent(cs, s->pipe_ev[k], 0));
-      RfftSrc src{s->stage_in + c0 * nt, 0, 1, 0, 0};
-      LTB_LAUNCH(launch_rfft_rows(p->fft, src, p->nt, nc, s->xhat + c0, cols, cs), 1);
-      LTB_LAUNCH(launch_gemv_n(gemv_window(p->shape, c0, nc, k > 0), p->fhat, s->xhat, s->partials, s->dhat,
-                               s->tickets, cs),
-                 1);
-    }
-    LTB_LAUNCH(launch_irfft_rows(p->fft, s->dhat, p->rows, 0, 1, p->nt, p->rows, 1.0 / p->npad, s->stage_out,
-                                 cs),
-               1);
+    if ((st = fm_host_enqueue(p, s, in, s->stage_out)) != LTB_OK) return st;
     LTB_CUDA_TRY(cudaMemcpyAsync(out, s->stage_out, sizeof(double) * p->rows * nt, cudaMemcpyDeviceToHost, cs));
     LTB_CUDA_TRY(cudaStreamSynchronize(cs));
     LTB_CUDA_TRY(cudaStreamSynchronize(xs));
@@ -786,6 +803,24 @@ ltb_status apply_device(const ltb_plan* p, ltb_scratch* s, const double* in, dou
   return adjoint ? apply_adjoint_dev(p, s, in, out) : apply_dev(p, s, in, out);
 }
 cudaStream_t scratch_stream(ltb_scratch* s) { return s->stream; }
+ltb_status fm_from_host(const ltb_plan* p, ltb_scratch* s, const double* in_host, double* d_dev) {
+  if (!p || !s || s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");
+  return fm_host_enqueue(p, s, in_host, d_dev);
+}
+ltb_status fstar_to_host(const ltb_plan* p, ltb_scratch* s, const double* d_dev, double* m_host) {
+  if (!p || !s || s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");
+  ltb_status st = ensure_stage(s, (size_t)std::max(p->cols, p->rows) * p->nt,
+                               (size_t)std::max(p->cols, p->rows) * p->nt);
+  if (st != LTB_OK) return st;
+  return adjoint_to_host(p, s, d_dev, s->stage_out, m_host);
+}
+double* scratch_stage_in(ltb_scratch* s, size_t n) {
+  return ensure_stage(s, n, s->stage_out_n) == LTB_OK ? s->stage_in : nullptr;
+}
+double* scratch_stage_out(ltb_scratch* s, size_t n) {
+  return ensure_stage(s, s->stage_in_n, n) == LTB_OK ? s->stage_out : nullptr;
+}
+int scratch_device(const ltb_scratch* s) { return s->device; }
 int plan_device(const ltb_plan* p) { return p->device; }
 void plan_dims(const ltb_plan* p, int* rows, int* cols, int* nt) {
   *rows = p->rows;

@@ -98,7 +98,29 @@ struct ltb_engine {
   ltb_scratch* fq_scratch = nullptr;
   cudaStream_t fq_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // The reference's online calls are const and re-entrant (solve_k_inplace /
+  // infer_map are called from parallel_for workers, bayes_engine.cpp:252-256,
+  // 389).  Here they share the staging buffers, the TRSV hand-off buffers and
+  // the events, so every entry point holds this lock for its whole
+  // (synchronous) duration; recursive because infer_map -> infer_and_forecast.
+  std::recursive_mutex mu;
 };
+
+namespace {
+struct EngLock {
+  std::unique_lock<std::recursive_mutex> lk;
+  explicit EngLock(const ltb_engine* e) {
+    if (e) lk = std::unique_lock<std::recursive_mutex>(const_cast<ltb_engine*>(e)->mu);
+  }
+};
+// The persistent K^{-1} kernel needs every CTA resident at once and fills the
+// GPU: two of them (two engines, two streams) must never overlap on a device.
+// Held from the launch until the call has synchronized its stream.
+struct DevLock {
+  std::unique_lock<std::mutex> lk;
+  explicit DevLock(int dev) : lk(trsv_device_mutex(dev)) {}
+};
+}  // namespace
 
 void release_phase3(ltb_engine* e);  // Q d state (below)
 
@@ -221,7 +243,11 @@ ltb_status check_solve_status(const ltb_engine* e, cudaStream_t st) {
   ENG_CUDA(cudaMemcpyAsync(&h, e->factor.status, sizeof(int), cudaMemcpyDeviceToHost, st));
   ENG_CUDA(cudaStreamSynchronize(st));
   if (h) {
+    // re-arm for the next call: the error word and the grid-barrier words (a
+    // timed-out barrier leaves its arrival count behind)
     cudaMemsetAsync(e->factor.status, 0, sizeof(int), st);
+    cudaMemsetAsync(e->factor.gsync, 0, 2 * sizeof(unsigned), st);
+    cudaStreamSynchronize(st);
     return efail(LTB_CUDA, "solve_k: dependency wait timed out in the TRSV chain");
   }
   return LTB_OK;
@@ -253,6 +279,7 @@ ltb_status fq_scratch_for(ltb_engine* e, cudaStream_t st, ltb_scratch** out) {
 extern "C" {
 
 ltb_status ltb_engine_set_world(ltb_engine* e, int world, int rank) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "set_world: null engine");
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
     return efail(LTB_INVALID, "set_world: world=%d rank=%d (1 <= world <= %d)", world, rank, kMaxRanks);
@@ -263,6 +290,7 @@ ltb_status ltb_engine_set_world(ltb_engine* e, int world, int rank) {
 }
 
 ltb_status ltb_engine_ipc_handle(ltb_engine* e, void* out) {
+  EngLock lk_(e);
   if (!e || !out) return efail(LTB_INVALID, "ipc_handle: null argument");
   if (!e->factorized) return efail(LTB_STATE, "ipc_handle: set the factor first");
   Guard gd(e->device);
@@ -273,6 +301,7 @@ ltb_status ltb_engine_ipc_handle(ltb_engine* e, void* out) {
 }
 
 ltb_status ltb_engine_connect(ltb_engine* e, const void* handles) {
+  EngLock lk_(e);
   if (!e || !handles) return efail(LTB_INVALID, "connect: null argument");
   if (!e->factorized) return efail(LTB_STATE, "connect: set the factor first");
   Guard gd(e->device);
@@ -283,6 +312,7 @@ ltb_status ltb_engine_connect(ltb_engine* e, const void* handles) {
 }
 
 ltb_status ltb_engine_set_factor(ltb_engine* e, const double* L, int n, size_t ld, int ptr_kind) {
+  EngLock lk_(e);
   if (!e || !L) return efail(LTB_INVALID, "set_factor: null argument");
   if (ld < (size_t)n) return efail(LTB_DIMENSION, "set_factor: ld < n");
   if (e->world > 1)
@@ -308,6 +338,7 @@ ltb_status ltb_engine_set_factor(ltb_engine* e, const double* L, int n, size_t l
 }
 
 ltb_status ltb_engine_set_factor_generated(ltb_engine* e, int n, uint64_t seed) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "set_factor_generated: null engine");
   Guard gd(e->device);
   ltb_status st = factor_prepare(e, n);
@@ -356,6 +387,7 @@ extern "C" {
 ltb_status ltb_engine_form_k(ltb_engine* e, const double* f_kernel, const double* g_kernel,
                              const double* prior3, int rows, int cols, int nt, double sigma2,
                              int ptr_kind) {
+  EngLock lk_(e);
   if (!e || !f_kernel) return efail(LTB_INVALID, "form_K: null argument");
   if (!g_kernel && !prior3) return efail(LTB_INVALID, "form_K: need the G kernel or the prior (prior3)");
   ltb_status st = form_k_check(e, "form_K");
@@ -392,6 +424,7 @@ ltb_status ltb_engine_form_k(ltb_engine* e, const double* f_kernel, const double
 
 ltb_status ltb_engine_form_k_generated(ltb_engine* e, uint64_t seed, uint64_t stream, double h_x,
                                        double gamma, double delta, double sigma2) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "form_K: null engine");
   ltb_status st = form_k_check(e, "form_K");
   if (st != LTB_OK) return st;
@@ -408,6 +441,7 @@ ltb_status ltb_engine_form_k_generated(ltb_engine* e, uint64_t seed, uint64_t st
 }
 
 ltb_status ltb_engine_factorize(ltb_engine* e) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "factorize: null engine");
   if (!e->kformed) return efail(LTB_STATE, "engine: missing offline artifact: K (run form_K)");
   Guard gd(e->device);
@@ -429,6 +463,7 @@ ltb_status ltb_engine_factorize(ltb_engine* e) {
 
 ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* factorize_ms,
                                  double* formq_ms) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "offline_ms: null engine");
   if (formk_ms) *formk_ms = e->formk_ms;
   if (factorize_ms) *factorize_ms = e->factorize_ms;
@@ -437,6 +472,7 @@ ltb_status ltb_engine_offline_ms(const ltb_engine* e, double* formk_ms, double* 
 }
 
 ltb_status ltb_engine_export_lower(const ltb_engine* e_, double* out, size_t ld, int ptr_kind) {
+  EngLock lk_(e_);
   ltb_engine* e = const_cast<ltb_engine*>(e_);
   if (!e || !out) return efail(LTB_INVALID, "export_lower: null argument");
   if (!e->kformed && !e->factorized) return efail(LTB_STATE, "engine: missing offline artifact: K or its factor");
@@ -461,13 +497,13 @@ ltb_status ltb_engine_export_lower(const ltb_engine* e_, double* out, size_t ld,
 }
 
 ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, int ptr_kind) {
+  EngLock lk_(e);
   if (!e || !s || !y) return efail(LTB_INVALID, "solve_k: null argument");
   ltb_status st = require_factor(e);
   if (st != LTB_OK) return st;
   Guard gd(e->device);
+  DevLock dl_(e->device);
   const cudaStream_t strm = scratch_stream(s);
-  const size_t n = (size_t)e->factor.n;
-  (void)n;
   st = solve_dev(e, y, y, strm,
                  ptr_kind == LTB_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
   return st != LTB_OK ? st : check_solve_status(e, strm);
@@ -475,11 +511,13 @@ ltb_status ltb_engine_solve_k(const ltb_engine* e, ltb_scratch* s, double* y, in
 
 ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, const double* d,
                                          double* m_map, double* q, double* seconds, int ptr_kind) {
+  EngLock lk_(e_);
   if (!e_ || !s || !d) return efail(LTB_INVALID, "infer_map: null argument");
   ltb_engine* e = const_cast<ltb_engine*>(e_);
   ltb_status st = require_factor(e);
   if (st != LTB_OK) return st;
   Guard gd(e->device);
+  DevLock dl_(e->device);
   const cudaStream_t strm = scratch_stream(s);
   const size_t nd_nt = (size_t)e->nd * e->nt, nm_nt = (size_t)e->nm * e->nt,
                nq_nt = (size_t)e->nq * e->nt;
@@ -532,12 +570,14 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
 
 ltb_status ltb_engine_infer_map(const ltb_engine* e, ltb_scratch* s, const double* d,
                                 double* m_map, double* seconds, int ptr_kind) {
+  EngLock lk_(e);
   if (!m_map) return efail(LTB_INVALID, "infer_map: null m_map");
   return ltb_engine_infer_and_forecast(e, s, d, m_map, nullptr, seconds, ptr_kind);
 }
 
 ltb_status ltb_engine_forecast(const ltb_engine* e_, ltb_scratch* s, const double* m, double* q,
                                int ptr_kind) {
+  EngLock lk_(e_);
   if (!e_ || !s || !m || !q) return efail(LTB_INVALID, "forecast: null argument");
   ltb_engine* e = const_cast<ltb_engine*>(e_);
   Guard gd(e->device);
@@ -552,6 +592,7 @@ ltb_status ltb_engine_forecast(const ltb_engine* e_, ltb_scratch* s, const doubl
 // ---- diagnostics: per-step timestamps of the TRSV sweeps ----
 extern "C" ltb_status ltb_engine_trsv_trace(ltb_engine* e, int enable, unsigned long long* host_out,
                                             int n) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "trsv_trace: null engine");
   Guard gd(e->device);
   if (!e->factorized) return efail(LTB_STATE, "trsv_trace: no factor");
@@ -582,6 +623,9 @@ extern "C" ltb_status ltb_debug_dtrsv_emulated(int n, int P, uint64_t seed, cons
                                                double* seconds) {
   if (P < 1 || P > kMaxRanks || n < 1 || !b_host || !x_host)
     return efail(LTB_INVALID, "dtrsv_emulated: bad arguments");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevLock dl_(dev);
   TriFactor ts[kMaxRanks];
   TriFactor* tp[kMaxRanks];
   const double* bp[kMaxRanks];
@@ -833,6 +877,7 @@ ltb_status ltb_normal_quantile(double p, double* out) {
 
 ltb_status ltb_engine_set_phase3(ltb_engine* e, const double* Q, size_t ldq,
                                  const double* gpost_q_diag, int ptr_kind) {
+  EngLock lk_(e);
   if (!e || !Q || !gpost_q_diag) return efail(LTB_INVALID, "set_phase3: null argument");
   if (!e->fq && e->nq == 0) return efail(LTB_STATE, "set_phase3: engine has no F_q plan (N_q unknown)");
   const long long rows = (long long)e->nq * e->nt, cols = (long long)e->nd * e->nt;
@@ -877,6 +922,7 @@ ltb_status ltb_engine_set_phase3(ltb_engine* e, const double* Q, size_t ldq,
 
 ltb_status ltb_engine_predict_qoi(const ltb_engine* e, ltb_scratch* s, const double* d, double level,
                                   double* q, double* lo, double* hi, double* seconds, int ptr_kind) {
+  EngLock lk_(e);
   if (!e || !s || !d || !q) return efail(LTB_INVALID, "predict_qoi: null argument");
   if (!(level > 0 && level < 1)) return efail(LTB_CONFIG, "predict_qoi: credible level must lie in (0, 1)");
   Guard gd(e->device);
@@ -1006,6 +1052,7 @@ extern "C" ltb_status ltb_fnv1a64_file(const char* path, uint64_t* out) {
 // set_factor from chol.dnsm (workflow.cpp:324 read_dense): the strict upper
 // part of the stored matrix is ignored (it may hold K, bayes_engine.cpp:180-193)
 extern "C" ltb_status ltb_engine_load_factor_dnsm(ltb_engine* e, const char* path) {
+  EngLock lk_(e);
   if (!e || !path) return efail(LTB_INVALID, "load_factor_dnsm: null argument");
   if (e->world > 1)
     return efail(LTB_STATE, "load_factor_dnsm: a distributed factor is built per rank (set_factor_generated)");
@@ -1055,6 +1102,7 @@ extern "C" ltb_status ltb_engine_load_factor_dnsm(ltb_engine* e, const char* pat
 // set_phase3 from Q.dnsm and Gamma_post_q.dnsm (workflow.cpp:325-330)
 extern "C" ltb_status ltb_engine_load_phase3_dnsm(ltb_engine* e, const char* q_path,
                                                   const char* gpost_path) {
+  EngLock lk_(e);
   if (!e || !q_path || !gpost_path) return efail(LTB_INVALID, "load_phase3_dnsm: null argument");
   const uint64_t rows = (uint64_t)e->nq * e->nt, cols = (uint64_t)e->nd * e->nt;
   FILE* fq = nullptr;
@@ -1182,6 +1230,7 @@ ltb_status form_q_check(ltb_engine* e, int nq) {
 extern "C" ltb_status ltb_engine_form_q(ltb_engine* e, const double* f_kernel, const double* fq_kernel,
                                         const double* gq_kernel, const double* prior3, int nd, int nq,
                                         int nm, int nt, int ptr_kind) {
+  EngLock lk_(e);
   if (!e || !f_kernel || !fq_kernel) return efail(LTB_INVALID, "form_Q: null argument");
   if (!gq_kernel && !prior3) return efail(LTB_INVALID, "form_Q: need the Gq kernel or the prior (prior3)");
   ltb_status st = form_q_check(e, nq);
@@ -1220,6 +1269,7 @@ extern "C" ltb_status ltb_engine_form_q(ltb_engine* e, const double* f_kernel, c
 extern "C" ltb_status ltb_engine_form_q_generated(ltb_engine* e, uint64_t seed, uint64_t stream_f,
                                                   uint64_t stream_fq, int nq, double h_x, double gamma,
                                                   double delta) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "form_Q: null engine");
   ltb_status st = form_q_check(e, nq);
   if (st != LTB_OK) return st;
@@ -1239,6 +1289,7 @@ extern "C" ltb_status ltb_engine_form_q_generated(ltb_engine* e, uint64_t seed, 
 
 extern "C" ltb_status ltb_engine_export_phase3(const ltb_engine* e, double* Q, size_t ldq, double* gpost,
                                                double* prior_cov, size_t ldg, int ptr_kind) {
+  EngLock lk_(e);
   if (!e) return efail(LTB_INVALID, "export_phase3: null engine");
   Guard gd(e->device);
   std::lock_guard<std::mutex> lk(g_qoi_mu);
@@ -1300,6 +1351,7 @@ __global__ void integrate_kernel(const double* __restrict__ m, int n_rows, int n
 
 extern "C" ltb_status ltb_engine_set_residual_model(ltb_engine* e, const ltb_plan* plan_f, double sigma2,
                                                     double h_x, double gamma, double delta) {
+  EngLock lk_(e);
   if (!e || !plan_f) return efail(LTB_INVALID, "set_residual_model: null argument");
   int r, c, t;
   plan_dims(plan_f, &r, &c, &t);
@@ -1315,6 +1367,7 @@ extern "C" ltb_status ltb_engine_set_residual_model(ltb_engine* e, const ltb_pla
 
 extern "C" ltb_status ltb_engine_map_residual(const ltb_engine* e_, ltb_scratch* s, const double* d,
                                               const double* m_map, double* rel_residual, int ptr_kind) {
+  EngLock lk_(e_);
   ltb_engine* e = const_cast<ltb_engine*>(e_);
   if (!e || !s || !d || !m_map || !rel_residual) return efail(LTB_INVALID, "map_residual: null argument");
   if (!e->plan_f) return efail(LTB_STATE, "engine: no residual model (set_residual_model)");

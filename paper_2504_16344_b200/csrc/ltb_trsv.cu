@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "ltb_common.cuh"
 #include "ltb_gen.cuh"
@@ -199,8 +200,11 @@ struct WorkerSmem {
   double sR[2 * kTB];
 };
 
-// grid-wide barrier of this launch (all CTAs co-resident, see launch())
-LTB_DEV void grid_barrier(unsigned* gsync) {
+// grid-wide barrier of this launch (all CTAs co-resident, see launch()).
+// Bounded like every other wait: if some CTA never arrives (residency lost to
+// another kernel or process) the waiters give up after kSpinNs, flag *status
+// and the kernel runs to completion with the host reporting LTB_CUDA.
+LTB_DEV void grid_barrier(unsigned* gsync, int* status) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* gen = gsync + 1;
@@ -211,12 +215,27 @@ LTB_DEV void grid_barrier(unsigned* gsync) {
       __threadfence();
       atomicAdd(gsync + 1, 1u);
     } else {
-      while (*gen == g) __nanosleep(32);
+      const unsigned long long t0 = globaltimer();
+      while (*gen == g) {
+        __nanosleep(32);
+        if (*(volatile int*)status) break;
+        if (globaltimer() - t0 > kSpinNs) {
+          atomicExch(status, 1);
+          break;
+        }
+      }
     }
     __threadfence();
   }
   __syncthreads();
 }
+
+// Every value handed to another CTA / rank through a sentinel-armed slot goes
+// through here: a NaN (e.g. from a NaN in d: -NaN is exactly the all-ones
+// sentinel) is replaced by the canonical quiet NaN, so NaN inputs propagate
+// to a NaN result as in the reference's Eigen TRSV instead of stalling the
+// consumers.
+LTB_DEV double handoff(double v) { return isnan(v) ? __longlong_as_double(0x7ff8000000000000ll) : v; }
 
 // ---------------- chain ------------------------------------------------------
 // Chain tiles are stored split by half: step I, half h, tile k, column c,
@@ -360,7 +379,7 @@ LTB_DEV void head_step(const DistArgs& a, ChainSmem& sm, const ChainRing& cr, co
 #pragma unroll
     for (int k = 0; k < kMaxLook - 1; ++k)
       if (k < L - 1) s += pk[k];
-    const double v = -s;
+    const double v = handoff(-s);
     sm.xr[slot][tid] = v;
 #pragma unroll
     for (int k = 1; k < kMaxLook; ++k)
@@ -559,7 +578,7 @@ LTB_DEV void worker_forward_row(const DistArgs& a, const RankView& rv, WorkerSme
   for (int k = 0; k < kCPT; ++k) s = fma(sm.sD[(kCPT * q + k) * kPad + i], sm.rr[kCPT * q + k], s);
   sm.red[q][i] = s;
   __syncthreads();
-  if (tid < kTB) a.peer[0][off_cf(nb) + (size_t)I * kTB + tid] = red_sum(sm.red, tid);
+  if (tid < kTB) a.peer[0][off_cf(nb) + (size_t)I * kTB + tid] = handoff(red_sum(sm.red, tid));
   __syncthreads();
   if (a.trace && tid == 0 && a.r0 == 0) a.trace[2 * nb + I] = globaltimer();
 }
@@ -634,7 +653,7 @@ LTB_DEV void worker_transposed_col(const DistArgs& a, const RankView& rv, int r,
     sm.red[part][ii] = s;
   }
   __syncthreads();
-  if (tid < kTB) a.peer[0][off_cb(nb) + ((size_t)r * nb + I) * kTB + tid] = red_sum(sm.red, tid);
+  if (tid < kTB) a.peer[0][off_cb(nb) + ((size_t)r * nb + I) * kTB + tid] = handoff(red_sum(sm.red, tid));
   __syncthreads();
   if (a.trace && tid == 0 && a.r0 == 0 && r == 0) a.trace[3 * nb + I] = globaltimer();
 }
@@ -658,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
     for (size_t e = (size_t)lc * kThreads + threadIdx.x; e < n1 + n2; e += (size_t)a.gper * kThreads)
       base[e < n1 ? e : off_cf(nb) + (e - n1)] = kSentinel;
   }
-  grid_barrier(a.gsync);
+  grid_barrier(a.gsync, a.status);
   // (2) real multi-GPU: no rank may push before every receiver has re-armed
   if (a.nloc < a.P) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -681,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
         }
       }
     }
-    grid_barrier(a.gsync);
+    grid_barrier(a.gsync, a.status);
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && a.r0 == 0) a.trace[4 * nb] = globaltimer();
 
@@ -833,19 +852,32 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
   }
 }
 
-int g_coop_blocks[kMaxLook + 1] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};  // per cluster size
+constexpr int kMaxDevices = 64;
+// co-resident CTA count per (device, cluster size), measured once per device
+int g_coop_blocks[kMaxDevices][kMaxLook + 1];
+std::once_flag g_coop_once;
+std::mutex g_coop_mu;
+
+const void* trsv_fn(int look) { return look == 8 ? (const void*)trsv_kernel<8> : (const void*)trsv_kernel<4>; }
 
 cudaError_t coop_blocks(int look, int* out) {
-  int& cb = g_coop_blocks[look];
+  int dev = 0, sms = 0, per = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(g_coop_once, [] {
+    for (auto& d : g_coop_blocks)
+      for (int& v : d) v = -1;
+  });
+  const void* fn = trsv_fn(look);
+  // the shared-memory opt-in is per device: set it for the current one on
+  // every launch (cheap), not only for the first device that solved
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingSmem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_coop_mu);
+  int& cb = g_coop_blocks[dev][look];
   if (cb < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const void* fn = look == 8 ? (const void*)trsv_kernel<8> : (const void*)trsv_kernel<4>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kRingSmem);
-    if (e != cudaSuccess) return e;
-    // clusters of two co-resident CTAs (the chain pair); workers come in pairs too
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(look * 16);
     cfg.blockDim = dim3(kThreads);
@@ -861,14 +893,21 @@ cudaError_t coop_blocks(int look, int* out) {
     if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) clusters = 0;
     cudaGetLastError();
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, kRingSmem);
-    // (some tools report no cluster occupancy: fall back to the per-SM count;
-    // the grid never exceeds what one SM per CTA can hold)
     const int by_sm = sms * per;
-    cb = (clusters > 0 ? std::min(by_sm, clusters * look) : by_sm) & ~(look - 1);
+    if (clusters > 0) {
+      cb = std::min(by_sm, clusters * look);
+    } else {
+      // no cluster occupancy from the runtime (some tools intercept the
+      // query): assume the co-resident fraction measured on B200 with the
+      // query available -- clusters of 8 fit on 120 of 148 SMs, clusters of
+      // 4 on 144 -- rather than one CTA per SM, which would not fit
+      cb = (int)((long long)by_sm * (look == 8 ? 120 : 144) / 148);
+    }
+    cb &= ~(look - 1);
     cb = std::max(cb, 2 * look);
     if (getenv("LTB_DEBUG"))
-      fprintf(stderr, "ltb trsv: sms=%d blocks/SM=%d clusters=%d -> %d co-resident CTAs\n", sms, per, clusters,
-              cb);
+      fprintf(stderr, "ltb trsv: dev %d sms=%d blocks/SM=%d clusters=%d -> %d co-resident CTAs\n", dev, sms, per,
+              clusters, cb);
   }
   *out = cb;
   return cudaSuccess;
@@ -921,18 +960,31 @@ cudaError_t launch(const DistArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kRingSmem;
   cfg.stream = st;
-  // The grid barrier and the spin waits need every CTA resident at once.  The
-  // grid is sized to the measured cluster occupancy (coop_blocks) on a GPU the
-  // solve has to itself; the cooperative launch attribute would state the same
-  // guarantee, but Nsight Compute cannot launch cooperative kernels that also
-  // carry a cluster dimension, and every dependency wait in the kernel times
-  // out into a status error rather than hanging if residency ever fails.
-  cudaLaunchAttribute at[1];
+  // The grid barrier and the spin waits need every CTA resident at once: the
+  // grid is sized to the measured cluster occupancy (coop_blocks), launches
+  // on a device are serialized (trsv_device_mutex), and the launch carries the
+  // cooperative attribute, which makes the driver guarantee co-residency (or
+  // refuse the launch).  Nsight Compute cannot replay a cooperative kernel
+  // that also has a cluster dimension; where the cooperative launch is
+  // refused for that reason the plain launch is used, and every wait in the
+  // kernel is bounded (status error, never a hang).
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = a.look;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
+  static const bool no_coop = getenv("LTB_TRSV_NONCOOP") != nullptr;
+  cudaError_t e = cudaErrorNotSupported;
+  if (!no_coop) {
+    cfg.numAttrs = 2;
+    e = a.look == 8 ? cudaLaunchKernelEx(&cfg, trsv_kernel<8>, a) : cudaLaunchKernelEx(&cfg, trsv_kernel<4>, a);
+    if (e == cudaSuccess) return e;
+    if (e == cudaErrorCooperativeLaunchTooLarge) return e;  // would not be co-resident: never launch it
+    cudaGetLastError();
+  }
   cfg.numAttrs = 1;
   return a.look == 8 ? cudaLaunchKernelEx(&cfg, trsv_kernel<8>, a) : cudaLaunchKernelEx(&cfg, trsv_kernel<4>, a);
 }
@@ -1022,6 +1074,11 @@ cudaError_t trsv_connect(TriFactor& t, const cudaIpcMemHandle_t* handles) {
 }
 
 double* trsv_result(TriFactor& t) { return t.recv + off_xb(t.nb); }
+
+std::mutex& trsv_device_mutex(int dev) {
+  static std::mutex mus[kMaxDevices];
+  return mus[(dev >= 0 && dev < kMaxDevices) ? dev : 0];
+}
 
 cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
   for (int p = 0; p < t.P; ++p)

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 namespace ltb {
 
 constexpr int kTB = 64;        // factor tile edge
@@ -65,6 +67,11 @@ cudaError_t trsv_connect(TriFactor& t, const cudaIpcMemHandle_t* handles);
 // cooperative launch per rank; ranks must launch concurrently.
 cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st);
 double* trsv_result(TriFactor& t);
+// Process-wide lock of device `dev` for the persistent K^{-1} launch: the
+// kernel fills the GPU and needs all of its CTAs resident, so two of them
+// must never run at once.  Callers hold it from the launch until they have
+// synchronized the launch stream.
+std::mutex& trsv_device_mutex(int dev);
 // All P ranks emulated by ONE cooperative launch on the current GPU (test /
 // validation of the distributed algorithm without P GPUs).
 cudaError_t trsv_solve_emulated(TriFactor* const* ts, const double* const* bs, int P,

@@ -389,6 +389,114 @@ class MatvecPlan:
         return m
 
 
+class ShardedMatvecPlan:
+    """One MatvecPlan with its N_m columns sharded over several GPUs of this
+    process (include/ltb.h ltb_plan_create_sharded): same apply_raw /
+    apply_adjoint_raw contract as MatvecPlan; device buffers live on the home
+    device ``devices[0]``.  Devices may repeat (shards on one GPU)."""
+
+    class Scratch:
+        def __init__(self, plan, stream=None):
+            h = C.c_void_p()
+            if stream is not None and not isinstance(stream, int):
+                stream = stream.cuda_stream or 1
+            check(_lib.load().ltb_sscratch_create(plan._h, C.c_void_p(stream or 0), C.byref(h)))
+            self._h = h
+            self.plan = plan
+
+        def sync(self):
+            check(_lib.load().ltb_sscratch_sync(self._h))
+
+        def close(self):
+            if getattr(self, "_h", None):
+                _lib.load().ltb_sscratch_destroy(self._h)
+                self._h = None
+
+        def __del__(self):
+            try:
+                self.close()
+            except Exception:
+                pass
+
+    def __init__(self, kernel, devices, unit_cols=0):
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        opts = _opts(None, unit_cols)
+        check(_lib.load().ltb_plan_create_sharded(C.c_void_p(kernel.data.ctypes.data), kernel.rows_out,
+                                                  kernel.n_cols, kernel.n_time, int(kernel.tag), len(devices),
+                                                  devs, C.byref(opts), C.byref(h)))
+        self._h = h
+        self._dims()
+
+    @classmethod
+    def generated(cls, rows, cols, nt, seed, devices, tag=KernelTag.F, stream=None, unit_cols=0):
+        """Sharded plan of the device-generated kernel (ltb_plan_create_generated
+        per shard, each its own column range of the rows x cols kernel)."""
+        self = cls.__new__(cls)
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        opts = _opts(None, unit_cols)
+        stream = int(tag) + 1 if stream is None else stream
+        check(_lib.load().ltb_plan_create_generated_sharded(rows, cols, nt, int(tag), seed, stream, len(devices),
+                                                            devs, C.byref(opts), C.byref(h)))
+        self._h = h
+        self._dims()
+        return self
+
+    def _dims(self):
+        r, c, t, n = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(_lib.load().ltb_splan_dims(self._h, C.byref(r), C.byref(c), C.byref(t), C.byref(n)))
+        self._r, self._c, self._t, self._n = r.value, c.value, t.value, n.value
+
+    def shards(self):
+        """[(device, c0, c1, peer)] per shard."""
+        out = []
+        for k in range(self._n):
+            d, a, b, p = C.c_int(), C.c_longlong(), C.c_longlong(), C.c_int()
+            check(_lib.load().ltb_splan_shard(self._h, k, C.byref(d), C.byref(a), C.byref(b), C.byref(p)))
+            out.append((d.value, a.value, b.value, bool(p.value)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().ltb_splan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rows_out(self):
+        return self._r
+
+    def n_cols(self):
+        return self._c
+
+    def n_time(self):
+        return self._t
+
+    def kernel_hat_sqnorm(self):
+        out = C.c_double()
+        check(_lib.load().ltb_splan_kernel_hat_sqnorm(self._h, C.byref(out)))
+        return out.value
+
+    def apply_raw(self, inp, out, scratch):
+        pi, ki, _a = _buffer(inp, self._c * self._t, "apply_raw input")
+        po, ko, _b = _buffer(out, self._r * self._t, "apply_raw output", writable=True)
+        if ki != ko:
+            raise ValueError("apply_raw: input and output must both be host or both device")
+        check(_lib.load().ltb_apply_sharded(self._h, scratch._h, pi, po, ki))
+
+    def apply_adjoint_raw(self, inp, out, scratch):
+        pi, ki, _a = _buffer(inp, self._r * self._t, "apply_adjoint_raw input")
+        po, ko, _b = _buffer(out, self._c * self._t, "apply_adjoint_raw output", writable=True)
+        if ki != ko:
+            raise ValueError("apply_adjoint_raw: input and output must both be host or both device")
+        check(_lib.load().ltb_apply_adjoint_sharded(self._h, scratch._h, pi, po, ki))
+
+
 def dense_apply(kernel, v, adjoint=False, mem_cap_bytes=2 << 30):
     """fft_matvec.hpp:80-87 / fft_matvec.cpp:267-315: the FFT-free time-domain
     block-Toeplitz product on the device (the reference's test oracle, kept for
