@@ -393,6 +393,16 @@ def bench_online(ltb, torch, reps=20, cpu=True, parity=True):
         eng.infer_raw(dh, mh, qh)
         e2e.append(time.perf_counter() - t0)
     e2e.sort()
+    # reference-style: infer_map builds a Scratch for the G* plan per call
+    # (bayes_engine.cpp:317)
+    fresh = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sc = ltb.MatvecPlan.Scratch(g)
+        eng.infer_raw(dh, mh, qh, scratch=sc)
+        sc.close()
+        fresh.append(time.perf_counter() - t0)
+    fresh.sort()
     # the Q d forecast route with credible intervals (predict_qoi), device time incl. copies
     obs = ltb.ObsSeries(nd, nt, ltb.Layout.SpaceMajorRows, dh)
     pq = sorted(eng.predict_qoi(obs).seconds for _ in range(reps))
@@ -403,6 +413,7 @@ def bench_online(ltb, torch, reps=20, cpu=True, parity=True):
                      "factorized on the device from the generated F and its prior-premultiplied G)",
            "latency_ms": med * 1e3, "latency_min_ms": dev[0] * 1e3,
            "e2e_ms": e2e[len(e2e) // 2] * 1e3,
+           "e2e_fresh_scratch_ms": fresh[len(fresh) // 2] * 1e3,
            "bytes": byts, "achieved_gbs": byts / med / 1e9,
            "solve_k_ms": solve[len(solve) // 2] * 1e3,
            "gstar_ms": sum(gst["Fstar"]) / reps, "fq_ms": sum(fqt["F"]) / reps,
@@ -618,6 +629,28 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_e2e = float(t.item())
     e2e_value = world * step_bytes / (ms_e2e * 1e-3) / 1e9
+
+    # reference-style calls: a fresh Scratch per apply, as MatvecPlan::apply(m)
+    # builds one (fft_matvec.cpp:232-235) -- the C++ drop-in's Scratch ctor /
+    # dtor are exactly ltb_scratch_create / ltb_scratch_destroy (pooled)
+    fresh_ms = None
+    if world == 1:
+        def step_fresh():
+            s1 = ltb.MatvecPlan.Scratch(plan)
+            plan.apply_raw(m_hn, dout_hn, s1)
+            s1.close()
+            s2 = ltb.MatvecPlan.Scratch(plan)
+            plan.apply_adjoint_raw(d_hn, mout_hn, s2)
+            s2.close()
+
+        step_fresh()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_fresh()
+        e1.record(stream)
+        barrier()
+        fresh_ms = e0.elapsed_time(e1) / args.steps
     if world == 1:
         h2d, d2h = 8 * (nm * nt + nd * nt), 8 * (nd * nt + nm * nt)
     else:  # + the partial / broadcast d round trips through pinned host memory
@@ -687,7 +720,9 @@ def run_ours(args):
             "f_ms": f_ms, "fstar_ms": fs_ms,
             "hbm_frac_step": value / world / peak,
             "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "fresh_scratch_ms_per_step": fresh_ms,
+                    "fresh_scratch_overhead": (fresh_ms / ms_e2e - 1.0) if fresh_ms else None},
             "roofline": roof,
             "gpu_launches": int(launches),
             "clocks": clk,

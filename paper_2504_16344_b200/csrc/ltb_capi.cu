@@ -14,6 +14,8 @@
 #include <vector>
 #include <algorithm>
 #include <atomic>
+#include <memory>
+#include <mutex>
 
 #include "../../include/ltb.h"
 #include "ltb_gen.cuh"
@@ -109,6 +111,13 @@ std::vector<double2> twiddles(int n) {
 
 }  // namespace
 
+struct ScratchPool {
+  std::mutex mu;
+  std::vector<ltb_scratch*> free;
+  bool plan_alive = true;
+};
+constexpr size_t kScratchPoolMax = 8;
+
 struct ltb_plan {
   int device = 0;
   int rows = 0, cols = 0, nt = 0, npad = 0, nf = 0, tag = 0;
@@ -119,13 +128,23 @@ struct ltb_plan {
   double2* big_tw = nullptr;    // [W_n1 | W_n2 | W_N]
   GemvShape shape{};
   size_t bytes = 0;
+  // Scratch pool: the reference builds a fresh Scratch for every apply(m)
+  // (fft_matvec.cpp:232-235), every infer_map (bayes_engine.cpp:317) and
+  // every form_K column (:144).  Released scratches park here with their
+  // workspaces and private stream, so such a Scratch costs a pointer swap
+  // instead of ~0.5 GB of cudaMalloc + a device-synchronizing cudaFree.
+  // Shared with the scratches, so a Scratch may outlive its plan (as in the
+  // reference, where a Scratch owns its buffers outright).
+  std::shared_ptr<struct ScratchPool> pool = std::make_shared<ScratchPool>();
 };
 
 struct ltb_scratch {
   const ltb_plan* plan = nullptr;
+  std::shared_ptr<ScratchPool> pool;
   int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
+  cudaStream_t stream = nullptr;  // the stream applies run on (caller's or priv)
+  cudaStream_t priv = nullptr;    // private stream (created when no stream is given; kept by the pool)
+  cudaEvent_t released = nullptr; // recorded on release: the next owner's stream waits on it
   double2* xhat = nullptr;      // nf * cols
   double2* dhat = nullptr;      // nf * rows
   double2* partials = nullptr;  // GEMV-N unit partials
@@ -231,9 +250,17 @@ ltb_status plan_init(ltb_plan* p, int rows, int cols, int nt, int tag, const ltb
   return LTB_OK;
 }
 
+void scratch_free(ltb_scratch* s);
+
 void plan_free(ltb_plan* p) {
   if (!p) return;
   DeviceGuard g(p->device);
+  {
+    std::lock_guard<std::mutex> lk(p->pool->mu);
+    for (ltb_scratch* s : p->pool->free) scratch_free(s);
+    p->pool->free.clear();
+    p->pool->plan_alive = false;
+  }
   cudaFree(p->fhat);
   cudaFree(p->tw);
   cudaFree(p->big_tw);
@@ -608,40 +635,12 @@ ltb_status ltb_plan_copy_kernel_hat(const ltb_plan* p, int f0, int nfreq, double
   return LTB_OK;
 }
 
-ltb_status ltb_scratch_create(const ltb_plan* p, void* stream, ltb_scratch** out) {
-  if (!p || !out) return fail(LTB_INVALID, "ltb_scratch_create: null argument");
-  *out = nullptr;
-  DeviceGuard g(p->device);
-  ltb_scratch* s = new ltb_scratch();
-  s->plan = p;
-  s->device = p->device;
-  auto bail = [&](cudaError_t e) {
-    ltb_scratch_destroy(s);
-    return fail(LTB_CUDA, "ltb_scratch_create: %s", cudaGetErrorString(e));
-  };
-  cudaError_t e;
-  if (stream) {
-    s->stream = (cudaStream_t)stream;
-  } else {
-    if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(e);
-    s->own_stream = true;
-  }
-  const size_t nx = (size_t)p->nf * p->cols, nd = (size_t)p->nf * p->rows;
-  if ((e = cudaMalloc(&s->xhat, sizeof(double2) * nx)) != cudaSuccess) return bail(e);
-  if ((e = cudaMalloc(&s->dhat, sizeof(double2) * nd)) != cudaSuccess) return bail(e);
-  if ((e = cudaMalloc(&s->partials, sizeof(double2) * gemv_n_partials(p->shape))) != cudaSuccess) return bail(e);
-  if ((e = cudaMalloc(&s->tickets, sizeof(unsigned) * (size_t)p->nf * gemv_n_row_tiles(p->shape))) != cudaSuccess) return bail(e);
-  if ((e = cudaMalloc(&s->red, sizeof(double) * (1024 + 8))) != cudaSuccess) return bail(e);
-  *out = s;
-  return LTB_OK;
-}
+}  // extern "C"
 
-ltb_status ltb_scratch_destroy(ltb_scratch* s) {
-  if (!s) return LTB_OK;
+namespace {
+void scratch_free(ltb_scratch* s) {
   DeviceGuard g(s->device);
-  // a borrowed stream may already be gone (its owner tears down first);
-  // cudaFree below synchronizes the device anyway
-  if (s->own_stream && s->stream) cudaStreamSynchronize(s->stream);
+  if (s->priv) cudaStreamSynchronize(s->priv);
   cudaFree(s->xhat);
   cudaFree(s->dhat);
   cudaFree(s->partials);
@@ -652,9 +651,94 @@ ltb_status ltb_scratch_destroy(ltb_scratch* s) {
   for (cudaEvent_t e : s->events) cudaEventDestroy(e);
   for (cudaEvent_t e : s->pipe_ev)
     if (e) cudaEventDestroy(e);
+  if (s->released) cudaEventDestroy(s->released);
   if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
-  if (s->own_stream) cudaStreamDestroy(s->stream);
+  if (s->priv) cudaStreamDestroy(s->priv);
   delete s;
+}
+
+// bind a (new or pooled) scratch to the caller's stream, or its private one
+cudaError_t scratch_bind(ltb_scratch* s, void* stream) {
+  if (stream) {
+    s->stream = (cudaStream_t)stream;
+  } else {
+    if (!s->priv) {
+      cudaError_t e = cudaStreamCreateWithFlags(&s->priv, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    s->stream = s->priv;
+  }
+  // whatever the previous owner queued on its stream finishes first
+  return s->released ? cudaStreamWaitEvent(s->stream, s->released, 0) : cudaSuccess;
+}
+}  // namespace
+
+extern "C" {
+
+ltb_status ltb_scratch_create(const ltb_plan* p, void* stream, ltb_scratch** out) {
+  if (!p || !out) return fail(LTB_INVALID, "ltb_scratch_create: null argument");
+  *out = nullptr;
+  DeviceGuard g(p->device);
+  ltb_scratch* s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(p->pool->mu);
+    if (!p->pool->free.empty()) {
+      s = p->pool->free.back();
+      p->pool->free.pop_back();
+    }
+  }
+  if (s) {
+    cudaError_t e = scratch_bind(s, stream);
+    if (e != cudaSuccess) {
+      scratch_free(s);
+      return fail(LTB_CUDA, "ltb_scratch_create: %s", cudaGetErrorString(e));
+    }
+    *out = s;
+    return LTB_OK;
+  }
+  s = new ltb_scratch();
+  s->plan = p;
+  s->pool = p->pool;
+  s->device = p->device;
+  auto bail = [&](cudaError_t e) {
+    scratch_free(s);
+    return fail(LTB_CUDA, "ltb_scratch_create: %s", cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if ((e = scratch_bind(s, stream)) != cudaSuccess) return bail(e);
+  const size_t nx = (size_t)p->nf * p->cols, nd = (size_t)p->nf * p->rows;
+  if ((e = cudaMalloc(&s->xhat, sizeof(double2) * nx)) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->dhat, sizeof(double2) * nd)) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->partials, sizeof(double2) * gemv_n_partials(p->shape))) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->tickets, sizeof(unsigned) * (size_t)p->nf * gemv_n_row_tiles(p->shape))) != cudaSuccess) return bail(e);
+  if ((e = cudaMalloc(&s->red, sizeof(double) * (1024 + 8))) != cudaSuccess) return bail(e);
+  *out = s;
+  return LTB_OK;
+}
+
+// Returns the scratch to its plan's pool (workspaces and private stream
+// kept; work still queued on its stream is fenced by an event the next owner
+// waits on), or frees it when the pool is full.
+ltb_status ltb_scratch_destroy(ltb_scratch* s) {
+  if (!s) return LTB_OK;
+  DeviceGuard g(s->device);
+  s->timing = false;
+  s->next_quad = 0;
+  bool pooled = false;
+  if (s->pool && (s->released || cudaEventCreateWithFlags(&s->released, cudaEventDisableTiming) == cudaSuccess) &&
+      cudaEventRecord(s->released, s->stream) == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(s->pool->mu);
+    if (s->pool->plan_alive && s->pool->free.size() < kScratchPoolMax) {
+      s->pool->free.push_back(s);
+      pooled = true;
+    }
+  }
+  cudaGetLastError();
+  if (!pooled) {
+    // a borrowed stream may already be gone (its owner tears down first);
+    // cudaFree in scratch_free synchronizes the device anyway
+    scratch_free(s);
+  }
   return LTB_OK;
 }
 

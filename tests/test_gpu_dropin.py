@@ -20,3 +20,20 @@ def test_dropin_reference_cases():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "checks passed" in r.stdout
+
+
+def test_dropin_reference_cases_sharded():
+    """The same reference cases with every MatvecPlan sharded over GPUs by
+    the drop-in (LTB_DEVICES): two real GPUs when present, else two shards on
+    device 0 -- same interface, same bars."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if not os.path.exists(EXE):
+        pytest.skip("dropin_test not built (needs the reference headers at build time)")
+    devs = "0,1" if torch.cuda.device_count() >= 2 else "0,0"
+    env = dict(os.environ, LTB_DEVICES=devs)
+    r = subprocess.run([EXE], capture_output=True, text=True, timeout=300, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "checks passed" in r.stdout
