@@ -728,7 +728,8 @@ def run_ours(args):
             "clocks": clk,
             "parity": parity,
             "comm": {"backend": "nccl", "world_size": world,
-                     "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+                     "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version()),
+                     "init_lines": nccl_init_lines()}
                     if world > 1 else None,
             "online": online,
             "cpu_baseline": cpu,
@@ -742,10 +743,25 @@ def run_ours(args):
 
 def nccl_env():
     """Communicator init lines (NCCL_DEBUG=INFO, subsystem INIT: nranks,
-    rings / NVLS) go to stderr, so stdout stays the one JSON line."""
+    rings / NVLS) go to a per-process file, so stdout stays the one JSON
+    line; nccl_init_lines() echoes them to stderr and into the line."""
     os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ltb_nccl.%h.%p.log")
+
+
+def nccl_init_lines():
+    import socket
+    path = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
+    try:
+        with open(path) as fh:
+            lines = fh.read().splitlines()
+    except OSError:
+        return []
+    for ln in lines:
+        print(ln, file=sys.stderr)
+    keys = ("nRanks", "NVLS", "comm 0x", "Init COMPLETE", "Connected all")
+    return [ln.strip() for ln in lines if any(k in ln for k in keys)][:8]
 
 
 def relaunch(n):

@@ -197,6 +197,7 @@ ltb_status plan_init(ltb_plan* p, int rows, int cols, int nt, int tag, const ltb
   if (tag < 0 || tag > 3) return fail(LTB_INVALID, "MatvecPlan: bad kernel tag %d", tag);
   p->device = (opts && opts->device >= 0) ? opts->device : -1;
   if (p->device < 0) cudaGetDevice(&p->device);
+  DeviceGuard g(p->device);  // F-hat and the twiddles live on the plan's device
   p->rows = rows;
   p->cols = cols;
   p->nt = nt;
