@@ -751,13 +751,15 @@ def nccl_env():
 
 
 def nccl_init_lines():
-    import socket
-    path = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
-    try:
-        with open(path) as fh:
-            lines = fh.read().splitlines()
-    except OSError:
-        return []
+    import glob
+    pat = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", "*").replace("%p", str(os.getpid()))
+    lines = []
+    for path in sorted(glob.glob(pat)):
+        try:
+            with open(path) as fh:
+                lines += fh.read().splitlines()
+        except OSError:
+            pass
     for ln in lines:
         print(ln, file=sys.stderr)
     keys = ("nRanks", "NVLS", "comm 0x", "Init COMPLETE", "Connected all")
