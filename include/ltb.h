@@ -369,6 +369,14 @@ ltb_status ltb_engine_map_residual(const ltb_engine* e, ltb_scratch* s, const do
 
 /* integrate_displacement (bayes_engine.cpp:411-419): out[x] = dt_obs *
  * sum_j m[x][j] of a SpaceMajorRows field (n_rows x n_time) */
+/* reindex (core.hpp:92-95, core.cpp:40-51): bijective permutation of an
+ * n_rows x n_time series between TimeMajorBlocks (j * n_rows + r) and
+ * SpaceMajorRows (r * n_time + j) -- bit exact (a pure permutation).  Host
+ * pointers: synchronous; device pointers: asynchronous on cuda_stream (NULL =
+ * legacy default stream).  from == to copies; in == out only then. */
+ltb_status ltb_reindex(const double* in, int n_rows, int n_time, int from_layout, int to_layout,
+                       double* out, int ptr_kind, void* cuda_stream);
+
 ltb_status ltb_integrate_displacement(const double* m, int n_rows, int n_time, double dt_obs,
                                       double* out, int ptr_kind);
 

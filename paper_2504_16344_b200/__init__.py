@@ -10,7 +10,7 @@ from .matvec import (BlockSeries, BlockToeplitzKernel, CapacityError, ConfigErro
                      CudaError, IoError,
                      DimensionError, KernelTag, Layout, LayoutError, LtbError, MatvecPlan,
                      NumericalError, ObsSeries, QoISeries, ShardedMatvecPlan, SpaceTimeField, StateError,
-                     algorithmic_bytes, dense_apply, reindex)
+                     algorithmic_bytes, dense_apply, reindex, reindex_device)
 from .engine import InferenceEngine, MapResult, QoIPrediction, normal_quantile  # noqa: F401
 from .artifacts import (Manifest, fnv1a64_file, infer_from_artifacts, read_manifest, read_series,  # noqa: F401
                         verify_manifest, write_dense, write_engine_artifacts, write_kernel, write_manifest,

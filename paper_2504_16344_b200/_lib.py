@@ -94,6 +94,7 @@ SIGNATURES = {
     "ltb_sscratch_stream": ([_vp], _vp),
     "ltb_apply_sharded": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_apply_adjoint_sharded": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
+    "ltb_reindex": ([_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp], C.c_int),
 }
 
 _lib = None

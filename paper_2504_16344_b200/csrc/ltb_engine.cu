@@ -1422,6 +1422,71 @@ extern "C" ltb_status ltb_engine_map_residual(const ltb_engine* e_, ltb_scratch*
   return LTB_OK;
 }
 
+// ---- reindex (core.cpp:40-51): the TimeMajorBlocks <-> SpaceMajorRows
+// permutation is a transpose of an R x C row-major matrix (SpaceMajorRows ->
+// TimeMajorBlocks: R = n_rows, C = n_time; the other way R = n_time,
+// C = n_rows).  32 x 32 tiles staged through padded shared memory: both the
+// reads and the writes are 256-byte coalesced rows, every value moved once
+// (HBM-bound: 16 bytes per element), bit exact.
+namespace {
+__global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ in, long long R, long long C,
+                                                        double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const long long tiles_c = (C + 31) / 32, tiles = ((R + 31) / 32) * tiles_c;
+  for (long long tb = blockIdx.x; tb < tiles; tb += gridDim.x) {
+    const long long r0 = (tb / tiles_c) * 32, c0 = (tb % tiles_c) * 32;
+    for (int k = threadIdx.y; k < 32; k += 8) {
+      const long long r = r0 + k, c = c0 + threadIdx.x;
+      if (r < R && c < C) tile[k][threadIdx.x] = in[r * C + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += 8) {
+      const long long c = c0 + k, r = r0 + threadIdx.x;  // out is C x R
+      if (r < R && c < C) out[c * R + r] = tile[threadIdx.x][k];
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+extern "C" ltb_status ltb_reindex(const double* in, int n_rows, int n_time, int from_layout, int to_layout,
+                                  double* out, int ptr_kind, void* cuda_stream) {
+  if (!in || !out) return efail(LTB_INVALID, "reindex: null argument");
+  if (n_rows < 1 || n_time < 1) return efail(LTB_DIMENSION, "reindex: series dims must be >= 1");
+  const bool ok_l = (from_layout == LTB_TIME_MAJOR_BLOCKS || from_layout == LTB_SPACE_MAJOR_ROWS) &&
+                    (to_layout == LTB_TIME_MAJOR_BLOCKS || to_layout == LTB_SPACE_MAJOR_ROWS);
+  if (!ok_l) return efail(LTB_INVALID, "reindex: bad layout");
+  if (ptr_kind != LTB_PTR_HOST && ptr_kind != LTB_PTR_DEVICE) return efail(LTB_INVALID, "reindex: bad ptr_kind");
+  if (in == out && from_layout != to_layout) return efail(LTB_INVALID, "reindex: in-place permutation not supported");
+  const size_t n = (size_t)n_rows * n_time;
+  const cudaStream_t st = (cudaStream_t)cuda_stream;
+  DevArr din, dout;
+  const double* src = in;
+  double* dst = out;
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(din.alloc(n));
+    ENG_CUDA(dout.alloc(n));
+    ENG_CUDA(cudaMemcpyAsync(din.p, in, n * 8, cudaMemcpyHostToDevice, st));
+    src = din.p;
+    dst = dout.p;
+  }
+  if (from_layout == to_layout) {
+    ENG_CUDA(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    const long long R = from_layout == LTB_SPACE_MAJOR_ROWS ? n_rows : n_time;
+    const long long C = from_layout == LTB_SPACE_MAJOR_ROWS ? n_time : n_rows;
+    const long long tiles = ((R + 31) / 32) * ((C + 31) / 32);
+    transpose_kernel<<<(unsigned)std::max(1ll, std::min(tiles, 148ll * 8)), dim3(32, 8), 0, st>>>(src, R, C, dst);
+    ENG_CUDA(cudaGetLastError());
+    count_launches(1);
+  }
+  if (ptr_kind == LTB_PTR_HOST) {
+    ENG_CUDA(cudaMemcpyAsync(out, dst, n * 8, cudaMemcpyDeviceToHost, st));
+    ENG_CUDA(cudaStreamSynchronize(st));
+  }
+  return LTB_OK;
+}
+
 extern "C" ltb_status ltb_integrate_displacement(const double* m, int n_rows, int n_time, double dt_obs,
                                                  double* out, int ptr_kind) {
   if (!m || !out) return efail(LTB_INVALID, "integrate_displacement: null argument");

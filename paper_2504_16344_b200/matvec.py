@@ -119,16 +119,28 @@ class QoISeries(BlockSeries):
 
 
 def reindex(v, target):
-    """Bijective layout permutation (core.cpp:40-51); bit exact."""
+    """Bijective layout permutation (core.cpp:40-51), on the device through
+    ltb_reindex (a tiled transpose of the host values); bit exact."""
     v.check_consistent("reindex")
     target = Layout(target)
-    if target == v.layout:
-        return type(v)(v.n_rows, v.n_time, v.layout, v.values.copy())
-    if target == Layout.TimeMajorBlocks:  # (r, j) at r*nt+j -> j*rows+r
-        vals = v.values.reshape(v.n_rows, v.n_time).T.reshape(-1)
-    else:
-        vals = v.values.reshape(v.n_time, v.n_rows).T.reshape(-1)
-    return type(v)(v.n_rows, v.n_time, target, np.ascontiguousarray(vals))
+    n = v.n_rows * v.n_time
+    out = np.empty(n)
+    check(_lib.load().ltb_reindex(C.c_void_p(v.values.ctypes.data), v.n_rows, v.n_time, int(v.layout),
+                                  int(target), C.c_void_p(out.ctypes.data), PTR_HOST, None))
+    return type(v)(v.n_rows, v.n_time, target, out)
+
+
+def reindex_device(values, n_rows, n_time, layout, target, out=None):
+    """reindex of a CUDA float64 tensor (asynchronous on torch's current
+    stream); returns the permuted tensor."""
+    import torch
+    n = int(n_rows) * int(n_time)
+    out = torch.empty_like(values) if out is None else out
+    pi, _k1, _a = _buffer(values, n, "reindex input")
+    po, _k2, _b = _buffer(out, n, "reindex output", writable=True)
+    check(_lib.load().ltb_reindex(pi, int(n_rows), int(n_time), int(layout), int(target), po, PTR_DEVICE,
+                                  C.c_void_p(torch.cuda.current_stream().cuda_stream or 1)))
+    return out
 
 
 class BlockToeplitzKernel:
