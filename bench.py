@@ -667,6 +667,8 @@ def run_ours(args):
     ach_h = gb / (gemv_h_ms * 1e-3) / 1e9
     total_stage = sum(stages["F"]) + sum(stages["Fstar"])
     traffic = load_traffic()
+    if traffic and traffic.get("shape") != [nd, nm, nt]:
+        traffic = None  # captured at another shape: not this kernel's traffic
     dominant = "gemv_h" if gemv_h_ms >= gemv_n_ms else "gemv_n"
     roof = {
         "bound": "hbm", "kernel": dominant,
@@ -674,6 +676,7 @@ def run_ours(args):
         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
         "frac": (ach_h if dominant == "gemv_h" else ach_n) / peak,
         "traffic": (traffic or {}).get(dominant),
+        "traffic_source": (traffic or {}).get("source"),
         "algorithmic_bytes_per_launch": gb,
         "gemv_n": {"ms": gemv_n_ms, "achieved": ach_n, "frac": ach_n / peak},
         "gemv_h": {"ms": gemv_h_ms, "achieved": ach_h, "frac": ach_h / peak},
@@ -700,7 +703,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            res = cpu_reference_run(nd, nt, seed, min(nm, args.cpu_sample_cols), os.cpu_count() or 1, 3)
+            # the same call, sample and repetitions as the reference arm (run_reference)
+            res = cpu_reference_run(nd, nt, seed, min(nm, args.cpu_sample_cols), os.cpu_count() or 1,
+                                    max(1, args.steps))
             if res:
                 cpu = {"value": res["gbs"], "unit": "GB/s", "cores": os.cpu_count() or 1,
                        "kind": "reference", "sample": res["sample"],
