@@ -316,104 +316,76 @@ __global__ void pad_identity_kernel(double* tiles, int n, int nb) {
 }
 
 // ---------------------------------------------------------------------------
-// (3) tile Cholesky, panel step k.  The diagonal block alone: one CTA factors
-// A_kk in shared memory (right-looking elimination a_rj -= (a_rc / d_c) a_jc,
-// L_rj = a_rj / sqrt(d_j)), writes L_kk, and inverts it for the panel:
-// L_kk^{-1} by 2x2 block recursion (8x8 diagonal blocks by substitution, then
-// Linv21 = -Linv22 (L21 Linv11) at 8 -> 16 -> 32 -> 64), so the panel tiles
-// L_ik = A_ik L_kk^{-T} become one DMMA product each (chol_update_kernel,
-// mode 2) instead of 64 dependent elimination steps per panel CTA.
+// (3) tile Cholesky.  Panel step k: one CTA per panel tile row holds
+// [A_kk; A_ik] (128 rows x 64); thread (row, q) keeps the row's 16 entries
+// j = 4 t + q in registers.  Column c: the owners of column c publish a_rc
+// to shared memory, one barrier, then every row r > c eliminates
+// a_rj -= (a_rc / d_c) a_jc (c < j, j <= r on the diagonal block) from the
+// broadcast column (d_c = a_cc).  Finally L_rj = a_rj / sqrt(d_j),
+// L_jj = sqrt(d_j).  CTA 0 writes L_kk (strict upper zeroed), every CTA its
+// panel tile L_ik = A_ik L_kk^{-T}.
 // ---------------------------------------------------------------------------
-constexpr int kDiagThreads = 256;
-constexpr int kDP = kT + 1;  // padded row
-constexpr size_t kDiagSmem = (size_t)3 * kT * kDP * sizeof(double);
+constexpr int kPanelRows = 2 * kT;
+constexpr int kPanelSplit = 4;                 // threads per row
+constexpr int kPerThread = kT / kPanelSplit;   // 16 register entries
+constexpr int kPanelThreads = kPanelRows * kPanelSplit;
 
-__global__ void __launch_bounds__(kDiagThreads)
-    chol_diag_kernel(double* __restrict__ tiles, int k, double* __restrict__ linv_out, int* status) {
-  extern __shared__ double dsm[];
-  double* a = dsm;                // a[r * kDP + c]
-  double* li = dsm + kT * kDP;    // L^{-1}
-  double* tmp = dsm + 2 * kT * kDP;
-  __shared__ int bad;
-  const int t = threadIdx.x;
-  double* T = tiles + tile_at(k, k);
-  if (t == 0) bad = 0;
-  for (int e = t; e < kTile; e += kDiagThreads) {
-    const int c = e >> 6, r = e & 63;  // column-major tile
-    a[r * kDP + c] = T[e];
-  }
-  const int r = t & 63, q = t >> 6;
+__global__ void __launch_bounds__(kPanelThreads)
+    chol_panel_kernel(double* __restrict__ tiles, int nb, int k, int* status) {
+  __shared__ double col[2][kPanelRows];
+  __shared__ double rsq[kT];
+  const int row = threadIdx.x % kPanelRows, q = threadIdx.x / kPanelRows;
+  const int ip = k + 1 + blockIdx.x;  // panel tile row (none when ip >= nb)
+  const bool diag_row = row < kT;
+  const bool has_panel = ip < nb;
+  double* src = diag_row ? tiles + tile_at(k, k) + row
+                         : (has_panel ? tiles + tile_at(ip, k) + (row - kT) : nullptr);
+  double a[kPerThread];
+#pragma unroll
+  for (int t = 0; t < kPerThread; ++t) a[t] = src ? src[(kPanelSplit * t + q) * kT] : 0.0;
+  bool bad = false;
+  const int jmax = diag_row ? row : kT - 1;
   for (int c = 0; c < kT; ++c) {
+    if (q == (c & (kPanelSplit - 1))) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < kPerThread; ++t)
+        if (kPanelSplit * t + q == c) v = a[t];
+      col[c & 1][row] = v;
+    }
     __syncthreads();
-    double d = a[c * kDP + c];
+    double d = col[c & 1][c];
     if (!(d > 0.0) || !isfinite(d)) {
-      if (t == 0) bad = 1;
+      bad = true;
       d = 1.0;
     }
-    if (r > c) {
-      const double lrc = a[r * kDP + c] / d;
-      for (int j = c + 1 + q; j <= r; j += 4) a[r * kDP + j] = fma(-lrc, a[j * kDP + c], a[r * kDP + j]);
+    if (row > c) {
+      const double lic = col[c & 1][row] / d;
+#pragma unroll
+      for (int t = 0; t < kPerThread; ++t) {
+        const int j = kPanelSplit * t + q;
+        if (j > c && j <= jmax) a[t] = fma(-lic, col[c & 1][j], a[t]);
+      }
     }
   }
-  __syncthreads();
-  __shared__ double rsq[kT];
-  if (t < kT) {
-    double v = a[t * kDP + t];
+  // publish the pivots: owner (j, j % 4) of a_jj
+  if (diag_row && q == (row & (kPanelSplit - 1))) {
+    double v = 1.0;
+#pragma unroll
+    for (int t = 0; t < kPerThread; ++t)
+      if (kPanelSplit * t + q == row) v = a[t];
     if (!(v > 0.0) || !isfinite(v)) v = 1.0;
-    rsq[t] = 1.0 / sqrt(v);
+    rsq[row] = 1.0 / sqrt(v);
   }
   __syncthreads();
-  // L in place (lower), upper zeroed; written back as the tile
-  for (int e = t; e < kTile; e += kDiagThreads) {
-    const int c = e >> 6, rr = e & 63;
-    const double v = rr > c ? a[rr * kDP + c] * rsq[c] : (rr == c ? 1.0 / rsq[c] : 0.0);
-    a[rr * kDP + c] = v;
-    li[rr * kDP + c] = 0.0;
-    T[e] = v;
-  }
-  __syncthreads();
-  // 8x8 diagonal blocks: thread (block b, column j) substitutes L_bb x = e_j
-  if (t < kT) {
-    const int o = (t >> 3) * 8, j = t & 7;
-    double x[8];
+  if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(status, 0, k + 1);
+  if (diag_row ? blockIdx.x == 0 : has_panel) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      double sum = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-      for (int m = 0; m < i; ++m)
-        if (m >= j) sum = fma(-a[(o + i) * kDP + o + m], x[m], sum);
-      x[i] = i < j ? 0.0 : sum / a[(o + i) * kDP + o + i];
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) li[(o + i) * kDP + o + j] = x[i];
-  }
-  // combine: blocks of 2s from two blocks of s
-  for (int sz = 8; sz < kT; sz *= 2) {
-    __syncthreads();
-    const int nblk = kT / (2 * sz), per = sz * sz;
-    // tmp = L21 Linv11 (L21 full, Linv11 lower: m >= c)
-    for (int e = t; e < nblk * per; e += kDiagThreads) {
-      const int b = e / per, rc = e - b * per, rr = rc / sz, c = rc - rr * sz, o = b * 2 * sz;
-      double acc = 0.0;
-      for (int m = c; m < sz; ++m) acc = fma(a[(o + sz + rr) * kDP + o + m], li[(o + m) * kDP + o + c], acc);
-      tmp[(o + sz + rr) * kDP + o + c] = acc;
-    }
-    __syncthreads();
-    // Linv21 = -Linv22 tmp (Linv22 lower: m <= rr)
-    for (int e = t; e < nblk * per; e += kDiagThreads) {
-      const int b = e / per, rc = e - b * per, rr = rc / sz, c = rc - rr * sz, o = b * 2 * sz;
-      double acc = 0.0;
-      for (int m = 0; m <= rr; ++m)
-        acc = fma(li[(o + sz + rr) * kDP + o + sz + m], tmp[(o + sz + m) * kDP + o + c], acc);
-      li[(o + sz + rr) * kDP + o + c] = -acc;
+    for (int t = 0; t < kPerThread; ++t) {
+      const int j = kPanelSplit * t + q;
+      src[j * kT] = !diag_row || j < row ? a[t] * rsq[j] : (j == row ? 1.0 / rsq[j] : 0.0);
     }
   }
-  __syncthreads();
-  for (int e = t; e < kTile; e += kDiagThreads) {
-    const int c = e >> 6, rr = e & 63;  // column-major, as the tiles
-    linv_out[e] = li[rr * kDP + c];
-  }
-  if (t == 0 && bad) atomicCAS(status, 0, k + 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -426,12 +398,8 @@ constexpr int kUS = kT + 4;  // 68 == 4 mod 16
 constexpr int kUpdThreads = 256;
 constexpr size_t kUpdSmem = (size_t)2 * kT * kUS * sizeof(double);
 
-// mode 0: the lower triangle of tiles from (base, base); mode 1: block column
-// `base`; mode 2 (panel): L_ik = A_ik L_kk^{-T} for i >= base, B = linv
-// (column-major L_kk^{-1}), accumulators from zero, no negation
 __global__ void __launch_bounds__(kUpdThreads)
-    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int base, int column_only,
-                       const double* __restrict__ linv) {
+    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int base, int column_only) {
   extern __shared__ __align__(16) double usm[];
   double* sA = usm;
   double* sB = usm + kT * kUS;
@@ -445,10 +413,8 @@ __global__ void __launch_bounds__(kUpdThreads)
     i = base + li;
     j = base + lj;
   }
-  const bool panel = column_only == 2;
-  if (panel) j = k;
   const double* Lik = tiles + tile_at(i, k);
-  const double* Ljk = panel ? linv : tiles + tile_at(j, k);
+  const double* Ljk = tiles + tile_at(j, k);
   double* Aij = tiles + tile_at(i, j);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
@@ -469,9 +435,8 @@ __global__ void __launch_bounds__(kUpdThreads)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
-          acc[mt][nt8][2 * h + c] = panel ? 0.0 : Aij[col * kT + r];
+          acc[mt][nt8][2 * h + c] = Aij[col * kT + r];
         }
-  const double sgn = panel ? 1.0 : -1.0;
   cp_wait<0>();
   __syncthreads();
 #pragma unroll
@@ -480,8 +445,8 @@ __global__ void __launch_bounds__(kUpdThreads)
     double a[2][2], b[2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      a[mt][0] = sgn * sA[kr + wm * 32 + mt * 16 + gq];
-      a[mt][1] = sgn * sA[kr + wm * 32 + mt * 16 + gq + 8];
+      a[mt][0] = -sA[kr + wm * 32 + mt * 16 + gq];
+      a[mt][1] = -sA[kr + wm * 32 + mt * 16 + gq + 8];
     }
 #pragma unroll
     for (int nt8 = 0; nt8 < 2; ++nt8) b[nt8] = sB[kr + wn * 16 + nt8 * 8 + gq];
@@ -779,11 +744,7 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   const int nb = t.nb;
   cudaError_t e = cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kUpdSmem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem);
   if (e != cudaSuccess) return e;
-  double* linv = nullptr;  // L_kk^{-1} of the current block column (panel operand)
-  if ((e = cudaMalloc(&linv, kTile * sizeof(double))) != cudaSuccess) return e;
   // Lookahead over two streams: the high-priority stream runs panel(k) and
   // the update of block column k+1 only (U1), so panel(k+1) can start while
   // the low-priority stream applies the rest of update k (U2) -- the
@@ -793,13 +754,9 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);
   cudaStream_t main_s = nullptr, side = nullptr;
-  if ((e = cudaStreamCreateWithPriority(&main_s, cudaStreamNonBlocking, greatest)) != cudaSuccess) {
-    cudaFree(linv);
-    return e;
-  }
+  if ((e = cudaStreamCreateWithPriority(&main_s, cudaStreamNonBlocking, greatest)) != cudaSuccess) return e;
   if ((e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least)) != cudaSuccess) {
     cudaStreamDestroy(main_s);
-    cudaFree(linv);
     return e;
   }
   cudaEvent_t ev_panel = nullptr, ev_u2 = nullptr, ev_fork = nullptr, ev_join = nullptr;
@@ -815,24 +772,20 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   bool u2_pending = false;
   for (int k = 0; k < nb; ++k) {
     const int m = nb - k - 1;
-    chol_diag_kernel<<<1, kDiagThreads, kDiagSmem, main_s>>>(t.tiles, k, linv, t.status);
+    chol_panel_kernel<<<std::max(1, m), kPanelThreads, 0, main_s>>>(t.tiles, nb, k, t.status);
     ++launches;
-    if (m > 0) {
-      chol_update_kernel<<<(unsigned)m, kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, k + 1, 2, linv);
-      ++launches;
-    }
     if (m == 0) break;
     // U2(k): tiles (i, j), k + 2 <= j <= i
     if (m > 1) {
       cudaEventRecord(ev_panel, main_s);
       cudaStreamWaitEvent(side, ev_panel, 0);
       chol_update_kernel<<<(unsigned)((long long)(m - 1) * m / 2), kUpdThreads, kUpdSmem, side>>>(
-          t.tiles, nb, k, k + 2, 0, nullptr);
+          t.tiles, nb, k, k + 2, 0);
       ++launches;
     }
     // U1(k): block column k + 1, after U2(k - 1) updated it
     if (u2_pending) cudaStreamWaitEvent(main_s, ev_u2, 0);
-    chol_update_kernel<<<(unsigned)m, kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, k + 1, 1, nullptr);
+    chol_update_kernel<<<(unsigned)m, kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, k + 1, 1);
     ++launches;
     u2_pending = m > 1;
     if (u2_pending) cudaEventRecord(ev_u2, side);
@@ -850,7 +803,6 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   cudaStreamSynchronize(side);
   cudaStreamDestroy(main_s);
   cudaStreamDestroy(side);
-  cudaFree(linv);
   cudaEventDestroy(ev_panel);
   cudaEventDestroy(ev_u2);
   cudaEventDestroy(ev_fork);
