@@ -109,6 +109,15 @@ ltb_status ltb_plan_create_generated_premultiplied(int rows, int cols, int nt, i
                                                    double gamma, double delta,
                                                    const ltb_opts* opts, ltb_plan** out);
 
+/* Column shard [c0, c0 + cols) of the G* plan of a generated rows x nm_total
+ * kernel: every slab is generated and premultiplied over all nm_total
+ * columns (Gamma_x couples the columns), only the shard's columns are
+ * transformed -- the per-rank G* of the distributed online phase. */
+ltb_status ltb_plan_create_generated_premultiplied_shard(int rows, int cols, int nt, int tag, uint64_t seed,
+                                                         uint64_t stream, long long nm_total, long long c0,
+                                                         double h_x, double gamma, double delta,
+                                                         const ltb_opts* opts, ltb_plan** out);
+
 /* Plan from a BTPZ1 kernel archive written by the reference (io.cpp:71-100:
  * "BTPZ1", u64 rows, cols, N_t, tag, [row][col][lag] doubles), streamed
  * slab by slab to the device (LTB_IO on a missing / bad / truncated file).
@@ -369,6 +378,22 @@ ltb_status ltb_engine_map_residual(const ltb_engine* e, ltb_scratch* s, const do
 
 /* integrate_displacement (bayes_engine.cpp:411-419): out[x] = dt_obs *
  * sum_j m[x][j] of a SpaceMajorRows field (n_rows x n_time) */
+/* ---- distributed offline phase 2 (one process per GPU, world > 1) ----
+ * form_K (bayes_engine.cpp:136-172) and factorize (:176-209) straight into
+ * the row-cyclic layout the distributed K^{-1} reads, so config 5 (n =
+ * 252,000, 254 GB) runs on a real factor.  Collective over NCCL: rank 0 gets
+ * an id with ltb_nccl_unique_id, every rank passes it to ltb_engine_set_comm
+ * (after ltb_engine_set_world).  form_K takes the GLOBAL N_m of the
+ * generated F kernel (F and its prior-premultiplied G, full, on every rank);
+ * factorize leaves each rank's block rows of L and prepares the K^{-1} apply
+ * (IPC connect as after ltb_engine_set_factor_generated).  world == 1 runs
+ * the same code without NCCL. */
+ltb_status ltb_nccl_unique_id(void* out128);
+ltb_status ltb_engine_set_comm(ltb_engine* e, const void* id128);
+ltb_status ltb_engine_form_k_generated_dist(ltb_engine* e, long long nm_total, uint64_t seed, uint64_t stream,
+                                            double h_x, double gamma, double delta, double sigma2);
+ltb_status ltb_engine_factorize_dist(ltb_engine* e);
+
 /* reindex (core.hpp:92-95, core.cpp:40-51): bijective permutation of an
  * n_rows x n_time series between TimeMajorBlocks (j * n_rows + r) and
  * SpaceMajorRows (r * n_time + j) -- bit exact (a pure permutation).  Host

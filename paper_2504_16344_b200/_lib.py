@@ -95,6 +95,14 @@ SIGNATURES = {
     "ltb_apply_sharded": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_apply_adjoint_sharded": ([_vp, _vp, _vp, _vp, C.c_int], C.c_int),
     "ltb_reindex": ([_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp], C.c_int),
+    "ltb_nccl_unique_id": ([_vp], C.c_int),
+    "ltb_plan_create_generated_premultiplied_shard": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                                       C.c_longlong, C.c_longlong, C.c_double, C.c_double,
+                                                       C.c_double, _vp, C.POINTER(_vp)], C.c_int),
+    "ltb_engine_set_comm": ([_vp, _vp], C.c_int),
+    "ltb_engine_form_k_generated_dist": ([_vp, C.c_longlong, C.c_uint64, C.c_uint64, C.c_double, C.c_double,
+                                          C.c_double, C.c_double], C.c_int),
+    "ltb_engine_factorize_dist": ([_vp], C.c_int),
 }
 
 _lib = None

@@ -1088,8 +1088,11 @@ __global__ void count_nonfinite_slab(const double* x, long long n, unsigned long
 }
 
 // F-hat columns of kernel rows [r0, r0+R) from a device slab [R][cols][nt]
-cudaError_t slab_to_fhat(ltb_plan* p, const double* slab, int r0, int R, cudaStream_t st) {
-  RfftSrc src{slab, 0, R, (long long)p->cols, 0};
+// slab: R kernel rows x src_cols columns (src_cols >= c0 + p->cols); the
+// plan's columns are slab columns c0 ..
+cudaError_t slab_to_fhat(ltb_plan* p, const double* slab, int r0, int R, long long src_cols, long long c0,
+                         cudaStream_t st) {
+  RfftSrc src{slab, 0, R, src_cols, c0};
   src.oP = R;           // logical row g = c R + rr ...
   src.oQ = p->rows;     // ... lands in F-hat column c rows + r0 + rr
   src.o0 = r0;
@@ -1112,11 +1115,14 @@ struct SlabSource {
   const double* ptr = nullptr;
   uint64_t key = 0;
   FILE* fh = nullptr;
+  long long src_cols = 0;  // generated: columns of the whole kernel (0 = the plan's)
+  long long c0 = 0;        // generated: first column of the plan (a column shard)
 };
 
 // Build p->fhat slab by slab, optionally premultiplying by Gamma_x first.
 ltb_status build_plan_slabs(ltb_plan* p, const SlabSource& src, const PriorDev* prior) {
-  const size_t row_elems = (size_t)p->cols * p->nt;
+  const long long src_cols = src.src_cols > 0 ? src.src_cols : p->cols;
+  const size_t row_elems = (size_t)src_cols * p->nt;
   // up to 64 kernel rows / 1 GB per slab: the premultiply runs one thread per
   // (row, lag) line, so larger slabs keep more of the GPU busy
   int R = (int)std::max<size_t>(1, std::min<size_t>(64, (size_t)(1u << 30) / (row_elems * 8)));
@@ -1158,10 +1164,10 @@ ltb_status build_plan_slabs(ltb_plan* p, const SlabSource& src, const PriorDev* 
     if (prior) {
       const long long lines = (long long)rr * p->nt;
       prior_premultiply_kernel<<<(unsigned)std::max(1ll, std::min(148ll * 16, (lines + 127) / 128)), 128>>>(
-          slab, rr, p->cols, p->nt, prior->ldiag, prior->lsub);
+          slab, rr, (int)src_cols, p->nt, prior->ldiag, prior->lsub);
       g_launches += 1;
     }
-    e = slab_to_fhat(p, slab, r0, rr, 0);
+    e = slab_to_fhat(p, slab, r0, rr, src_cols, src.c0, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return done(fail(LTB_CUDA, "plan build: %s", cudaGetErrorString(e)));
     g_launches += 1;
@@ -1208,7 +1214,8 @@ ltb_status plan_from_source(int rows, int cols, int nt, int tag, const SlabSourc
   }
   DeviceGuard g(p->device);
   PriorDev prior;
-  if (prior3 && (st = make_prior(cols, prior3[0], prior3[1], prior3[2], prior)) != LTB_OK) {
+  const int prior_cols = src.src_cols > 0 ? (int)src.src_cols : cols;
+  if (prior3 && (st = make_prior(prior_cols, prior3[0], prior3[1], prior3[2], prior)) != LTB_OK) {
     plan_free(p);
     return st;
   }
@@ -1279,6 +1286,23 @@ ltb_status ltb_plan_create_generated_premultiplied(int rows, int cols, int nt, i
   SlabSource src;
   src.kind = 2;
   src.key = gen_key(seed, stream);
+  const double prior[3] = {h_x, gamma, delta};
+  return plan_from_source(rows, cols, nt, tag, src, prior, opts, out);
+}
+
+ltb_status ltb_plan_create_generated_premultiplied_shard(int rows, int cols, int nt, int tag, uint64_t seed,
+                                                         uint64_t stream, long long nm_total, long long c0,
+                                                         double h_x, double gamma, double delta,
+                                                         const ltb_opts* opts, ltb_plan** out) {
+  if (!out) return fail(LTB_INVALID, "plan_create_generated_premultiplied_shard: null out");
+  *out = nullptr;
+  if (c0 < 0 || nm_total < c0 + cols)
+    return fail(LTB_DIMENSION, "generated plan: shard [%lld, %lld) outside nm_total=%lld", c0, c0 + cols, nm_total);
+  SlabSource src;
+  src.kind = 2;
+  src.key = gen_key(seed, stream);
+  src.src_cols = nm_total;
+  src.c0 = c0;
   const double prior[3] = {h_x, gamma, delta};
   return plan_from_source(rows, cols, nt, tag, src, prior, opts, out);
 }

@@ -104,6 +104,9 @@ struct ltb_engine {
   // the events, so every entry point holds this lock for its whole
   // (synchronous) duration; recursive because infer_map -> infer_and_forecast.
   std::recursive_mutex mu;
+  // distributed offline phase 2 (ltb_engine_set_comm)
+  const Nccl* nccl = nullptr;
+  ncclComm_t comm = nullptr;
 };
 
 namespace {
@@ -171,6 +174,7 @@ ltb_status ltb_engine_destroy(ltb_engine* e) {
   if (e->f_scratch) ltb_scratch_destroy(e->f_scratch);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->comm && e->nccl) e->nccl->CommDestroy(e->comm);
   release_phase3(e);
   delete e;
   return LTB_OK;
@@ -438,6 +442,108 @@ ltb_status ltb_engine_form_k_generated(ltb_engine* e, uint64_t seed, uint64_t st
   ENG_CUDA(cudaMemcpy(dg.p, df.p, cnt * sizeof(double), cudaMemcpyDeviceToDevice));
   if ((st = premultiply_device(dg.p, e->nd, e->nm, e->nt, h_x, gamma, delta)) != LTB_OK) return st;
   return form_k_dev(e, df.p, dg.p, e->nm, sigma2);
+}
+
+// ---- distributed offline phase 2 (one process per GPU) ----
+ltb_status ltb_nccl_unique_id(void* out) {
+  if (!out) return efail(LTB_INVALID, "nccl_unique_id: null argument");
+  const char* why = nullptr;
+  const Nccl* api = nccl_api(&why);
+  if (!api) return efail(LTB_CUDA, "nccl_unique_id: %s", why);
+  ncclUniqueId id;
+  const ncclResult_t r = api->GetUniqueId(&id);
+  if (r != ncclSuccess) return efail(LTB_CUDA, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  memcpy(out, &id, sizeof(id));
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_set_comm(ltb_engine* e, const void* id) {
+  EngLock lk_(e);
+  if (!e || !id) return efail(LTB_INVALID, "set_comm: null argument");
+  if (e->world == 1) return LTB_OK;  // nothing to exchange
+  const char* why = nullptr;
+  const Nccl* api = nccl_api(&why);
+  if (!api) return efail(LTB_CUDA, "set_comm: %s", why);
+  Guard gd(e->device);
+  if (e->comm) {
+    api->CommDestroy(e->comm);
+    e->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  const ncclResult_t r = api->CommInitRank(&e->comm, e->world, uid, e->rank);
+  if (r != ncclSuccess) return efail(LTB_CUDA, "ncclCommInitRank: %s", api->GetErrorString(r));
+  e->nccl = api;
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_form_k_generated_dist(ltb_engine* e, long long nm_total, uint64_t seed, uint64_t stream,
+                                            double h_x, double gamma, double delta, double sigma2) {
+  EngLock lk_(e);
+  if (!e) return efail(LTB_INVALID, "form_K: null engine");
+  if (nm_total < 1) return efail(LTB_DIMENSION, "form_K: nm_total must be >= 1");
+  if (e->world > 1 && !e->comm) return efail(LTB_STATE, "form_K: distributed engine without a communicator (set_comm)");
+  if ((long long)e->nd * e->nt > INT32_MAX / 2) return efail(LTB_CAPACITY, "form_K: n_data too large");
+  Guard gd(e->device);
+  ltb_status st = factor_prepare(e, e->nd * e->nt);
+  if (st != LTB_OK) return st;
+  const size_t cnt = (size_t)e->nd * nm_total * e->nt;
+  size_t free_b = 0, total_b = 0;
+  ENG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (2 * cnt * sizeof(double) + (256u << 20) > free_b)
+    return efail(LTB_CAPACITY, "form_K: the F and G kernels need %zu bytes, %zu free", 2 * cnt * sizeof(double),
+                 free_b);
+  DevBuf df, dg;
+  ENG_CUDA(cudaMalloc(&df.p, cnt * sizeof(double)));
+  ENG_CUDA(cudaMalloc(&dg.p, cnt * sizeof(double)));
+  ENG_CUDA(launch_gen_fill(gen_key(seed, stream), 0, (long long)cnt, df.p, 0));
+  count_launches(1);
+  ENG_CUDA(cudaMemcpy(dg.p, df.p, cnt * sizeof(double), cudaMemcpyDeviceToDevice));
+  if ((st = premultiply_device(dg.p, e->nd, (int)nm_total, e->nt, h_x, gamma, delta)) != LTB_OK) return st;
+  ENG_CUDA(cudaDeviceSynchronize());
+  ENG_CUDA(cudaEventRecord(e->ev0, 0));
+  const char* why = nullptr;
+  cudaError_t err = formk_device_dist(e->factor, df.p, dg.p, e->nd, (int)nm_total, e->nt, sigma2, e->nccl, e->comm, 0,
+                                      &why);
+  count_launches(formk_last_launches());
+  if (err != cudaSuccess)
+    return efail(LTB_CUDA, "form_K (distributed): %s", why ? why : cudaGetErrorString(err));
+  ENG_CUDA(cudaEventRecord(e->ev1, 0));
+  ENG_CUDA(cudaEventSynchronize(e->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  e->formk_ms = ms;
+  e->kformed = true;
+  return LTB_OK;
+}
+
+ltb_status ltb_engine_factorize_dist(ltb_engine* e) {
+  EngLock lk_(e);
+  if (!e) return efail(LTB_INVALID, "factorize: null engine");
+  if (!e->kformed) return efail(LTB_STATE, "engine: missing offline artifact: K (run form_K)");
+  if (e->world > 1 && !e->comm) return efail(LTB_STATE, "factorize: distributed engine without a communicator");
+  Guard gd(e->device);
+  ENG_CUDA(cudaEventRecord(e->ev0, 0));
+  int bad = -1;
+  const char* why = nullptr;
+  cudaError_t err = cholesky_dist(e->factor, e->nccl, e->comm, 0, &bad, &why);
+  count_launches(formk_last_launches());
+  e->kformed = false;  // overwritten in place (bayes_engine.cpp:180-193)
+  if (err == cudaErrorInvalidValue)
+    return efail(LTB_NUMERICAL, "factorize: K not positive definite (pivot failure in block column %d)", bad);
+  if (err != cudaSuccess) return efail(LTB_CUDA, "factorize (distributed): %s", why ? why : cudaGetErrorString(err));
+  ENG_CUDA(cudaEventRecord(e->ev1, 0));
+  ENG_CUDA(cudaEventSynchronize(e->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  e->factorize_ms = ms;
+  err = trsv_prepare_dist(e->factor, e->nccl, e->comm, 0, &why);
+  count_launches(3);
+  if (err == cudaErrorInvalidValue)
+    return efail(LTB_NUMERICAL, "set_factor: zero or non-finite diagonal in the Cholesky factor");
+  if (err != cudaSuccess) return efail(LTB_CUDA, "factorize (distributed) prepare: %s", why ? why : cudaGetErrorString(err));
+  e->factorized = true;
+  return LTB_OK;
 }
 
 ltb_status ltb_engine_factorize(ltb_engine* e) {

@@ -5,6 +5,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "ltb_common.cuh"
 #include "ltb_formk.h"
@@ -100,6 +101,10 @@ LTB_DEV void gram_load_stage(double* sA, double* sB, const double* f, const doub
 
 // Output of a lag Gram: the packed lower 64x64 tiles of K (dense == 0), or
 // a dense column-major block (dense == 1, rows x cols, leading dim ld).
+// dense == 2: the packed lower tiles of ONE rank of a row-cyclic factor
+// (block row I on rank I mod P, ltb_trsv.h); CTA row tile bi then covers this
+// rank's local block rows 2 bi and 2 bi + 1 (global I = rank + P (2 bi + h)),
+// and cum[bi] counts the column tiles of the row tiles before bi.
 struct GramOut {
   int dense;
   double* p;
@@ -107,16 +112,44 @@ struct GramOut {
   int rows, cols;  // dense extent
   int nb;          // packed: 64-blocks
   int tiles_j;     // dense: 128-wide column tiles
+  int P, rank;     // dense == 2
+  const long long* cum;
+  int npairs;
 };
 
+// tile offset of local block row li on rank r of P (ltb_trsv.cu row_off)
+__host__ __device__ inline size_t drow_off(long long li, int r, int P) {
+  return (size_t)(li * (r + 1) + (long long)P * li * (li - 1) / 2);
+}
+
+// global row of row m of CTA row tile bi
+LTB_DEV int grow(const GramOut& o, int bi, int m) {
+  if (o.dense != 2) return bi * kBM + m;
+  return (o.rank + o.P * (2 * bi + (m >> 6))) * kT + (m & 63);
+}
+
 LTB_DEV double* out_elem(const GramOut& o, int i, int j) {
+  if (o.dense == 2) {
+    const int I = i >> 6, J = j >> 6;
+    if (I >= o.nb || J > I || I % o.P != o.rank) return nullptr;
+    return o.p + (drow_off(I / o.P, o.rank, o.P) + J) * kTile + (size_t)(j & 63) * kT + (i & 63);
+  }
   if (o.dense) return (i < o.rows && j < o.cols) ? o.p + (size_t)j * o.ld + i : nullptr;
   const int I = i >> 6, J = j >> 6;
   return (I < o.nb && J <= I) ? o.p + tile_at(I, J) + (size_t)(j & 63) * kT + (i & 63) : nullptr;
 }
 
 LTB_DEV void gram_tile(const GramOut& o, long long t, int* bi, int* bj) {
-  if (o.dense) {
+  if (o.dense == 2) {
+    int lo = 0, hi = o.npairs - 1;  // largest bi with cum[bi] <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (o.cum[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    *bi = lo;
+    *bj = (int)(t - o.cum[lo]);
+  } else if (o.dense) {
     *bi = (int)(t / o.tiles_j);
     *bj = (int)(t % o.tiles_j);
   } else {
@@ -140,7 +173,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int slice = blockIdx.x % split;
   int bi, bj;
   gram_tile(o, tile, &bi, &bj);
-  const int i0 = bi * kBM, j0 = bj * kBM;
+  const int j0 = bj * kBM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // warp tile 64 (rows) x 32 (cols)
@@ -150,7 +183,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const double* rowB;
   {
     const int m = kPair ? 2 * (tid & 63) : (tid & 127);
-    const int ia = i0 + m, ib = j0 + m;
+    const int ia = grow(o, bi, m), ib = j0 + m;
     rowA = ia < na ? f + (size_t)(ia / nt) * nm * nt + ia % nt : nullptr;
     rowB = ib < nbr ? g + (size_t)(ib / nt) * nm * nt + ib % nt : nullptr;
   }
@@ -230,7 +263,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int i = i0 + wm * 64 + mt * 16 + gq + 8 * h;
+          const int i = grow(o, bi, wm * 64 + mt * 16 + gq + 8 * h);
           const int j = j0 + wn * 32 + nt8 * 8 + 2 * tq + c;
           double* dst = out_elem(o, i, j);
           if (dst) *dst = acc[mt][nt8][2 * h + c];
@@ -249,7 +282,7 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, long 
     const int m = e / kBM, c = e % kBM;
     double v = 0.0;
     for (int s = 0; s < split; ++s) v += P[(size_t)s * kBM * kBM + e];
-    double* dst = out_elem(o, bi * kBM + m, bj * kBM + c);
+    double* dst = out_elem(o, grow(o, bi, m), bj * kBM + c);
     if (dst) *dst = v;
   }
 }
@@ -330,16 +363,17 @@ constexpr int kPanelSplit = 4;                 // threads per row
 constexpr int kPerThread = kT / kPanelSplit;   // 16 register entries
 constexpr int kPanelThreads = kPanelRows * kPanelSplit;
 
-__global__ void __launch_bounds__(kPanelThreads)
-    chol_panel_kernel(double* __restrict__ tiles, int nb, int k, int* status) {
+// one CTA: diagonal block from diag_in (rows 0-63), panel tile `panel`
+// (rows 64-127, nullptr = none); L_kk to diag_out (nullptr = not this CTA),
+// L_ik back into `panel` and, if given, a copy into panel_copy
+LTB_DEV void chol_panel_cta(const double* diag_in, double* diag_out, double* panel, double* panel_copy, int k,
+                            bool report, int* status) {
   __shared__ double col[2][kPanelRows];
   __shared__ double rsq[kT];
   const int row = threadIdx.x % kPanelRows, q = threadIdx.x / kPanelRows;
-  const int ip = k + 1 + blockIdx.x;  // panel tile row (none when ip >= nb)
   const bool diag_row = row < kT;
-  const bool has_panel = ip < nb;
-  double* src = diag_row ? tiles + tile_at(k, k) + row
-                         : (has_panel ? tiles + tile_at(ip, k) + (row - kT) : nullptr);
+  const bool has_panel = panel != nullptr;
+  const double* src = diag_row ? diag_in + row : (has_panel ? panel + (row - kT) : nullptr);
   double a[kPerThread];
 #pragma unroll
   for (int t = 0; t < kPerThread; ++t) a[t] = src ? src[(kPanelSplit * t + q) * kT] : 0.0;
@@ -378,14 +412,26 @@ __global__ void __launch_bounds__(kPanelThreads)
     rsq[row] = 1.0 / sqrt(v);
   }
   __syncthreads();
-  if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(status, 0, k + 1);
-  if (diag_row ? blockIdx.x == 0 : has_panel) {
+  if (bad && report && threadIdx.x == 0) atomicCAS(status, 0, k + 1);
+  double* dst = diag_row ? (diag_out ? diag_out + row : nullptr) : (has_panel ? panel + (row - kT) : nullptr);
+  double* cpy = (!diag_row && panel_copy) ? panel_copy + (row - kT) : nullptr;
+  if (dst) {
 #pragma unroll
     for (int t = 0; t < kPerThread; ++t) {
       const int j = kPanelSplit * t + q;
-      src[j * kT] = !diag_row || j < row ? a[t] * rsq[j] : (j == row ? 1.0 / rsq[j] : 0.0);
+      const double v = !diag_row || j < row ? a[t] * rsq[j] : (j == row ? 1.0 / rsq[j] : 0.0);
+      dst[j * kT] = v;
+      if (cpy) cpy[j * kT] = v;
     }
   }
+}
+
+__global__ void __launch_bounds__(kPanelThreads)
+    chol_panel_kernel(double* __restrict__ tiles, int nb, int k, int* status) {
+  const int ip = k + 1 + blockIdx.x;  // panel tile row (none when ip >= nb)
+  double* dkk = tiles + tile_at(k, k);
+  chol_panel_cta(dkk, blockIdx.x == 0 ? dkk : nullptr, ip < nb ? tiles + tile_at(ip, k) : nullptr, nullptr, k,
+                 blockIdx.x == 0, status);
 }
 
 // ---------------------------------------------------------------------------
@@ -398,24 +444,11 @@ constexpr int kUS = kT + 4;  // 68 == 4 mod 16
 constexpr int kUpdThreads = 256;
 constexpr size_t kUpdSmem = (size_t)2 * kT * kUS * sizeof(double);
 
-__global__ void __launch_bounds__(kUpdThreads)
-    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int base, int column_only) {
+// A_ij -= L_ik L_jk^T for one tile (DMMA)
+LTB_DEV void tile_update_cta(const double* __restrict__ Lik, const double* __restrict__ Ljk, double* __restrict__ Aij) {
   extern __shared__ __align__(16) double usm[];
   double* sA = usm;
   double* sB = usm + kT * kUS;
-  int i, j;
-  if (column_only) {  // tiles (i, base), i >= base
-    i = base + (int)blockIdx.x;
-    j = base;
-  } else {  // the lower triangle of tiles from (base, base)
-    int li, lj;
-    tri_pair(blockIdx.x, &li, &lj);
-    i = base + li;
-    j = base + lj;
-  }
-  const double* Lik = tiles + tile_at(i, k);
-  const double* Ljk = tiles + tile_at(j, k);
-  double* Aij = tiles + tile_at(i, j);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
@@ -466,6 +499,25 @@ __global__ void __launch_bounds__(kUpdThreads)
           const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
           Aij[col * kT + r] = acc[mt][nt8][2 * h + c];
         }
+}
+
+
+__global__ void __launch_bounds__(kUpdThreads)
+    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int base, int column_only) {
+  int i, j;
+  if (column_only) {  // tiles (i, base), i >= base
+    i = base + (int)blockIdx.x;
+    j = base;
+  } else {  // the lower triangle of tiles from (base, base)
+    int li, lj;
+    tri_pair(blockIdx.x, &li, &lj);
+    i = base + li;
+    j = base + lj;
+  }
+  const double* Lik = tiles + tile_at(i, k);
+  const double* Ljk = tiles + tile_at(j, k);
+  double* Aij = tiles + tile_at(i, j);
+  tile_update_cta(Lik, Ljk, Aij);
 }
 
 // packed lower tiles -> column-major lower triangle
@@ -876,5 +928,229 @@ cudaError_t transpose_to(const double* X, size_t ldx, int n, int m, double* Q, c
                                                                                                      Q);
   return cudaGetLastError();
 }
+
+
+// ===========================================================================
+// Distributed offline phase 2 (one process per GPU, P ranks): form_K and the
+// tile Cholesky straight into the row-cyclic layout the distributed K^{-1}
+// reads (block row I on rank I mod P, ltb_trsv.h), NCCL for the exchanges.
+//  * form_K: each rank computes the lag Gram for its own block rows (CTA row
+//    tiles = pairs of its block rows, all columns of the lower triangle);
+//    the diagonal recurrence K(t, j) = A(t, j) + K(t-1, j-1) then runs block
+//    row by block row in order, the last row of block row I handed to the
+//    owner of I + 1 (2 MB at n = 252,000, NCCL send / recv) as the carry;
+//  * Cholesky, block column k: the owner broadcasts A_kk (32 KB); every rank
+//    forms its panel tiles L_ik = A_ik L_kk^{-T} (the one-GPU panel CTA) and
+//    all-gathers the column; every rank applies A_ij -= L_ik L_jk^T to its
+//    own rows (the one-GPU DMMA tile update).
+// Per-tile arithmetic is the one-GPU kernels', in the same order, so the
+// distributed factor equals the one-GPU factor (up to the split-k tail of
+// the lag Gram, which sums k-slices in order either way).
+// ===========================================================================
+namespace {
+
+// recurrence over block row I with carry_in = row 64 I - 1 (columns
+// 0 .. 64 I - 1) and carry_out = row 64 I + 63 (columns 0 .. 64 I + 63) of
+// F G* (sigma2 is added to the stored diagonal only, as diag_prefix_kernel);
+// thread per diagonal delta = i - j
+__global__ void dist_recur_kernel(const GramOut o, int I, int n, int nt, double sigma2,
+                                  const double* __restrict__ carry_in, double* __restrict__ carry_out) {
+  const int r0 = I * kT, rend = min(r0 + kT, n);
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < r0 + kT; d += gridDim.x * blockDim.x) {
+    int i = max(r0, d);
+    if (i >= rend) continue;
+    double prev = (i == r0 && i - d - 1 >= 0 && r0 > 0) ? carry_in[i - d - 1] : 0.0;
+    for (; i < rend; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (i + q < rend) v[q] = *out_elem(o, i + q, i + q - d);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (i + q < rend) {
+          const int ii = i + q, jj = ii - d;
+          double x = v[q];
+          if (ii % nt != 0 && jj % nt != 0) x += prev;  // the recurrence runs on F G* alone
+          *out_elem(o, ii, jj) = d == 0 ? x + sigma2 : x;
+          prev = x;
+          if (ii == r0 + kT - 1 && carry_out) carry_out[jj] = x;
+        }
+    }
+  }
+}
+
+// identity on the padding diagonal of the last block row (its owner)
+__global__ void dist_pad_identity_kernel(double* tiles, int n, int nb, int r, int P) {
+  const int i = n + threadIdx.x, I = nb - 1;
+  if (i < nb * kT) tiles[(drow_off(I / P, r, P) + I) * kTile + (size_t)(i & 63) * kT + (i & 63)] = 1.0;
+}
+
+// first block row > k owned by rank q, and how many there are
+__host__ __device__ inline int dist_first(int k, int q, int P) { return k + 1 + ((q - (k + 1)) % P + P) % P; }
+__host__ __device__ inline int dist_count(int first, int nb, int P) { return first < nb ? (nb - 1 - first) / P + 1 : 0; }
+
+__global__ void __launch_bounds__(kPanelThreads)
+    dist_panel_kernel(double* __restrict__ tiles, int r, int P, int k, int nb, const double* __restrict__ akk,
+                      int owner, double* __restrict__ sendbuf, int* status) {
+  const int first = dist_first(k, r, P), cnt = dist_count(first, nb, P);
+  const int b = blockIdx.x, i = first + P * b;
+  double* dkk = owner && b == 0 ? tiles + (drow_off(k / P, r, P) + k) * kTile : nullptr;
+  double* pt = b < cnt ? tiles + (drow_off(i / P, r, P) + k) * kTile : nullptr;
+  chol_panel_cta(akk, dkk, pt, b < cnt ? sendbuf + (size_t)b * kTile : nullptr, k, owner && b == 0, status);
+}
+
+// own rows i > k, tiles j in (k, i]: A_ij -= L_ik L_jk^T, L_jk from the
+// gathered column (rank q's rows at recv[q * cntmax + (j - first_q) / P])
+__global__ void __launch_bounds__(kUpdThreads)
+    dist_update_kernel(double* __restrict__ tiles, int r, int P, int k, int nb, const double* __restrict__ recv,
+                       int cntmax) {
+  const int first = dist_first(k, r, P), cnt = dist_count(first, nb, P);
+  const long long b = blockIdx.x;
+  int lo = 0, hi = cnt - 1;  // row a: tiles before it a (first - k) + P a (a - 1) / 2
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if ((long long)mid * (first - k) + (long long)P * mid * (mid - 1) / 2 <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const int a = lo, i = first + P * a;
+  const int j = k + 1 + (int)(b - ((long long)a * (first - k) + (long long)P * a * (a - 1) / 2));
+  const int q = j % P, fq = dist_first(k, q, P);
+  const double* Lik = tiles + (drow_off(i / P, r, P) + k) * kTile;
+  const double* Ljk = recv + ((size_t)q * cntmax + (j - fq) / P) * kTile;
+  double* Aij = tiles + (drow_off(i / P, r, P) + j) * kTile;
+  tile_update_cta(Lik, Ljk, Aij);
+}
+
+#define NCCL_TRY(expr)                                                            \
+  do {                                                                            \
+    ncclResult_t r_ = (expr);                                                     \
+    if (r_ != ncclSuccess) {                                                      \
+      if (err) *err = api->GetErrorString(r_);                                    \
+      return cudaErrorUnknown;                                                    \
+    }                                                                             \
+  } while (0)
+
+struct DevMem {
+  void* p = nullptr;
+  ~DevMem() { cudaFree(p); }
+};
+
+}  // namespace
+
+cudaError_t formk_device_dist(TriFactor& t, const double* f, const double* g, int nd, int nm, int nt, double sigma2,
+                              const Nccl* api, ncclComm_t comm, cudaStream_t st, const char** err) {
+  const int n = t.n, nb = t.nb, P = t.P, r = t.rank;
+  if (n != nd * nt || nm < 1 || (P > 1 && (!api || !comm))) return cudaErrorInvalidValue;
+  const int nloc = r < nb ? (nb - 1 - r) / P + 1 : 0, npairs = (nloc + 1) / 2;
+  g_last_launches = 0;
+  GramOut o{};
+  o.dense = 2;
+  o.p = t.tiles;
+  o.nb = nb;
+  o.P = P;
+  o.rank = r;
+  o.npairs = npairs;
+  std::vector<long long> cum(npairs + 1, 0);
+  for (int bi = 0; bi < npairs; ++bi) {
+    const int I1 = r + P * (2 * bi + 1), Imax = I1 < nb ? I1 : r + P * 2 * bi;
+    cum[bi + 1] = cum[bi] + ((long long)kT * Imax + kT - 1) / kBM + 1;
+  }
+  DevMem dcum, cin, cout;
+  cudaError_t e;
+  if ((e = cudaMalloc(&dcum.p, sizeof(long long) * (npairs + 1))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(dcum.p, cum.data(), sizeof(long long) * (npairs + 1), cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return e;
+  o.cum = static_cast<const long long*>(dcum.p);
+  if (npairs > 0 && (e = lag_gram(f, n, g, n, nm, nt, o, cum[npairs], st)) != cudaSuccess) return e;
+  // the recurrence, block row by block row, carries handed to the next owner
+  if ((e = cudaMalloc(&cin.p, sizeof(double) * (size_t)nb * kT)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&cout.p, sizeof(double) * (size_t)nb * kT)) != cudaSuccess) return e;
+  double* ci = static_cast<double*>(cin.p);
+  double* co = static_cast<double*>(cout.p);
+  for (int li = 0; li < nloc; ++li) {
+    const int I = r + P * li;
+    if (I > 0 && P > 1) NCCL_TRY(api->Recv(ci, (size_t)kT * I, ncclDouble, (I - 1) % P, comm, st));
+    const int diags = kT * I + kT;
+    dist_recur_kernel<<<(unsigned)std::max(1, std::min(148 * 4, (diags + 255) / 256)), 256, 0, st>>>(
+        o, I, n, nt, sigma2, ci, co);
+    ++g_last_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (I + 1 < nb) {
+      if (P > 1) NCCL_TRY(api->Send(co, (size_t)kT * I + kT, ncclDouble, (I + 1) % P, comm, st));
+      else std::swap(ci, co);
+    }
+  }
+  if ((nb - 1) % P == r && nb * kT > n) {
+    dist_pad_identity_kernel<<<1, kT, 0, st>>>(t.tiles, n, nb, r, P);
+    ++g_last_launches;
+  }
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the temporaries above are freed on return
+  return e;
+}
+
+cudaError_t cholesky_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaStream_t st, int* bad_block,
+                          const char** err) {
+  const int nb = t.nb, P = t.P, r = t.rank;
+  if (P > 1 && (!api || !comm)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(dist_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kUpdSmem);
+  if (e != cudaSuccess) return e;
+  const int cnt0 = (nb + P - 1) / P;  // bound on any rank's rows > k
+  DevMem akk, sendb, recvb, stat;
+  if ((e = cudaMalloc(&akk.p, sizeof(double) * kTile)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&sendb.p, sizeof(double) * kTile * (size_t)cnt0)) != cudaSuccess) return e;
+  if (P > 1 && (e = cudaMalloc(&recvb.p, sizeof(double) * kTile * (size_t)cnt0 * P)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&stat.p, sizeof(int) * P)) != cudaSuccess) return e;
+  double* a = static_cast<double*>(akk.p);
+  double* sb = static_cast<double*>(sendb.p);
+  double* rb = P > 1 ? static_cast<double*>(recvb.p) : sb;
+  cudaMemsetAsync(t.status, 0, sizeof(int), st);
+  g_last_launches = 0;
+  for (int k = 0; k < nb; ++k) {
+    const int owner = k % P;
+    if (r == owner &&
+        (e = cudaMemcpyAsync(a, t.tiles + (drow_off(k / P, r, P) + k) * kTile, sizeof(double) * kTile,
+                             cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return e;
+    if (P > 1) NCCL_TRY(api->Broadcast(a, a, kTile, ncclDouble, owner, comm, st));
+    const int cnt = dist_count(dist_first(k, r, P), nb, P);
+    const int grid = cnt > 0 ? cnt : (r == owner ? 1 : 0);
+    if (grid) {
+      dist_panel_kernel<<<grid, kPanelThreads, 0, st>>>(t.tiles, r, P, k, nb, a, r == owner, sb, t.status);
+      ++g_last_launches;
+    }
+    if (k == nb - 1) break;
+    int cntmax = 0;
+    for (int q = 0; q < P; ++q) cntmax = std::max(cntmax, dist_count(dist_first(k, q, P), nb, P));
+    if (P > 1) NCCL_TRY(api->AllGather(sb, rb, (size_t)cntmax * kTile, ncclDouble, comm, st));
+    const int first = dist_first(k, r, P);
+    const long long tiles = (long long)cnt * (first - k) + (long long)P * cnt * (cnt - 1) / 2;
+    if (tiles > 0) {
+      dist_update_kernel<<<(unsigned)tiles, kUpdThreads, kUpdSmem, st>>>(t.tiles, r, P, k, nb, rb,
+                                                                          P > 1 ? cntmax : cnt0);
+      ++g_last_launches;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // every rank learns of a failed pivot (only the owner's CTA reports it)
+  int* sp = static_cast<int*>(stat.p);
+  if (P > 1) NCCL_TRY(api->AllGather(t.status, sp, 1, ncclInt, comm, st));
+  else if ((e = cudaMemcpyAsync(sp, t.status, sizeof(int), cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+  std::vector<int> h(P, 0);
+  if ((e = cudaMemcpyAsync(h.data(), sp, sizeof(int) * P, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  int bad = 0;
+  for (int v : h) bad = (v && (!bad || v < bad)) ? v : bad;
+  cudaMemsetAsync(t.status, 0, sizeof(int), st);
+  if (bad) {
+    if (bad_block) *bad_block = bad - 1;
+    return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+#undef NCCL_TRY
 
 }  // namespace ltb

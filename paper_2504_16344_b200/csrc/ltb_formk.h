@@ -22,6 +22,7 @@
 
 #include <cuda_runtime.h>
 
+#include "ltb_nccl.h"
 #include "ltb_trsv.h"
 
 namespace ltb {
@@ -58,5 +59,16 @@ cudaError_t qoi_covariance(const double* P, const double* YtY, int m, double* gp
 cudaError_t symmetrize(double* A, int m, cudaStream_t st);
 // Q (m x n, column-major, ld m) = X^T
 cudaError_t transpose_to(const double* X, size_t ldx, int n, int m, double* Q, cudaStream_t st);
+
+// ---- distributed (t.P ranks, one process per GPU; t from trsv_alloc(t, n, P, rank)) ----
+// form_K into this rank's block rows: f, g are the FULL kernels [nd][nm][nt]
+// on every rank; collective over comm (the recurrence carries).  P == 1
+// runs the same code without NCCL.
+cudaError_t formk_device_dist(TriFactor& t, const double* f, const double* g, int nd, int nm, int nt, double sigma2,
+                              const Nccl* api, ncclComm_t comm, cudaStream_t st, const char** err);
+// in-place K -> L over the ranks (collective); cudaErrorInvalidValue + bad_block
+// on every rank when K is not positive definite
+cudaError_t cholesky_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaStream_t st, int* bad_block,
+                          const char** err);
 
 }  // namespace ltb

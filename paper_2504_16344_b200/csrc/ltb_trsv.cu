@@ -791,14 +791,22 @@ LTB_DEV void stage_tile(bool gen, const double* tiles, uint64_t key, double scal
 }
 
 // one CTA per diagonal tile, thread c solves L_II x = e_c
+// diag_all (distributed factor): the all-gathered diagonal tiles, tile I at
+// slot (I mod P) cntd + I / P; else the packed single-rank tiles / generated
 __global__ void __launch_bounds__(64) invert_diag_kernel(bool gen, const double* __restrict__ tiles,
                                                          uint64_t key, double scale, int n,
-                                                         double* __restrict__ dinv, int* status) {
+                                                         double* __restrict__ dinv, int* status,
+                                                         const double* __restrict__ diag_all, int cntd, int P) {
   extern __shared__ double inv_smem[];
   double* sL = inv_smem;               // kTB * kPad
   double* sX = inv_smem + kTB * kPad;  // kTB * kPad
   const int I = blockIdx.x, c = threadIdx.x;
-  stage_tile(gen, tiles, key, scale, n, I, I, sL);
+  if (diag_all) {
+    const double* T = diag_all + ((size_t)(I % P) * cntd + I / P) * kTile;
+    for (int e = c; e < kTile; e += kTB) sL[(e >> 6) * kPad + (e & 63)] = T[e];
+  } else {
+    stage_tile(gen, tiles, key, scale, n, I, I, sL);
+  }
   __syncthreads();
   for (int i = 0; i < kTB; ++i) {
     double s = (i == c) ? 1.0 : 0.0;
@@ -850,6 +858,62 @@ __global__ void __launch_bounds__(256) chain_tiles_kernel(bool gen, const double
     }
     C[chain_idx(look, I, k - 1, i, jj)] = s;
   }
+}
+
+// ---- a real distributed factor (ltb_formk.h cholesky_dist): dinv for every
+// block from the all-gathered diagonal tiles, the chain tiles computed by the
+// owner of each L tile and gathered on rank 0 ----
+__global__ void pack_diag_kernel(const double* __restrict__ tiles, int r, int P, double* __restrict__ out) {
+  const int li = blockIdx.x, I = r + P * li;
+  const double* T = tiles + (row_off(li, r, P) + (size_t)I) * kTile;
+  for (int e = threadIdx.x; e < kTile; e += blockDim.x) out[(size_t)li * kTile + e] = T[e];
+}
+
+// grid (nloc, look, 2): own row R, term k = blockIdx.y + 1, J = R - k:
+//   dir 0: Dinv_RR L_{R,J}            (= mf[R][k-1])
+//   dir 1: Dinv_JJ^T L_{R,J}^T        (= mb[J][k-1])
+// into out[((li * 2 + dir) * look + k - 1)] as plain column-major tiles
+__global__ void __launch_bounds__(256) chain_tiles_dist_kernel(const double* __restrict__ tiles, int r, int P,
+                                                               const double* __restrict__ dinv, int look,
+                                                               double* __restrict__ out) {
+  extern __shared__ double ct_smem[];
+  double* sA = ct_smem;
+  double* sB = ct_smem + kTB * kPad;
+  const int li = blockIdx.x, k = blockIdx.y + 1, dir = blockIdx.z;
+  const int R = r + P * li, J = R - k;
+  double* C = out + ((size_t)(li * 2 + dir) * look + k - 1) * kTile;
+  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6;
+  if (J < 0) {
+    for (int e = tid; e < kTile; e += blockDim.x) C[e] = 0.0;
+    return;
+  }
+  const double* A = dinv + (size_t)(dir == 0 ? R : J) * kTile;
+  const double* T = tiles + (row_off(li, r, P) + (size_t)J) * kTile;
+  for (int e = tid; e < kTile; e += blockDim.x) {
+    sA[(e >> 6) * kPad + (e & 63)] = A[e];
+    sB[(e >> 6) * kPad + (e & 63)] = T[e];
+  }
+  __syncthreads();
+  for (int jj = 16 * q; jj < 16 * q + 16; ++jj) {
+    double sum = 0.0;
+    if (dir == 0) {
+      for (int l = 0; l < kTB; ++l) sum = fma(sA[l * kPad + i], sB[jj * kPad + l], sum);
+    } else {
+      for (int l = 0; l < kTB; ++l) sum = fma(sA[i * kPad + l], sB[l * kPad + jj], sum);
+    }
+    C[jj * kTB + i] = sum;
+  }
+}
+
+// rank 0: rank q's chain tiles into mf / mb (chain_idx layout)
+__global__ void chain_scatter_kernel(const double* __restrict__ buf, int q, int P, int look, double* __restrict__ mf,
+                                     double* __restrict__ mb) {
+  const int li = blockIdx.x, k = blockIdx.y + 1, dir = blockIdx.z;
+  const int R = q + P * li, I = dir == 0 ? R : R - k;
+  if (I < 0) return;
+  const double* C = buf + ((size_t)(li * 2 + dir) * look + k - 1) * kTile;
+  double* M = dir == 0 ? mf : mb;
+  for (int e = threadIdx.x; e < kTile; e += blockDim.x) M[chain_idx(look, I, k - 1, e & 63, e >> 6)] = C[e];
 }
 
 constexpr int kMaxDevices = 64;
@@ -917,7 +981,7 @@ cudaError_t prepare(TriFactor& t, bool gen, uint64_t key, double scale, cudaStre
   const int smem = 2 * kTB * kPad * (int)sizeof(double);
   cudaFuncSetAttribute(invert_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(chain_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  invert_diag_kernel<<<t.nb, kTB, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv, t.status);
+  invert_diag_kernel<<<t.nb, kTB, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv, t.status, nullptr, 0, 1);
   if (t.rank == 0)
     chain_tiles_kernel<<<dim3(t.nb, t.look, 2), 256, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv,
                                                                    t.mf, t.mb, t.nb, t.look);
@@ -1055,6 +1119,72 @@ cudaError_t trsv_setup_generated(TriFactor& t, uint64_t seed, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return prepare(t, true, key, scale, st);
+}
+
+cudaError_t trsv_prepare_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaStream_t st, const char** err) {
+  const int nb = t.nb, P = t.P, r = t.rank, L = t.look;
+  if (P > 1 && (!api || !comm)) return cudaErrorInvalidValue;
+  auto nloc_of = [&](int q) { return q < nb ? (nb - 1 - q) / P + 1 : 0; };
+  const int nloc = nloc_of(r), cntd = (nb + P - 1) / P;
+  const int smem = 2 * kTB * kPad * (int)sizeof(double);
+  cudaFuncSetAttribute(invert_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(chain_tiles_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  double *sendd = nullptr, *alld = nullptr, *cbuf = nullptr, *rbuf = nullptr;
+  auto done = [&](cudaError_t e) {
+    cudaStreamSynchronize(st);
+    cudaFree(sendd);
+    cudaFree(alld);
+    cudaFree(cbuf);
+    cudaFree(rbuf);
+    return e;
+  };
+  auto nccl_fail = [&](ncclResult_t rr) {
+    if (err) *err = api->GetErrorString(rr);
+    return done(cudaErrorUnknown);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&sendd, sizeof(double) * kTile * (size_t)cntd)) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&alld, sizeof(double) * kTile * (size_t)cntd * P)) != cudaSuccess) return done(e);
+  if (nloc) pack_diag_kernel<<<nloc, 256, 0, st>>>(t.tiles, r, P, sendd);
+  if (P > 1) {
+    ncclResult_t rr = api->AllGather(sendd, alld, (size_t)cntd * kTile, ncclDouble, comm, st);
+    if (rr != ncclSuccess) return nccl_fail(rr);
+  } else if ((e = cudaMemcpyAsync(alld, sendd, sizeof(double) * kTile * cntd, cudaMemcpyDeviceToDevice, st)) !=
+             cudaSuccess) {
+    return done(e);
+  }
+  invert_diag_kernel<<<nb, kTB, smem, st>>>(false, nullptr, 0, 0.0, t.n, t.dinv, t.status, alld, cntd, P);
+  // chain tiles of this rank's L tiles, gathered on rank 0
+  const size_t per = (size_t)2 * L * kTile;
+  if ((e = cudaMalloc(&cbuf, sizeof(double) * per * std::max(1, nloc))) != cudaSuccess) return done(e);
+  if (nloc) chain_tiles_dist_kernel<<<dim3(nloc, L, 2), 256, smem, st>>>(t.tiles, r, P, t.dinv, L, cbuf);
+  if (r == 0) {
+    cudaMemsetAsync(t.mf, 0, sizeof(double) * (size_t)nb * L * kTile, st);
+    cudaMemsetAsync(t.mb, 0, sizeof(double) * (size_t)nb * L * kTile, st);
+    if (nloc) chain_scatter_kernel<<<dim3(nloc, L, 2), 256, 0, st>>>(cbuf, 0, P, L, t.mf, t.mb);
+    if (P > 1 && (e = cudaMalloc(&rbuf, sizeof(double) * per * std::max(1, nloc_of(1)))) != cudaSuccess) return done(e);
+  }
+  for (int q = 1; q < P; ++q) {
+    const int nq = nloc_of(q);
+    if (!nq) continue;
+    if (r == q) {
+      ncclResult_t rr = api->Send(cbuf, per * nq, ncclDouble, 0, comm, st);
+      if (rr != ncclSuccess) return nccl_fail(rr);
+    } else if (r == 0) {
+      ncclResult_t rr = api->Recv(rbuf, per * nq, ncclDouble, q, comm, st);
+      if (rr != ncclSuccess) return nccl_fail(rr);
+      chain_scatter_kernel<<<dim3(nq, L, 2), 256, 0, st>>>(rbuf, q, P, L, t.mf, t.mb);
+    }
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return done(e);
+  int h = 0;
+  if ((e = cudaMemcpyAsync(&h, t.status, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return done(e);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(e);
+  if (h) {
+    cudaMemset(t.status, 0, sizeof(int));
+    return done(cudaErrorInvalidValue);
+  }
+  return done(cudaSuccess);
 }
 
 cudaError_t trsv_ipc_handle(const TriFactor& t, cudaIpcMemHandle_t* out) {

@@ -9,6 +9,8 @@
 
 #include <mutex>
 
+#include "ltb_nccl.h"
+
 namespace ltb {
 
 constexpr int kTB = 64;        // factor tile edge
@@ -59,6 +61,10 @@ cudaError_t trsv_prepare_packed(TriFactor& t, cudaStream_t st);
 // any P: pack this rank's rows of the synthetic factor (ltb_gen.cuh
 // gen_factor_entry) and build dinv / chain tiles from regenerated tiles
 cudaError_t trsv_setup_generated(TriFactor& t, uint64_t seed, cudaStream_t st);
+// A real distributed factor in t.tiles (ltb_formk.h cholesky_dist): dinv for
+// every block from the all-gathered diagonal tiles, chain tiles computed by the
+// owner of each L tile and gathered on rank 0 (collective over comm).
+cudaError_t trsv_prepare_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaStream_t st, const char** err);
 // P > 1: exchange `recv` (CUDA IPC); handles[p] for every rank
 cudaError_t trsv_ipc_handle(const TriFactor& t, cudaIpcMemHandle_t* out);
 cudaError_t trsv_connect(TriFactor& t, const cudaIpcMemHandle_t* handles);

@@ -114,14 +114,37 @@ class InferenceEngine:
         ``torch.distributed`` (collective)."""
         L = _lib.load()
         check(L.ltb_engine_set_factor_generated(self._h, self.n_data(), seed))
-        if self.world > 1:
-            import torch.distributed as dist
-            mine = (C.c_char * 64)()
-            check(L.ltb_engine_ipc_handle(self._h, mine))
-            handles = [None] * self.world
-            dist.all_gather_object(handles, bytes(mine), group=group)
-            blob = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
-            check(L.ltb_engine_connect(self._h, blob))
+        self._connect(group)
+
+    def _connect(self, group=None):
+        """Distributed K^{-1}: swap the CUDA IPC handles of the ranks' receive
+        buffers (collective)."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        L = _lib.load()
+        mine = (C.c_char * 64)()
+        check(L.ltb_engine_ipc_handle(self._h, mine))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(mine), group=group)
+        blob = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
+        check(L.ltb_engine_connect(self._h, blob))
+
+    def _ensure_comm(self, group=None):
+        """NCCL communicator of the distributed offline phase: rank 0's id
+        broadcast over ``torch.distributed`` (collective, once)."""
+        if self.world == 1 or getattr(self, "_comm", False):
+            return
+        import torch.distributed as dist
+        L = _lib.load()
+        buf = (C.c_char * 128)()
+        if self.rank == 0:
+            check(L.ltb_nccl_unique_id(buf))
+        obj = [bytes(buf) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        blob = (C.c_char * 128).from_buffer_copy(obj[0])
+        check(L.ltb_engine_set_comm(self._h, blob))
+        self._comm = True
 
     # ---- offline phase 2 on the device (bayes_engine.cpp:136-209) ----
     def form_K(self, f_kernel, g_kernel=None, prior=None, sigma2=0.0):
@@ -146,15 +169,34 @@ class InferenceEngine:
         p3 = (C.c_double * 3)(*prior) if prior is not None else None
         check(_lib.load().ltb_engine_form_k(self._h, pf, pg, p3, rows, cols, nt, float(sigma2), kind))
 
-    def form_K_generated(self, seed, stream, prior, sigma2):
+    def form_K_generated(self, seed, stream, prior, sigma2, nm_total=None, distributed=None, group=None):
         """form_K of the generated kernel (ltb_plan_create_generated's) and its
-        premultiplied G; prior = (h_x, gamma, delta)."""
+        premultiplied G; prior = (h_x, gamma, delta).  Distributed engines
+        (world > 1, or ``distributed=True`` to run that code path on one GPU)
+        form their block rows of K collectively; ``nm_total`` is the global
+        N_m of the generated kernel (default: this engine's plan columns)."""
         h_x, gamma, delta = prior
+        dist_path = self.world > 1 if distributed is None else bool(distributed)
+        if dist_path:
+            self._ensure_comm(group)
+            nm = self.n_space if nm_total is None else int(nm_total)
+            check(_lib.load().ltb_engine_form_k_generated_dist(self._h, nm, int(seed), int(stream), float(h_x),
+                                                               float(gamma), float(delta), float(sigma2)))
+            self._dist_k = True
+            return
         check(_lib.load().ltb_engine_form_k_generated(self._h, int(seed), int(stream), float(h_x),
                                                       float(gamma), float(delta), float(sigma2)))
+        self._dist_k = False
 
-    def factorize(self):
-        """In-place Cholesky of K (bayes_engine.cpp:176-209)."""
+    def factorize(self, group=None):
+        """In-place Cholesky of K (bayes_engine.cpp:176-209); after a
+        distributed form_K, the distributed factorisation (collective) and the
+        IPC hand-shake of the distributed K^{-1}."""
+        if getattr(self, "_dist_k", False):
+            check(_lib.load().ltb_engine_factorize_dist(self._h))
+            self._dist_k = False
+            self._connect(group)
+            return
         check(_lib.load().ltb_engine_factorize(self._h))
 
     def offline_ms(self):

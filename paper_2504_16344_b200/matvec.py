@@ -287,15 +287,22 @@ class MatvecPlan:
 
     @classmethod
     def generated_premultiplied(cls, rows, cols, nt, seed, prior, tag=KernelTag.F, stream=None,
-                                device=None, unit_cols=0):
-        """G* plan of the device-generated F kernel (all columns)."""
+                                device=None, unit_cols=0, nm_total=None, c0=0):
+        """G* plan of the device-generated F kernel: all columns, or (with
+        ``nm_total``) the column shard [c0, c0 + cols) of a rows x nm_total
+        kernel (premultiplied over all of its columns)."""
         self = cls.__new__(cls)
         h = C.c_void_p()
         opts = _opts(device, unit_cols)
         stream = int(tag) + 1 if stream is None else stream
         hx, gamma, delta = (float(v) for v in prior)
-        check(_lib.load().ltb_plan_create_generated_premultiplied(
-            rows, cols, nt, int(tag), seed, stream, hx, gamma, delta, C.byref(opts), C.byref(h)))
+        if nm_total is None:
+            check(_lib.load().ltb_plan_create_generated_premultiplied(
+                rows, cols, nt, int(tag), seed, stream, hx, gamma, delta, C.byref(opts), C.byref(h)))
+        else:
+            check(_lib.load().ltb_plan_create_generated_premultiplied_shard(
+                rows, cols, nt, int(tag), seed, stream, int(nm_total), int(c0), hx, gamma, delta, C.byref(opts),
+                C.byref(h)))
         self._h = h
         self._dims()
         return self

@@ -27,3 +27,22 @@ def test_distributed_online_phase():
                        capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "PASS" in r.stdout
+
+
+def test_distributed_offline_phase_real_factor():
+    """form_K + factorize distributed over the GPUs (NCCL), then the online
+    phase on that real factor, against the one-GPU path."""
+    import torch
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", str(world), "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), os.path.join(HERE, "dist_offline_check.py")],
+                       capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "PASS" in r.stdout
