@@ -65,3 +65,18 @@ def test_sharded_premultiplied_plan(ltb):
         assert orc.rel_err(got, ref[c0:c1]) <= 1e-14
     g = orc.prior_premultiply(orc.gen_kernel(seed, nd, nm, nt, stream=1), *PRIOR)
     assert orc.rel_err(ref.ravel(), orc.OraclePlan(g).apply_adjoint(d)) <= 1e-12
+
+
+def test_distributed_path_not_positive_definite(ltb):
+    """A K that is not SPD (sigma2 far below zero) fails the distributed
+    factorisation with NumericalError, as the one-GPU path (bayes_engine.cpp:
+    176-209 throws on a failed dpotrf / LLT)."""
+    nd, nm, nt, seed = 6, 64, 32, 3
+    pg = ltb.MatvecPlan.generated_premultiplied(nd, nm, nt, seed, PRIOR)
+    eng = ltb.InferenceEngine(pg)
+    eng.form_K_generated(seed, 1, PRIOR, -1e6, distributed=True)
+    with pytest.raises(ltb.NumericalError):
+        eng.factorize()
+    with pytest.raises(ltb.StateError):  # K was consumed; no factor
+        eng.infer_raw(np.zeros(nd * nt), np.empty(nm * nt))
+    eng.close()
