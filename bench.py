@@ -823,7 +823,8 @@ def nccl_env():
     """Communicator init lines (NCCL_DEBUG=INFO, subsystem INIT: nranks,
     rings / NVLS) go to a per-process file, so stdout stays the one JSON
     line; nccl_init_lines() echoes them to stderr and into the line."""
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":  # INFO prints the version line too
+        os.environ["NCCL_DEBUG"] = "INFO"
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ltb_nccl.%h.%p.log")
 
@@ -838,6 +839,9 @@ def nccl_init_lines():
                 lines += fh.read().splitlines()
         except OSError:
             pass
+    if not lines:
+        print("bench: no NCCL debug file matching %s (NCCL_DEBUG=%s)" % (pat, os.environ.get("NCCL_DEBUG")),
+              file=sys.stderr)
     for ln in lines:
         print(ln, file=sys.stderr)
     keys = ("nRanks", "NVLS", "comm 0x", "Init COMPLETE", "Connected all")
