@@ -350,80 +350,168 @@ __global__ void pad_identity_kernel(double* tiles, int n, int nb) {
 
 // ---------------------------------------------------------------------------
 // (3) tile Cholesky.  Panel step k: one CTA per panel tile row holds
-// [A_kk; A_ik] (128 rows x 64); thread (row, q) keeps the row's 16 entries
-// j = 4 t + q in registers.  Column c: the owners of column c publish a_rc
-// to shared memory, one barrier, then every row r > c eliminates
-// a_rj -= (a_rc / d_c) a_jc (c < j, j <= r on the diagonal block) from the
-// broadcast column (d_c = a_cc).  Finally L_rj = a_rj / sqrt(d_j),
-// L_jj = sqrt(d_j).  CTA 0 writes L_kk (strict upper zeroed), every CTA its
-// panel tile L_ik = A_ik L_kk^{-T}.
+// X = [A_kk; A_ik] (128 rows x 64, column-major in shared memory, column
+// stride 132 == 4 mod 16) and factors it blocked by 16 columns: for column
+// block b,
+//   (1) warp 0 factors the 16 x 16 diagonal block in registers (lane l owns
+//       row 16 b + l; column broadcasts by shuffle, no CTA barrier),
+//   (2) the rows below it (in A_kk and A_ik) solve against it, one thread
+//       per row (forward substitution, the diagonal block read as shared
+//       broadcasts),
+//   (3) the trailing columns are updated with DMMA (m16n8k4, k = 16).
+// 3 barriers per column block instead of one per column.  CTA 0 writes L_kk
+// (strict upper zeroed), every CTA its panel tile L_ik = A_ik L_kk^{-T}.
 // ---------------------------------------------------------------------------
 constexpr int kPanelRows = 2 * kT;
-constexpr int kPanelSplit = 4;                 // threads per row
-constexpr int kPerThread = kT / kPanelSplit;   // 16 register entries
-constexpr int kPanelThreads = kPanelRows * kPanelSplit;
+constexpr int kPanelThreads = 256;
+constexpr int kXS = kPanelRows + 4;  // 132
+constexpr int kPB = 16;              // column block
+constexpr size_t kPanelSmem = (size_t)kT * kXS * sizeof(double) + kT * sizeof(double);
+#ifdef LTB_PANEL_STAMPS  // tools/probes/panel_probe.cu only
+__device__ long long g_pstamp[32];
+#define PSTAMP(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_pstamp[i] = clock64()
+#else
+#define PSTAMP(i)
+#endif
 
 // one CTA: diagonal block from diag_in (rows 0-63), panel tile `panel`
 // (rows 64-127, nullptr = none); L_kk to diag_out (nullptr = not this CTA),
 // L_ik back into `panel` and, if given, a copy into panel_copy
 LTB_DEV void chol_panel_cta(const double* diag_in, double* diag_out, double* panel, double* panel_copy, int k,
                             bool report, int* status) {
-  __shared__ double col[2][kPanelRows];
-  __shared__ double rsq[kT];
-  const int row = threadIdx.x % kPanelRows, q = threadIdx.x / kPanelRows;
-  const bool diag_row = row < kT;
-  const bool has_panel = panel != nullptr;
-  const double* src = diag_row ? diag_in + row : (has_panel ? panel + (row - kT) : nullptr);
-  double a[kPerThread];
+  extern __shared__ __align__(16) double psm[];
+  double* X = psm;              // X[c * kXS + r]
+  double* rinv = psm + kT * kXS;  // 1 / L_cc
+  __shared__ int bad_any;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) bad_any = 0;
+  PSTAMP(0);
+  {
+    // thread: rows r, r + 1 (r = 2 (tid & 63)) of columns tid / 64 + 4 q; all
+    // 16 loads in flight before the shared stores
+    const int r = 2 * (tid & 63), c0 = tid >> 6;
+    const double* src = r < kT ? diag_in + r : (panel ? panel + r - kT : nullptr);
+    double2 v[kT / 4];
 #pragma unroll
-  for (int t = 0; t < kPerThread; ++t) a[t] = src ? src[(kPanelSplit * t + q) * kT] : 0.0;
-  bool bad = false;
-  const int jmax = diag_row ? row : kT - 1;
-  for (int c = 0; c < kT; ++c) {
-    if (q == (c & (kPanelSplit - 1))) {
-      double v = 0.0;
+    for (int q = 0; q < kT / 4; ++q)
+      v[q] = src ? *reinterpret_cast<const double2*>(src + (c0 + 4 * q) * kT) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int t = 0; t < kPerThread; ++t)
-        if (kPanelSplit * t + q == c) v = a[t];
-      col[c & 1][row] = v;
-    }
-    __syncthreads();
-    double d = col[c & 1][c];
-    if (!(d > 0.0) || !isfinite(d)) {
-      bad = true;
-      d = 1.0;
-    }
-    if (row > c) {
-      const double lic = col[c & 1][row] / d;
-#pragma unroll
-      for (int t = 0; t < kPerThread; ++t) {
-        const int j = kPanelSplit * t + q;
-        if (j > c && j <= jmax) a[t] = fma(-lic, col[c & 1][j], a[t]);
-      }
-    }
-  }
-  // publish the pivots: owner (j, j % 4) of a_jj
-  if (diag_row && q == (row & (kPanelSplit - 1))) {
-    double v = 1.0;
-#pragma unroll
-    for (int t = 0; t < kPerThread; ++t)
-      if (kPanelSplit * t + q == row) v = a[t];
-    if (!(v > 0.0) || !isfinite(v)) v = 1.0;
-    rsq[row] = 1.0 / sqrt(v);
+    for (int q = 0; q < kT / 4; ++q) *reinterpret_cast<double2*>(X + (c0 + 4 * q) * kXS + r) = v[q];
   }
   __syncthreads();
-  if (bad && report && threadIdx.x == 0) atomicCAS(status, 0, k + 1);
-  double* dst = diag_row ? (diag_out ? diag_out + row : nullptr) : (has_panel ? panel + (row - kT) : nullptr);
-  double* cpy = (!diag_row && panel_copy) ? panel_copy + (row - kT) : nullptr;
-  if (dst) {
+  PSTAMP(1);
+#pragma unroll 1
+  for (int cb = 0; cb < kT; cb += kPB) {
+    // (1) the diagonal block, rows / columns cb .. cb + 15: unscaled
+    // elimination a_rj -= a_rc (a_jc / a_cc) (the column's shuffles do not
+    // wait for this step's reciprocal), then L_rc = a_rc / sqrt(a_cc)
+    if (warp == 0) {
+      const int l = lane & 15, r = cb + l;
+      double d[kPB];
 #pragma unroll
-    for (int t = 0; t < kPerThread; ++t) {
-      const int j = kPanelSplit * t + q;
-      const double v = !diag_row || j < row ? a[t] * rsq[j] : (j == row ? 1.0 / rsq[j] : 0.0);
-      dst[j * kT] = v;
-      if (cpy) cpy[j * kT] = v;
+      for (int j = 0; j < kPB; ++j) d[j] = X[(cb + j) * kXS + r];
+      bool bad = false;
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) {
+        double col[kPB];  // a_jc, j > c (unscaled, from lane j)
+#pragma unroll
+        for (int j = 0; j < kPB; ++j)
+          if (j >= c) col[j] = __shfl_sync(0xffffffffu, d[c], j);
+        double piv = col[c];
+        if (!(piv > 0.0) || !isfinite(piv)) {
+          bad = true;
+          piv = 1.0;
+        }
+        const double f = l > c ? d[c] * (1.0 / piv) : 0.0;
+#pragma unroll
+        for (int j = 1; j < kPB; ++j)
+          if (j > c && l >= j) d[j] = fma(-f, col[j], d[j]);
+      }
+      // pivots: lane l's a_ll; rs_c = 1 / sqrt(a_cc) to every lane
+      double dl = 1.0;
+#pragma unroll
+      for (int j = 0; j < kPB; ++j)
+        if (j == l) dl = d[j];
+      if (!(dl > 0.0) || !isfinite(dl)) dl = 1.0;
+      const double sq = sqrt(dl), rs = 1.0 / sq;
+      if (lane < kPB) {
+#pragma unroll
+        for (int j = 0; j < kPB; ++j) {
+          const double rsj = __shfl_sync(0x0000ffffu, rs, j);
+          if (j < l) X[(cb + j) * kXS + r] = d[j] * rsj;
+        }
+        X[(cb + l) * kXS + r] = sq;
+        rinv[r] = rs;
+      }
+      if (bad && lane == 0) bad_any = 1;
+    }
+    __syncthreads();
+    PSTAMP(2 + 3 * (cb / kPB));
+    // (2) rows below the diagonal block: x D^T = a
+    const int r0 = cb + kPB;
+    if (tid < kPanelRows - r0) {
+      const int r = r0 + tid;
+      double x[kPB];
+#pragma unroll
+      for (int j = 0; j < kPB; ++j) x[j] = X[(cb + j) * kXS + r];
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) {
+        x[c] *= rinv[cb + c];
+#pragma unroll
+        for (int j = 1; j < kPB; ++j)
+          if (j > c) x[j] = fma(-x[c], X[(cb + c) * kXS + cb + j], x[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kPB; ++j) X[(cb + j) * kXS + r] = x[j];
+    }
+    __syncthreads();
+    PSTAMP(3 + 3 * (cb / kPB));
+    if (r0 >= kT) break;
+    // (3) X(r, j) -= sum_l X(r, cb + l) X(j, cb + l), r >= r0, r0 <= j < 64:
+    // 16 x 8 DMMA tiles, rows in groups of 16 from r0, columns in 8s from r0
+    {
+      const int gq = lane >> 2, tq = lane & 3;
+      const int nR = (kPanelRows - r0) / 16, nC = (kT - r0) / 8;
+      for (int t = warp; t < nR * nC; t += kPanelThreads / 32) {
+        const int rt = r0 + 16 * (t / nC), ct = r0 + 8 * (t % nC);
+        if (rt + 15 < ct) continue;  // strictly upper part of the diagonal block
+        double acc[4];
+        acc[0] = X[(ct + 2 * tq) * kXS + rt + gq];
+        acc[1] = X[(ct + 2 * tq + 1) * kXS + rt + gq];
+        acc[2] = X[(ct + 2 * tq) * kXS + rt + gq + 8];
+        acc[3] = X[(ct + 2 * tq + 1) * kXS + rt + gq + 8];
+#pragma unroll
+        for (int kk = 0; kk < kPB / 4; ++kk) {
+          const double* col = X + (cb + 4 * kk + tq) * kXS;
+          dmma(acc, -col[rt + gq], -col[rt + gq + 8], col[ct + gq]);
+        }
+        X[(ct + 2 * tq) * kXS + rt + gq] = acc[0];
+        X[(ct + 2 * tq + 1) * kXS + rt + gq] = acc[1];
+        X[(ct + 2 * tq) * kXS + rt + gq + 8] = acc[2];
+        X[(ct + 2 * tq + 1) * kXS + rt + gq + 8] = acc[3];
+      }
+    }
+    __syncthreads();
+    PSTAMP(4 + 3 * (cb / kPB));
+  }
+  PSTAMP(14);
+  if (bad_any && report && tid == 0) atomicCAS(status, 0, k + 1);
+  for (int e = tid; e < kT * kPanelRows / 2; e += kPanelThreads) {
+    const int c = e >> 6, r = 2 * (e & 63);
+    double2 v = *reinterpret_cast<const double2*>(X + c * kXS + r);
+    if (r < kT) {
+      if (diag_out) {
+        if (c > r) v.x = 0.0;
+        if (c > r + 1) v.y = 0.0;
+        *reinterpret_cast<double2*>(diag_out + c * kT + r) = v;
+      }
+    } else if (panel) {
+      *reinterpret_cast<double2*>(panel + c * kT + r - kT) = v;
+      if (panel_copy) *reinterpret_cast<double2*>(panel_copy + c * kT + r - kT) = v;
     }
   }
+  PSTAMP(15);
 }
 
 __global__ void __launch_bounds__(kPanelThreads)
@@ -797,6 +885,8 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   cudaError_t e = cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kUpdSmem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmem);
+  if (e != cudaSuccess) return e;
   // Lookahead over two streams: the high-priority stream runs panel(k) and
   // the update of block column k+1 only (U1), so panel(k+1) can start while
   // the low-priority stream applies the rest of update k (U2) -- the
@@ -824,7 +914,7 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   bool u2_pending = false;
   for (int k = 0; k < nb; ++k) {
     const int m = nb - k - 1;
-    chol_panel_kernel<<<std::max(1, m), kPanelThreads, 0, main_s>>>(t.tiles, nb, k, t.status);
+    chol_panel_kernel<<<std::max(1, m), kPanelThreads, kPanelSmem, main_s>>>(t.tiles, nb, k, t.status);
     ++launches;
     if (m == 0) break;
     // U2(k): tiles (i, j), k + 2 <= j <= i
@@ -832,7 +922,7 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
       cudaEventRecord(ev_panel, main_s);
       cudaStreamWaitEvent(side, ev_panel, 0);
       chol_update_kernel<<<(unsigned)((long long)(m - 1) * m / 2), kUpdThreads, kUpdSmem, side>>>(
-          t.tiles, nb, k, k + 2, 0);
+            t.tiles, nb, k, k + 2, 0);
       ++launches;
     }
     // U1(k): block column k + 1, after U2(k - 1) updated it
@@ -1097,6 +1187,8 @@ cudaError_t cholesky_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaSt
   cudaError_t e = cudaFuncSetAttribute(dist_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kUpdSmem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(dist_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmem);
+  if (e != cudaSuccess) return e;
   const int cnt0 = (nb + P - 1) / P;  // bound on any rank's rows > k
   DevMem akk, sendb, recvb, stat;
   if ((e = cudaMalloc(&akk.p, sizeof(double) * kTile)) != cudaSuccess) return e;
@@ -1118,7 +1210,7 @@ cudaError_t cholesky_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaSt
     const int cnt = dist_count(dist_first(k, r, P), nb, P);
     const int grid = cnt > 0 ? cnt : (r == owner ? 1 : 0);
     if (grid) {
-      dist_panel_kernel<<<grid, kPanelThreads, 0, st>>>(t.tiles, r, P, k, nb, a, r == owner, sb, t.status);
+      dist_panel_kernel<<<grid, kPanelThreads, kPanelSmem, st>>>(t.tiles, r, P, k, nb, a, r == owner, sb, t.status);
       ++g_last_launches;
     }
     if (k == nb - 1) break;
