@@ -590,22 +590,101 @@ LTB_DEV void tile_update_cta(const double* __restrict__ Lik, const double* __res
 }
 
 
+// A_ij -= L_ik L_jk^T + L_i,k+1 L_j,k+1^T (kc == 2) or L_ik L_jk^T (kc == 1):
+// the trailing update of a pair of block columns at once (K = 128) reads and
+// writes A_ij once per two columns -- half the tile traffic per flop of a
+// K = 64 update.  Operands stream through two 32-wide k stages (cp.async
+// double buffer, 68 KB: 3 CTAs per SM).  Tiles: mode 0, the lower triangle
+// from (base, base); mode 1, block columns base and base + 1 (i >= j);
+// mode 2, block column base.
 __global__ void __launch_bounds__(kUpdThreads)
-    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int base, int column_only) {
+    chol_update_kernel(double* __restrict__ tiles, int nb, int k, int kc, int base, int mode) {
   int i, j;
-  if (column_only) {  // tiles (i, base), i >= base
-    i = base + (int)blockIdx.x;
-    j = base;
-  } else {  // the lower triangle of tiles from (base, base)
+  const int b = (int)blockIdx.x, m0 = nb - base;
+  if (mode == 0) {
     int li, lj;
-    tri_pair(blockIdx.x, &li, &lj);
+    tri_pair(b, &li, &lj);
     i = base + li;
     j = base + lj;
+  } else if (mode == 2 || b < m0) {
+    i = base + b;
+    j = base;
+  } else {
+    i = base + 1 + (b - m0);
+    j = base + 1;
   }
-  const double* Lik = tiles + tile_at(i, k);
-  const double* Ljk = tiles + tile_at(j, k);
+  extern __shared__ __align__(16) double usm[];
+  constexpr int kKS = 32, kStage = 2 * kKS * kUS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int nch = 2 * kc;
+  auto load = [&](int q) {
+    const size_t off = (size_t)(q & 1) * kKS * kT;
+    const double* a = tiles + tile_at(i, k + (q >> 1)) + off;
+    const double* bb = tiles + tile_at(j, k + (q >> 1)) + off;
+    double* sa = usm + (q & 1) * kStage;
+    double* sb = sa + kKS * kUS;
+    for (int c = tid; c < kKS * kT / 2; c += kUpdThreads) {
+      const int l = c >> 5, m = 2 * (c & 31);
+      cp_async16(sa + l * kUS + m, a + l * kT + m, 16);
+      cp_async16(sb + l * kUS + m, bb + l * kT + m, 16);
+    }
+    cp_commit();
+  };
+  load(0);
+  load(1);
   double* Aij = tiles + tile_at(i, j);
-  tile_update_cta(Lik, Ljk, Aij);
+  double acc[2][2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
+          acc[mt][nt8][2 * h + c] = Aij[col * kT + r];
+        }
+  for (int q = 0; q < nch; ++q) {
+    if (q + 1 < nch) cp_wait<1>();
+    else cp_wait<0>();
+    __syncthreads();
+    const double* sA = usm + (q & 1) * kStage;
+    const double* sB = sA + kKS * kUS;
+#pragma unroll
+    for (int kk = 0; kk < kKS / 4; ++kk) {
+      const int kr = (kk * 4 + tq) * kUS;
+      double a[2][2], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        a[mt][0] = -sA[kr + wm * 32 + mt * 16 + gq];
+        a[mt][1] = -sA[kr + wm * 32 + mt * 16 + gq + 8];
+      }
+#pragma unroll
+      for (int nt8 = 0; nt8 < 2; ++nt8) bf[nt8] = sB[kr + wn * 16 + nt8 * 8 + gq];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt8 = 0; nt8 < 2; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], bf[nt8]);
+    }
+    if (q + 2 < nch) {
+      __syncthreads();
+      load(q + 2);
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt8 = 0; nt8 < 2; ++nt8)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
+          Aij[col * kT + r] = acc[mt][nt8][2 * h + c];
+        }
 }
 
 // packed lower tiles -> column-major lower triangle
@@ -912,24 +991,35 @@ cudaError_t cholesky_packed(TriFactor& t, cudaStream_t st, int* bad_block) {
   cudaStreamWaitEvent(side, ev_fork, 0);
   int launches = 0;
   bool u2_pending = false;
-  for (int k = 0; k < nb; ++k) {
-    const int m = nb - k - 1;
-    chol_panel_kernel<<<std::max(1, m), kPanelThreads, kPanelSmem, main_s>>>(t.tiles, nb, k, t.status);
+  const auto panel = [&](int k) {
+    chol_panel_kernel<<<std::max(1, nb - k - 1), kPanelThreads, kPanelSmem, main_s>>>(t.tiles, nb, k, t.status);
     ++launches;
-    if (m == 0) break;
-    // U2(k): tiles (i, j), k + 2 <= j <= i
-    if (m > 1) {
+  };
+  // block columns in pairs (k, k + 1): panel k, column k + 1 -= L_k L_k+1,k^T,
+  // panel k + 1, then the pair's K = 128 update of everything to the right
+  for (int k = 0; k < nb; k += 2) {
+    panel(k);
+    if (k + 1 >= nb) break;
+    chol_update_kernel<<<(unsigned)(nb - k - 1), kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, 1, k + 1, 2);
+    panel(k + 1);
+    launches += 1;
+    if (k + 2 >= nb) break;
+    // U2(k): tiles (i, j), k + 4 <= j <= i
+    const int m2 = nb - k - 4;
+    if (m2 > 0) {
       cudaEventRecord(ev_panel, main_s);
       cudaStreamWaitEvent(side, ev_panel, 0);
-      chol_update_kernel<<<(unsigned)((long long)(m - 1) * m / 2), kUpdThreads, kUpdSmem, side>>>(
-            t.tiles, nb, k, k + 2, 0);
+      chol_update_kernel<<<(unsigned)((long long)m2 * (m2 + 1) / 2), kUpdThreads, kUpdSmem, side>>>(
+          t.tiles, nb, k, 2, k + 4, 0);
       ++launches;
     }
-    // U1(k): block column k + 1, after U2(k - 1) updated it
+    // U1(k): block columns k + 2, k + 3, after U2(k - 2) updated them
     if (u2_pending) cudaStreamWaitEvent(main_s, ev_u2, 0);
-    chol_update_kernel<<<(unsigned)m, kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, k + 1, 1);
+    const int m1 = nb - k - 2;
+    chol_update_kernel<<<(unsigned)(m1 + std::max(0, m1 - 1)), kUpdThreads, kUpdSmem, main_s>>>(t.tiles, nb, k, 2,
+                                                                                               k + 2, 1);
     ++launches;
-    u2_pending = m > 1;
+    u2_pending = m2 > 0;
     if (u2_pending) cudaEventRecord(ev_u2, side);
   }
   cudaEventRecord(ev_join, side);
