@@ -523,29 +523,46 @@ __global__ void __launch_bounds__(kPanelThreads)
 }
 
 // ---------------------------------------------------------------------------
-// (4) trailing update A_ij -= L_ik L_jk^T for k < j <= i < nb: one CTA per
-// tile, L_ik and L_jk staged by cp.async (k-major = the column-major tile),
-// A_ij fragments loaded into the DMMA accumulators and stored back.
-// 8 warps, warp tile 32 x 16.
+// (4) trailing update A_ij -= L_ik L_jk^T (+ L_i,k+1 L_j,k+1^T): one CTA per
+// 64x64 tile, 8 warps (warp tile 32 x 16), accumulators seeded from A_ij
+// and stored back.  Block columns are updated in pairs (K = 128), so a
+// trailing tile is read and written once per two columns -- half the tile
+// traffic per flop of a K = 64 update.  Operands stream through a ring of S
+// cp.async stages of KS k columns (k-major = the column-major tile).
 // ---------------------------------------------------------------------------
 constexpr int kUS = kT + 4;  // 68 == 4 mod 16
 constexpr int kUpdThreads = 256;
-constexpr size_t kUpdSmem = (size_t)2 * kT * kUS * sizeof(double);
 
-// A_ij -= L_ik L_jk^T for one tile (DMMA)
-LTB_DEV void tile_update_cta(const double* __restrict__ Lik, const double* __restrict__ Ljk, double* __restrict__ Aij) {
+// A_ij -= sum_{c < kc} Li[c] Lj[c]^T for one tile, Li[c] / Lj[c] the operand
+// tiles of block column c of the update (kc <= 2)
+template <int KS, int S>
+LTB_DEV void tile_update_ring(const double* const (&Li)[2], const double* const (&Lj)[2], int kc,
+                              double* __restrict__ Aij) {
   extern __shared__ __align__(16) double usm[];
-  double* sA = usm;
-  double* sB = usm + kT * kUS;
+  constexpr int kStage = 2 * KS * kUS, kPer = kT / KS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
-  for (int c = tid; c < kTile / 2; c += kUpdThreads) {
-    const int l = c >> 5, m = 2 * (c & 31);
-    cp_async16(sA + l * kUS + m, Lik + l * kT + m, 16);
-    cp_async16(sB + l * kUS + m, Ljk + l * kT + m, 16);
-  }
-  cp_commit();
+  const int nch = kPer * kc;
+  // chunk q (k columns [KS (q % kPer), +KS) of block column k + q / kPer)
+  // into ring stage q % S; always one commit group per call
+  auto load = [&](int q) {
+    if (q < nch) {
+      const size_t off = (size_t)(q % kPer) * KS * kT;
+      const double* a = (q >= kPer ? Li[1] : Li[0]) + off;  // (not indexed: would go to local memory)
+      const double* bb = (q >= kPer ? Lj[1] : Lj[0]) + off;
+      double* sa = usm + (q % S) * kStage;
+      double* sb = sa + KS * kUS;
+      for (int c = tid; c < KS * kT / 2; c += kUpdThreads) {
+        const int l = c >> 5, m = 2 * (c & 31);
+        cp_async16(sa + l * kUS + m, a + l * kT + m, 16);
+        cp_async16(sb + l * kUS + m, bb + l * kT + m, 16);
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int q = 0; q < S - 1; ++q) load(q);
   double acc[2][2][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -558,24 +575,30 @@ LTB_DEV void tile_update_cta(const double* __restrict__ Lik, const double* __res
           const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
           acc[mt][nt8][2 * h + c] = Aij[col * kT + r];
         }
-  cp_wait<0>();
-  __syncthreads();
+  for (int q = 0; q < nch; ++q) {
+    cp_wait<S - 2>();
+    __syncthreads();  // chunk q landed for every thread; stage (q - 1) % S is free
+    load(q + S - 1);
+    const double* sA = usm + (q % S) * kStage;
+    const double* sB = sA + KS * kUS;
 #pragma unroll
-  for (int kk = 0; kk < kT / 4; ++kk) {
-    const int kr = (kk * 4 + tq) * kUS;
-    double a[2][2], b[2];
+    for (int kk = 0; kk < KS / 4; ++kk) {
+      const int kr = (kk * 4 + tq) * kUS;
+      double a[2][2], bf[2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      a[mt][0] = -sA[kr + wm * 32 + mt * 16 + gq];
-      a[mt][1] = -sA[kr + wm * 32 + mt * 16 + gq + 8];
+      for (int mt = 0; mt < 2; ++mt) {
+        a[mt][0] = -sA[kr + wm * 32 + mt * 16 + gq];
+        a[mt][1] = -sA[kr + wm * 32 + mt * 16 + gq + 8];
+      }
+#pragma unroll
+      for (int nt8 = 0; nt8 < 2; ++nt8) bf[nt8] = sB[kr + wn * 16 + nt8 * 8 + gq];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt8 = 0; nt8 < 2; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], bf[nt8]);
     }
-#pragma unroll
-    for (int nt8 = 0; nt8 < 2; ++nt8) b[nt8] = sB[kr + wn * 16 + nt8 * 8 + gq];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt8 = 0; nt8 < 2; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], b[nt8]);
   }
+  cp_wait<0>();
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -589,14 +612,17 @@ LTB_DEV void tile_update_cta(const double* __restrict__ Lik, const double* __res
         }
 }
 
+template <int KS, int S>
+constexpr size_t upd_smem() { return (size_t)S * 2 * KS * kUS * sizeof(double); }
 
-// A_ij -= L_ik L_jk^T + L_i,k+1 L_j,k+1^T (kc == 2) or L_ik L_jk^T (kc == 1):
-// the trailing update of a pair of block columns at once (K = 128) reads and
-// writes A_ij once per two columns -- half the tile traffic per flop of a
-// K = 64 update.  Operands stream through two 32-wide k stages (cp.async
-// double buffer, 68 KB: 3 CTAs per SM).  Tiles: mode 0, the lower triangle
-// from (base, base); mode 1, block columns base and base + 1 (i >= j);
-// mode 2, block column base.
+// 16-column k stages, double buffered: 35 KB of shared memory and 62
+// registers -> 4 CTAs per SM (32-column stages / deeper rings measured
+// slower: 3 CTAs per SM hide the tile loads and stores less well)
+constexpr int kUpdKS = 16, kUpdStages = 2;
+constexpr size_t kUpdSmem = upd_smem<kUpdKS, kUpdStages>();
+
+// tiles: mode 0, the lower triangle from (base, base); mode 1, block columns
+// base and base + 1 (i >= j); mode 2, block column base
 __global__ void __launch_bounds__(kUpdThreads)
     chol_update_kernel(double* __restrict__ tiles, int nb, int k, int kc, int base, int mode) {
   int i, j;
@@ -613,78 +639,9 @@ __global__ void __launch_bounds__(kUpdThreads)
     i = base + 1 + (b - m0);
     j = base + 1;
   }
-  extern __shared__ __align__(16) double usm[];
-  constexpr int kKS = 32, kStage = 2 * kKS * kUS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
-  const int nch = 2 * kc;
-  auto load = [&](int q) {
-    const size_t off = (size_t)(q & 1) * kKS * kT;
-    const double* a = tiles + tile_at(i, k + (q >> 1)) + off;
-    const double* bb = tiles + tile_at(j, k + (q >> 1)) + off;
-    double* sa = usm + (q & 1) * kStage;
-    double* sb = sa + kKS * kUS;
-    for (int c = tid; c < kKS * kT / 2; c += kUpdThreads) {
-      const int l = c >> 5, m = 2 * (c & 31);
-      cp_async16(sa + l * kUS + m, a + l * kT + m, 16);
-      cp_async16(sb + l * kUS + m, bb + l * kT + m, 16);
-    }
-    cp_commit();
-  };
-  load(0);
-  load(1);
-  double* Aij = tiles + tile_at(i, j);
-  double acc[2][2][4];
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt8 = 0; nt8 < 2; ++nt8)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
-          acc[mt][nt8][2 * h + c] = Aij[col * kT + r];
-        }
-  for (int q = 0; q < nch; ++q) {
-    if (q + 1 < nch) cp_wait<1>();
-    else cp_wait<0>();
-    __syncthreads();
-    const double* sA = usm + (q & 1) * kStage;
-    const double* sB = sA + kKS * kUS;
-#pragma unroll
-    for (int kk = 0; kk < kKS / 4; ++kk) {
-      const int kr = (kk * 4 + tq) * kUS;
-      double a[2][2], bf[2];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        a[mt][0] = -sA[kr + wm * 32 + mt * 16 + gq];
-        a[mt][1] = -sA[kr + wm * 32 + mt * 16 + gq + 8];
-      }
-#pragma unroll
-      for (int nt8 = 0; nt8 < 2; ++nt8) bf[nt8] = sB[kr + wn * 16 + nt8 * 8 + gq];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt8 = 0; nt8 < 2; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], bf[nt8]);
-    }
-    if (q + 2 < nch) {
-      __syncthreads();
-      load(q + 2);
-    }
-  }
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt8 = 0; nt8 < 2; ++nt8)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int r = wm * 32 + mt * 16 + gq + 8 * h, col = wn * 16 + nt8 * 8 + 2 * tq + c;
-          Aij[col * kT + r] = acc[mt][nt8][2 * h + c];
-        }
+  const double* const Li[2] = {tiles + tile_at(i, k), tiles + tile_at(i, k + kc - 1)};
+  const double* const Lj[2] = {tiles + tile_at(j, k), tiles + tile_at(j, k + kc - 1)};
+  tile_update_ring<kUpdKS, kUpdStages>(Li, Lj, kc, tiles + tile_at(i, j));
 }
 
 // packed lower tiles -> column-major lower triangle
@@ -1179,26 +1136,45 @@ __global__ void __launch_bounds__(kPanelThreads)
   chol_panel_cta(akk, dkk, pt, b < cnt ? sendbuf + (size_t)b * kTile : nullptr, k, owner && b == 0, status);
 }
 
-// own rows i > k, tiles j in (k, i]: A_ij -= L_ik L_jk^T, L_jk from the
-// gathered column (rank q's rows at recv[q * cntmax + (j - first_q) / P])
+// Gathered block column c of the factor: rank q's rows > c at
+// recv[q * cntmax + (j - dist_first(c, q, P)) / P]
+struct DistCol {
+  const double* recv;
+  int cntmax;
+};
+
+LTB_DEV const double* dist_gathered(const DistCol& g, int c, int j, int P) {
+  const int q = j % P;
+  return g.recv + ((size_t)q * g.cntmax + (j - dist_first(c, q, P)) / P) * kTile;
+}
+
+// own rows i > kl (kl = k + kc - 1), tiles j in (kl, i]:
+// A_ij -= sum_{c < kc} L_i,k+c L_j,k+c^T (column_only: just j = kl + 1, kc = 1)
 __global__ void __launch_bounds__(kUpdThreads)
-    dist_update_kernel(double* __restrict__ tiles, int r, int P, int k, int nb, const double* __restrict__ recv,
-                       int cntmax) {
-  const int first = dist_first(k, r, P), cnt = dist_count(first, nb, P);
+    dist_update_kernel(double* __restrict__ tiles, int r, int P, int k, int kc, int nb, const DistCol g0,
+                       const DistCol g1, int column_only) {
+  const int kl = k + kc - 1;
+  const int first = dist_first(kl, r, P), cnt = dist_count(first, nb, P);
   const long long b = blockIdx.x;
-  int lo = 0, hi = cnt - 1;  // row a: tiles before it a (first - k) + P a (a - 1) / 2
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) / 2;
-    if ((long long)mid * (first - k) + (long long)P * mid * (mid - 1) / 2 <= b) lo = mid;
-    else hi = mid - 1;
+  int a, j;
+  if (column_only) {
+    a = (int)b;
+    j = kl + 1;
+  } else {
+    int lo = 0, hi = cnt - 1;  // row a: tiles before it a (first - kl) + P a (a - 1) / 2
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if ((long long)mid * (first - kl) + (long long)P * mid * (mid - 1) / 2 <= b) lo = mid;
+      else hi = mid - 1;
+    }
+    a = lo;
+    j = kl + 1 + (int)(b - ((long long)a * (first - kl) + (long long)P * a * (a - 1) / 2));
   }
-  const int a = lo, i = first + P * a;
-  const int j = k + 1 + (int)(b - ((long long)a * (first - k) + (long long)P * a * (a - 1) / 2));
-  const int q = j % P, fq = dist_first(k, q, P);
-  const double* Lik = tiles + (drow_off(i / P, r, P) + k) * kTile;
-  const double* Ljk = recv + ((size_t)q * cntmax + (j - fq) / P) * kTile;
-  double* Aij = tiles + (drow_off(i / P, r, P) + j) * kTile;
-  tile_update_cta(Lik, Ljk, Aij);
+  const int i = first + P * a;
+  const size_t row = drow_off(i / P, r, P);
+  const double* const Li[2] = {tiles + (row + k) * kTile, tiles + (row + kl) * kTile};
+  const double* const Lj[2] = {dist_gathered(g0, k, j, P), dist_gathered(kc == 2 ? g1 : g0, kl, j, P)};
+  tile_update_ring<kUpdKS, kUpdStages>(Li, Lj, kc, tiles + (row + j) * kTile);
 }
 
 #define NCCL_TRY(expr)                                                            \
@@ -1282,36 +1258,54 @@ cudaError_t cholesky_dist(TriFactor& t, const Nccl* api, ncclComm_t comm, cudaSt
   const int cnt0 = (nb + P - 1) / P;  // bound on any rank's rows > k
   DevMem akk, sendb, recvb, stat;
   if ((e = cudaMalloc(&akk.p, sizeof(double) * kTile)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&sendb.p, sizeof(double) * kTile * (size_t)cnt0)) != cudaSuccess) return e;
-  if (P > 1 && (e = cudaMalloc(&recvb.p, sizeof(double) * kTile * (size_t)cnt0 * P)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&sendb.p, sizeof(double) * kTile * (size_t)cnt0 * 2)) != cudaSuccess) return e;
+  if (P > 1 && (e = cudaMalloc(&recvb.p, sizeof(double) * kTile * (size_t)cnt0 * P * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&stat.p, sizeof(int) * P)) != cudaSuccess) return e;
   double* a = static_cast<double*>(akk.p);
-  double* sb = static_cast<double*>(sendb.p);
-  double* rb = P > 1 ? static_cast<double*>(recvb.p) : sb;
   cudaMemsetAsync(t.status, 0, sizeof(int), st);
   g_last_launches = 0;
-  for (int k = 0; k < nb; ++k) {
-    const int owner = k % P;
+  // block column c: owner broadcasts A_cc, every rank factors its panel tiles
+  // (copies into send buffer c & 1), all-gather -> the gathered column
+  const auto panel_step = [&](int c, DistCol* g) -> cudaError_t {
+    const int owner = c % P;
+    double* sb = static_cast<double*>(sendb.p) + (size_t)(c & 1) * cnt0 * kTile;
+    double* rb = P > 1 ? static_cast<double*>(recvb.p) + (size_t)(c & 1) * cnt0 * P * kTile : sb;
+    cudaError_t e2;
     if (r == owner &&
-        (e = cudaMemcpyAsync(a, t.tiles + (drow_off(k / P, r, P) + k) * kTile, sizeof(double) * kTile,
-                             cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-      return e;
+        (e2 = cudaMemcpyAsync(a, t.tiles + (drow_off(c / P, r, P) + c) * kTile, sizeof(double) * kTile,
+                              cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return e2;
     if (P > 1) NCCL_TRY(api->Broadcast(a, a, kTile, ncclDouble, owner, comm, st));
-    const int cnt = dist_count(dist_first(k, r, P), nb, P);
+    const int cnt = dist_count(dist_first(c, r, P), nb, P);
     const int grid = cnt > 0 ? cnt : (r == owner ? 1 : 0);
     if (grid) {
-      dist_panel_kernel<<<grid, kPanelThreads, kPanelSmem, st>>>(t.tiles, r, P, k, nb, a, r == owner, sb, t.status);
+      dist_panel_kernel<<<grid, kPanelThreads, kPanelSmem, st>>>(t.tiles, r, P, c, nb, a, r == owner, sb, t.status);
       ++g_last_launches;
     }
-    if (k == nb - 1) break;
     int cntmax = 0;
-    for (int q = 0; q < P; ++q) cntmax = std::max(cntmax, dist_count(dist_first(k, q, P), nb, P));
-    if (P > 1) NCCL_TRY(api->AllGather(sb, rb, (size_t)cntmax * kTile, ncclDouble, comm, st));
-    const int first = dist_first(k, r, P);
-    const long long tiles = (long long)cnt * (first - k) + (long long)P * cnt * (cnt - 1) / 2;
+    for (int q = 0; q < P; ++q) cntmax = std::max(cntmax, dist_count(dist_first(c, q, P), nb, P));
+    if (P > 1 && c < nb - 1) NCCL_TRY(api->AllGather(sb, rb, (size_t)cntmax * kTile, ncclDouble, comm, st));
+    g->recv = rb;
+    g->cntmax = P > 1 ? cntmax : cnt0;
+    return cudaGetLastError();
+  };
+  // block columns in pairs (as cholesky_packed): panel k, column k + 1 -= its
+  // L_k part, panel k + 1, then the K = 128 update of the rest
+  for (int k = 0; k < nb; k += 2) {
+    DistCol g0{}, g1{};
+    if ((e = panel_step(k, &g0)) != cudaSuccess) return e;
+    if (k == nb - 1) break;
+    const int cnt_c = dist_count(dist_first(k, r, P), nb, P);  // own rows >= k + 1
+    if (cnt_c > 0) {
+      dist_update_kernel<<<(unsigned)cnt_c, kUpdThreads, kUpdSmem, st>>>(t.tiles, r, P, k, 1, nb, g0, g0, 1);
+      ++g_last_launches;
+    }
+    if ((e = panel_step(k + 1, &g1)) != cudaSuccess) return e;
+    if (k + 1 == nb - 1) break;
+    const int first = dist_first(k + 1, r, P), cnt = dist_count(first, nb, P);
+    const long long tiles = (long long)cnt * (first - k - 1) + (long long)P * cnt * (cnt - 1) / 2;
     if (tiles > 0) {
-      dist_update_kernel<<<(unsigned)tiles, kUpdThreads, kUpdSmem, st>>>(t.tiles, r, P, k, nb, rb,
-                                                                          P > 1 ? cntmax : cnt0);
+      dist_update_kernel<<<(unsigned)tiles, kUpdThreads, kUpdSmem, st>>>(t.tiles, r, P, k, 2, nb, g0, g1, 0);
       ++g_last_launches;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
