@@ -384,6 +384,7 @@ LTB_DEV void chol_panel_cta(const double* diag_in, double* diag_out, double* pan
   double* X = psm;              // X[c * kXS + r]
   double* rinv = psm + kT * kXS;  // 1 / L_cc
   __shared__ int bad_any;
+  __shared__ double cbuf[2 * kPB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) bad_any = 0;
   PSTAMP(0);
@@ -414,10 +415,16 @@ LTB_DEV void chol_panel_cta(const double* diag_in, double* diag_out, double* pan
       bool bad = false;
 #pragma unroll
       for (int c = 0; c < kPB; ++c) {
-        double col[kPB];  // a_jc, j > c (unscaled, from lane j)
+        // column c (a_jc, unscaled) through a per-step shared slot: one
+        // store per lane, then broadcast loads (fewer instructions on the
+        // dependent chain than 16 double shuffles)
+        double* cs = cbuf + (c & 1) * kPB;
+        cs[l] = d[c];
+        __syncwarp();
+        double col[kPB];
 #pragma unroll
         for (int j = 0; j < kPB; ++j)
-          if (j >= c) col[j] = __shfl_sync(0xffffffffu, d[c], j);
+          if (j >= c) col[j] = cs[j];
         double piv = col[c];
         if (!(piv > 0.0) || !isfinite(piv)) {
           bad = true;
