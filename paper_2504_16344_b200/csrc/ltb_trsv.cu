@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "ltb_common.cuh"
 #include "ltb_gen.cuh"
@@ -57,6 +58,12 @@ constexpr int kPad = 65;             // padded smem tile stride
 constexpr int kTile = kTB * kTB;
 constexpr int kRing = 4;             // worker TMA ring depth (32 KB stages)
 constexpr unsigned long long kSentinel = ~0ull;        // all-ones NaN
+// super-block chain (one GPU, trsv_super_kernel): kSB tiles = kSR rows per
+// chain step, kSChain CTAs with kSRows rows each
+constexpr int kSB = 8;
+constexpr int kSR = kSB * 64;
+constexpr int kSChain = 64;
+constexpr int kSRows = kSR / kSChain;
 constexpr unsigned long long kSpinNs = 4000000000ull;  // 4 s dependency-wait timeout
 
 // recv layout (in doubles)
@@ -156,6 +163,13 @@ struct DistArgs {
   unsigned* gsync;                // local grid barrier {count, generation}
   int* status;
   unsigned long long* trace;
+  const double* sfwd;             // super-block chain rows (trsv_super_kernel, P = 1)
+  const double* sbwd;
+  double* spart;                  // workers' partial sums (super_slot)
+  unsigned* stask;                // workers' task counter
+  const int4* stlist;             // task list (build_super_tasks)
+  int ntasks;
+  int ns, nchain;                 // super blocks, chain CTAs
 };
 
 // fixed-order sum of the kQ column-group partials of row r
@@ -738,6 +752,334 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
   }
 }
 
+// ---------------- super-block chain (P = 1) -----------------------------------
+// The diagonal chain at the granularity of super blocks of kSB = 8 tiles
+// (512 rows), with the super-block inverses precomputed (prepare_super):
+//   forward   y_S = L_SS^{-1} c_S - M1_S y_{S-1} - M2_S y_{S-2},
+//             Mk_S = L_SS^{-1} L_{S,S-k}
+//   backward  x_S = L_SS^{-T} d_S - M1'_S x_{S+1} - M2'_S x_{S+2},
+//             Mk'_S = L_SS^{-T} L_{S+k,S}^T
+// with c_S = b_S - sum_{J < S-2} L_SJ y_J and d_S = y_S - sum_{T > S+2}
+// L_TS^T x_T (super-block indices): the workers' last inputs exist two chain
+// steps before the chain needs their sums.  A chain step is ONE dense
+// 512 x 1536 product [L_SS^{-1} | -M1_S | -M2_S] [c_S; y_{S-1}; y_{S-2}]
+// spread over kSChain CTAs
+// (kSRows rows each, the next step's rows prefetched by one bulk copy);
+// the chain CTAs exchange y / x through global memory (NaN-sentinel slots).
+// The panel sums are cut into tasks of at most chs super blocks of one tile
+// row (column), spread round-robin over the workers in the order their
+// inputs appear, each handing off a 64-value partial sum; the chain adds the
+// <= kMaxParts partials of a row when it assembles c_S / d_S.  Long rows are
+// thereby streamed by many SMs at once: a row-per-worker split leaves the
+// last rows (3.9 MB at n = 8192) to one SM each, which bounds the sweep.
+constexpr int kSLook = 2;                 // previous super blocks the chain applies itself
+constexpr int kSRowLen = (1 + kSLook) * kSR;  // [inverse | -M1 | -M2] row
+constexpr size_t kSChainSmem = (size_t)(2 * kSRows * kSRowLen + kSRowLen) * sizeof(double) + 2 * sizeof(uint64_t);
+// super kernel workers: a kSRing-deep tile ring (deeper than the cluster
+// kernel's: more bytes in flight per SM while HBM is saturated), then their
+// reduction scratch and task queue, all in the dynamic region the chain
+// CTAs use for their rows
+constexpr int kSRing = 6;
+struct SuperWorkerSmem {
+  double red[kQ][kTB];
+  double sR[2 * kTB];
+};
+constexpr size_t kWorkerSmemOff = ((size_t)kSRing * kTile * sizeof(double) + kSRing * sizeof(uint64_t) + 127) / 128 * 128;
+constexpr int kMaxParts = 8;
+
+// super blocks per task for ns super blocks: <= kMaxParts partials per row
+__host__ __device__ inline int super_chs(int ns) { return (ns + kMaxParts - 1) / kMaxParts; }
+// forward: row I (super block S = I / kSB) has panel super blocks [0, S - 1)
+// in parts of chs; backward: column J has [S + 2, ns), parts counted from the
+// top (part 0 = the highest super blocks, whose x comes first)
+__host__ __device__ inline int super_parts_f(int S, int chs) {
+  return S > kSLook ? (S - kSLook + chs - 1) / chs : 0;
+}
+__host__ __device__ inline int super_parts_b(int S, int ns, int chs) {
+  return ns - S - 1 - kSLook > 0 ? (ns - S - 1 - kSLook + chs - 1) / chs : 0;
+}
+// partial-sum slots: [dir][row][part][64]
+__host__ __device__ inline size_t super_slot(int nb, int dir, int row, int part) {
+  return (((size_t)dir * nb + row) * kMaxParts + part) * kTB;
+}
+
+struct SuperTask {
+  int dir;     // 0 forward (tile row I), 1 backward (tile column J)
+  int rc;      // I or J
+  int part;
+  int k0, nt;  // first tile index, tile count (forward: J = k0 + e; backward: T = k0 - e)
+};
+
+// global task t of the list built by prepare_super (build_super_tasks):
+// {dir | part << 1, row / column, k0, nt}
+LTB_DEV bool super_task(const DistArgs& a, long long t, SuperTask* o) {
+  const int4 v = a.stlist[t];
+  o->dir = v.x & 1;
+  o->part = v.x >> 1;
+  o->rc = v.y;
+  o->k0 = v.z;
+  o->nt = v.w;
+  return true;
+}
+
+LTB_DEV const double* super_task_tile(const RankView& rv, const SuperTask& k, int e) {
+  return k.dir == 0 ? rv.tiles + (row_off(k.rc, 0, 1) + (size_t)(k.k0 + e)) * kTile
+                    : rv.tiles + (row_off(k.k0 - e, 0, 1) + (size_t)k.rc) * kTile;
+}
+
+// one worker's task stream: tasks are taken from a global counter (in the
+// order their inputs appear) when the TMA ring's issue cursor reaches them
+// (tid 0) and queued in shared memory for the consumer; every tile goes
+// through the ring, kRing tiles ahead across task boundaries
+constexpr int kTaskQ = kSRing + 2;
+
+LTB_DEV void super_ring_issue(TileRing& r, unsigned g, const double* src, uint64_t policy) {
+  const int s = g % kSRing;
+  mbar_arrive_expect_tx(r.full + s, kTile * sizeof(double));
+  bulk_g2s(r.stage + (size_t)s * kTile, src, kTile * sizeof(double), r.full + s, policy);
+}
+
+LTB_DEV void super_worker(const DistArgs& a, const RankView& rv, SuperWorkerSmem& sm, TileRing& ring, int* tq,
+                          uint64_t policy) {
+  const int tid = threadIdx.x, i = tid & 63, q = tid >> 6, nb = a.nb;
+  const double* yf = rv.recv + off_yf(nb);
+  const double* xb = rv.recv + off_xb(nb);
+  const long long ntasks = a.ntasks;
+  // issue cursor (tid 0 only): current task ik, next tile ie
+  int grabbed = 0, ie = 0;
+  SuperTask ik{};
+  bool ihave = true;
+  unsigned issued = 0, used = 0;
+  auto issue_one = [&]() {
+    while (ihave && (grabbed == 0 || ie >= ik.nt)) {
+      const long long t = (long long)atomicAdd(a.stask, 1u);
+      ihave = t < ntasks && super_task(a, t, &ik);
+      tq[grabbed % kTaskQ] = ihave ? (int)t : -1;
+      ++grabbed;
+      ie = 0;
+    }
+    if (!ihave) return;
+    super_ring_issue(ring, issued, super_task_tile(rv, ik, ie), policy);
+    ++issued;
+    ++ie;
+  };
+  if (tid == 0)
+    for (int s = 0; s < kSRing; ++s) issue_one();
+  for (int m = 0;; ++m) {
+    __syncthreads();  // tq[m] written (by tid 0, before this barrier)
+    const int t = tq[m % kTaskQ];
+    if (t < 0) break;
+    SuperTask k;
+    super_task(a, t, &k);
+    double acc[kCPT];
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) acc[c] = 0.0;
+    // the solution values of tile e + 1 are loaded while tile e computes
+    unsigned long long vraw[kCPT];
+    auto vload = [&](int e) {
+      if (k.dir == 0) {
+#pragma unroll
+        for (int c = 0; c < kCPT; ++c) vraw[c] = ld_relaxed_u64(yf + (size_t)(k.k0 + e) * kTB + kCPT * q + c);
+      } else {
+        vraw[0] = ld_relaxed_u64(xb + (size_t)(k.k0 - e) * kTB + i);
+      }
+    };
+    vload(0);
+    for (int e = 0; e < k.nt; ++e) {
+      const unsigned g = used++;
+      if (k.dir == 0) {
+        // y_J, columns [8q, 8q + 8) of tile L_IJ, row i
+        poll_block<kCPT>(vraw, yf + (size_t)(k.k0 + e) * kTB + kCPT * q, 1, a.status);
+        double yv[kCPT];
+#pragma unroll
+        for (int c = 0; c < kCPT; ++c) yv[c] = __longlong_as_double((long long)vraw[c]);
+        if (e + 1 < k.nt) vload(e + 1);
+        mbar_wait(ring.full + g % kSRing, (g / kSRing) & 1);
+        const double* T = ring.stage + (size_t)(g % kSRing) * kTile;
+#pragma unroll
+        for (int c = 0; c < kCPT; ++c) acc[c] = fma(T[(kCPT * q + c) * kTB + i], yv[c], acc[c]);
+      } else {
+        // x_T[j = i] times row i of tile L_TJ, columns [8q, 8q + 8)
+        const double xj = vraw[0] != kSentinel ? __longlong_as_double((long long)vraw[0])
+                                               : poll_value(xb + (size_t)(k.k0 - e) * kTB + i, a.status);
+        if (e + 1 < k.nt) vload(e + 1);
+        mbar_wait(ring.full + g % kSRing, (g / kSRing) & 1);
+        const double* T = ring.stage + (size_t)(g % kSRing) * kTile;
+#pragma unroll
+        for (int c = 0; c < kCPT; ++c) acc[c] = fma(T[(kCPT * q + c) * kTB + i], xj, acc[c]);
+      }
+      __syncthreads();  // stage consumed
+      if (tid == 0) issue_one();
+    }
+    // reduce to the task's 64 partial sums
+    double* out = a.spart + super_slot(nb, k.dir, k.rc, k.part);
+    if (k.dir == 0) {
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < kCPT; ++c) v += acc[c];
+      sm.red[q][i] = v;
+      __syncthreads();
+      if (tid < kTB) out[tid] = handoff(red_sum(sm.red, tid));
+    } else {
+#pragma unroll
+      for (int c = 0; c < kCPT; ++c) {
+        double v = acc[c];
+#pragma unroll
+        for (int m2 = 16; m2 > 0; m2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m2);
+        acc[c] = v;
+      }
+      if ((i & 31) == 0) {
+#pragma unroll
+        for (int c = 0; c < kCPT; ++c) sm.sR[(i >> 5) * kTB + kCPT * q + c] = acc[c];
+      }
+      __syncthreads();
+      if (tid < kTB) out[tid] = handoff(sm.sR[tid] + sm.sR[kTB + tid]);
+    }
+  }
+}
+
+LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
+  const int tid = threadIdx.x, nb = a.nb, ns = a.ns, nrow = nb * kTB, chs = super_chs(ns);
+  double* buf = reinterpret_cast<double*>(dsm);     // [2][kSRows][kSRowLen]
+  double* vin = buf + 2 * kSRows * kSRowLen;        // [kSRowLen]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vin + kSRowLen);
+  __shared__ double part[kSRows][kThreads / kSRows / 32];
+  const RankView rv = a.loc[0];
+  double* yf = rv.recv + off_yf(nb);
+  double* xb = rv.recv + off_xb(nb);
+  constexpr unsigned kBytes = kSRows * kSRowLen * sizeof(double);
+  auto rows_of = [&](int u) {
+    const int S = u < ns ? u : 2 * ns - 1 - u;
+    return (u < ns ? a.sfwd : a.sbwd) + ((size_t)S * kSR + (size_t)g * kSRows) * kSRowLen;
+  };
+  // step u + 2's rows are pulled into L2 while step u runs (the workers'
+  // panel streams saturate HBM; a bulk copy issued only one step ahead
+  // would wait behind them)
+  auto l2_prefetch = [&](int u) {
+    if (u < 2 * ns)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rows_of(u)), "r"(kBytes) : "memory");
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, kBytes);
+    bulk_g2s(buf, rows_of(0), kBytes, bar, policy_evict_first());
+    l2_prefetch(1);
+  }
+  __syncthreads();
+  constexpr int TPR = kThreads / kSRows;  // threads per row
+  const int row = tid / TPR, sub = tid % TPR;
+  for (int u = 0; u < 2 * ns; ++u) {
+    const bool fwd = u < ns;
+    const int S = fwd ? u : 2 * ns - 1 - u;
+    if (tid == 0 && u + 1 < 2 * ns) {  // that buffer was consumed in step u - 1
+      const int nx = (u + 1) & 1;
+      mbar_arrive_expect_tx(bar + nx, kBytes);
+      bulk_g2s(buf + (size_t)nx * kSRows * kSRowLen, rows_of(u + 1), kBytes, bar + nx, policy_evict_first());
+      l2_prefetch(u + 2);
+    }
+    {
+      // [c_S; y_{S-1}] (forward) or [d_S; x_{S+1}] (backward), 0 past the factor
+      const int k = tid, gr = S * kSR + k, rc = gr / kTB, ii = gr % kTB;
+      double v = 0.0;
+      if (gr < nrow) {
+        const int np = fwd ? super_parts_f(S, chs) : super_parts_b(S, ns, chs);
+        const double* ps = a.spart + super_slot(nb, fwd ? 0 : 1, rc, 0) + ii;
+        unsigned long long raw[kMaxParts];
+#pragma unroll
+        for (int c = 0; c < kMaxParts; ++c) raw[c] = c < np ? ld_relaxed_u64(ps + (size_t)c * kTB) : 0ull;
+        v = fwd ? __ldg(rv.b + gr) : poll_value(yf + gr, a.status);
+        poll_block<kMaxParts>(raw, ps, kTB, a.status);
+#pragma unroll
+        for (int c = 0; c < kMaxParts; ++c)
+          if (c < np) v -= __longlong_as_double((long long)raw[c]);
+      }
+      vin[k] = v;
+#pragma unroll
+      for (int d = 2; d <= kSLook; ++d) {
+        const int pS = fwd ? S - d : S + d, pr = pS * kSR + k;
+        vin[d * kSR + k] = (pS >= 0 && pS < ns && pr < nrow) ? poll_value((fwd ? yf : xb) + pr, a.status) : 0.0;
+      }
+    }
+    __syncthreads();
+    if (a.trace && g == 0 && tid == 0) a.trace[2 + 2 * ns + u] = globaltimer();  // inputs resolved
+    mbar_wait_bounded(bar + (u & 1), (u >> 1) & 1, a.status);
+    const double* R = buf + (size_t)(u & 1) * kSRows * kSRowLen + (size_t)row * kSRowLen;
+    // everything but the previous step's block first, then (the critical
+    // path) poll y_{S-1} / x_{S+1} and add its 512 columns
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSR / TPR; ++q) acc = fma(R[sub + q * TPR], vin[sub + q * TPR], acc);
+#pragma unroll 8
+    for (int q = 2 * kSR / TPR; q < kSRowLen / TPR; ++q) acc = fma(R[sub + q * TPR], vin[sub + q * TPR], acc);
+    {
+      const int pS = fwd ? S - 1 : S + 1, pr = pS * kSR + tid;
+      vin[kSR + tid] = (pS >= 0 && pS < ns && pr < nrow) ? poll_value((fwd ? yf : xb) + pr, a.status) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSR / TPR; ++q) acc = fma(R[kSR + sub + q * TPR], vin[kSR + sub + q * TPR], acc);
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if ((tid & 31) == 0) part[row][sub >> 5] = acc;
+    __syncthreads();
+    if (sub == 0) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < TPR / 32; ++w) v += part[row][w];
+      const int gr = S * kSR + g * kSRows + row;
+      if (gr < nrow) (fwd ? yf : xb)[gr] = handoff(v);
+    }
+    __syncthreads();
+    if (a.trace && g == 0 && tid == 0) a.trace[2 + u] = globaltimer();  // step published
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) trsv_super_kernel(const DistArgs a) {
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  const int nb = a.nb;
+  const RankView rv = a.loc[0];
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[0] = globaltimer();
+  {
+    const size_t n1 = off_ready(nb), n2 = recv_len(nb, 1) - off_cf(nb), n3 = super_slot(nb, 2, 0, 0);
+    unsigned long long* base = reinterpret_cast<unsigned long long*>(rv.recv);
+    unsigned long long* sp = reinterpret_cast<unsigned long long*>(a.spart);
+    for (size_t e = (size_t)blockIdx.x * kThreads + threadIdx.x; e < n1 + n2 + n3; e += (size_t)gridDim.x * kThreads) {
+      if (e < n1) base[e] = kSentinel;
+      else if (e < n1 + n2) base[off_cf(nb) + (e - n1)] = kSentinel;
+      else sp[e - n1 - n2] = kSentinel;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.stask = 0u;
+  grid_barrier(a.gsync, a.status);
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[1] = globaltimer();
+  if ((int)blockIdx.x < a.nchain) {
+    super_chain(a, ring_smem, blockIdx.x);
+  } else {
+    TileRing ring;
+    ring.stage = reinterpret_cast<double*>(ring_smem);
+    ring.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kSRing * kTile * sizeof(double));
+    ring.next = 0;
+    uint64_t policy = 0;
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < kSRing; ++st) mbar_init(ring.full + st, 1);
+      fence_mbar_init();
+      policy = policy_evict_first();
+    }
+    __syncthreads();
+    SuperWorkerSmem& wsm = *reinterpret_cast<SuperWorkerSmem*>(ring_smem + kWorkerSmemOff);
+    int* tq = reinterpret_cast<int*>(ring_smem + kWorkerSmemOff + sizeof(SuperWorkerSmem));
+    super_worker(a, rv, wsm, ring, tq, policy);
+  }
+  {
+    const double* xb = rv.recv + off_xb(nb);
+    for (size_t e = (size_t)blockIdx.x * kThreads + threadIdx.x; e < (size_t)nb * kTB; e += (size_t)gridDim.x * kThreads)
+      (void)poll_value(xb + e, a.status);
+  }
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[2 + 4 * a.ns] = globaltimer();
+}
+
 constexpr size_t kRingSmem = (size_t)kRing * kTile * sizeof(double) + kRing * sizeof(uint64_t);
 static_assert(kCStages * 2 * kHalfTile + (kMaxLook - 1) * kYSlots * kTB <= kRing * kTile && kCStages <= kRing,
               "the chain's tile stages and partial sums live in the worker ring's space");
@@ -916,6 +1258,134 @@ __global__ void chain_scatter_kernel(const double* __restrict__ buf, int q, int 
   for (int e = threadIdx.x; e < kTile; e += blockDim.x) M[chain_idx(look, I, k - 1, e & 63, e >> 6)] = C[e];
 }
 
+// ---- super-block chain rows (prepare_super, P = 1) ----
+// 64x64 tile (r, c) = src[r * rs + c * cs] into s[r * kPad + c] (transposed
+// when trans)
+LTB_DEV void super_load(double* s, const double* src, size_t rs, size_t cs, bool trans) {
+  for (int e = threadIdx.x; e < kTile; e += blockDim.x) {
+    const int r = e & 63, c = e >> 6;
+    const double v = src[(size_t)r * rs + (size_t)c * cs];
+    if (trans) s[c * kPad + r] = v;
+    else s[r * kPad + c] = v;
+  }
+}
+// acc[t] (row i = tid & 63, column 16 (tid >> 6) + t) += (A B)[i][col]
+LTB_DEV void super_mm(const double* sA, const double* sB, double (&acc)[16]) {
+  const int i = threadIdx.x & 63, c0 = 16 * (threadIdx.x >> 6);
+  for (int l = 0; l < kTB; ++l) {
+    const double av = sA[i * kPad + l];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = fma(av, sB[l * kPad + c0 + t], acc[t]);
+  }
+}
+LTB_DEV void super_store(double* dst, size_t rs, const double (&acc)[16], double scale) {
+  const int i = threadIdx.x & 63, c0 = 16 * (threadIdx.x >> 6);
+#pragma unroll
+  for (int t = 0; t < 16; ++t) dst[(size_t)i * rs + c0 + t] = scale * acc[t];
+}
+LTB_DEV const double* ptile(const double* tiles, int I, int J) {
+  return tiles + (row_off(I, 0, 1) + (size_t)J) * kTile;
+}
+
+// X = L_SS^{-1}, block column J of super block S = blockIdx.(x, y), into the
+// first half of the forward rows: X_JJ = Dinv_JJ, X_IJ = -Dinv_II sum_{J<=K<I}
+// L_IK X_KJ (tile indices inside the super block; identity past the factor)
+__global__ void __launch_bounds__(256) super_inv_kernel(const double* __restrict__ tiles,
+                                                        const double* __restrict__ dinv, int nb,
+                                                        double* __restrict__ sfwd) {
+  extern __shared__ double su_smem[];
+  double* sA = su_smem;
+  double* sB = su_smem + kTB * kPad;
+  const int S = blockIdx.x, J = blockIdx.y, b0 = S * kSB;
+  double* rows = sfwd + (size_t)S * kSR * kSRowLen;
+  auto xt = [&](int I, int K) { return rows + (size_t)(I * kTB) * kSRowLen + K * kTB; };
+  if (b0 + J >= nb) {  // padding: identity
+    for (int e = threadIdx.x; e < kTB; e += blockDim.x) xt(J, J)[(size_t)e * kSRowLen + e] = 1.0;
+    return;
+  }
+  {
+    const double* D = dinv + (size_t)(b0 + J) * kTile;
+    for (int e = threadIdx.x; e < kTile; e += blockDim.x) xt(J, J)[(size_t)(e & 63) * kSRowLen + (e >> 6)] = D[e];
+  }
+  for (int I = J + 1; I < kSB && b0 + I < nb; ++I) {
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    for (int K = J; K < I; ++K) {
+      __syncthreads();  // X_KJ written; previous operands consumed
+      super_load(sA, ptile(tiles, b0 + I, b0 + K), 1, kTB, false);
+      super_load(sB, xt(K, J), kSRowLen, 1, false);
+      __syncthreads();
+      super_mm(sA, sB, acc);
+    }
+    __syncthreads();
+    super_load(sA, dinv + (size_t)(b0 + I) * kTile, 1, kTB, false);
+    {  // sB = acc
+      const int i = threadIdx.x & 63, c0 = 16 * (threadIdx.x >> 6);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) sB[i * kPad + c0 + t] = acc[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    super_mm(sA, sB, acc);
+    super_store(xt(I, J), kSRowLen, acc, -1.0);
+  }
+}
+
+// the -Mk parts (k = 1 .. kSLook, columns k kSR ..): forward row tile I of S:
+// -Mk_S = -L_SS^{-1} L_{S,S-k} (dir 0, S >= k); backward -Mk'_S =
+// -L_SS^{-T} L_{S+k,S}^T (dir 1, S + k < ns).  Tile (I, J) = sum_K X_IK
+// L_{S,K ; S-k,J}  or  sum_K X_KI^T L_{S+k,J ; S,K}^T.  blockIdx.z = 2 (k - 1)
+// + dir.  (sfwd and sfwd_out are the same rows: read the inverse part,
+// write the Mk parts -- not __restrict__)
+__global__ void __launch_bounds__(256) super_m_kernel(const double* __restrict__ tiles, int nb, int ns,
+                                                      const double* sfwd, double* __restrict__ sbwd,
+                                                      double* sfwd_out) {
+  extern __shared__ double su_smem[];
+  double* sA = su_smem;
+  double* sB = su_smem + kTB * kPad;
+  const int S = blockIdx.x, I = blockIdx.y, dir = blockIdx.z & 1, dist = 1 + (blockIdx.z >> 1), b0 = S * kSB;
+  if ((dir == 0 && S < dist) || (dir == 1 && S + dist >= ns) || b0 + I >= nb) return;
+  const double* X = sfwd + (size_t)S * kSR * kSRowLen;
+  auto xt = [&](int R, int K) { return X + (size_t)(R * kTB) * kSRowLen + K * kTB; };
+  for (int J = 0; J < kSB; ++J) {
+    const int lr = dir == 0 ? 0 : b0 + dist * kSB + J;  // backward: L row block of S + dist
+    if (dir == 1 && lr >= nb) break;
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    const int k0 = dir == 0 ? 0 : I, k1 = dir == 0 ? I : kSB - 1;
+    for (int K = k0; K <= k1 && b0 + K < nb; ++K) {
+      __syncthreads();
+      if (dir == 0) {
+        super_load(sA, xt(I, K), kSRowLen, 1, false);
+        super_load(sB, ptile(tiles, b0 + K, b0 - dist * kSB + J), 1, kTB, false);
+      } else {
+        super_load(sA, xt(K, I), kSRowLen, 1, true);
+        super_load(sB, ptile(tiles, lr, b0 + K), 1, kTB, true);
+      }
+      __syncthreads();
+      super_mm(sA, sB, acc);
+    }
+    double* out = (dir == 0 ? sfwd_out : sbwd) + (size_t)S * kSR * kSRowLen + (size_t)(I * kTB) * kSRowLen +
+                  dist * kSR + J * kTB;
+    super_store(out, kSRowLen, acc, -1.0);
+  }
+}
+
+// first half of the backward rows: L_SS^{-T}
+__global__ void super_transpose_kernel(const double* __restrict__ sfwd, double* __restrict__ sbwd) {
+  __shared__ double t[32][33];
+  const size_t base = (size_t)blockIdx.z * kSR * kSRowLen;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y)
+    t[k][threadIdx.x] = sfwd[base + (size_t)(r0 + k) * kSRowLen + c0 + threadIdx.x];
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y)
+    sbwd[base + (size_t)(c0 + k) * kSRowLen + r0 + threadIdx.x] = t[threadIdx.x][k];
+}
+
 constexpr int kMaxDevices = 64;
 // co-resident CTA count per (device, cluster size), measured once per device
 int g_coop_blocks[kMaxDevices][kMaxLook + 1];
@@ -977,6 +1447,75 @@ cudaError_t coop_blocks(int look, int* out) {
   return cudaSuccess;
 }
 
+// The workers' task list, sorted by urgency: a task is READY after the chain
+// step that publishes its last input block and DUE at the chain step that
+// adds its sum; ordering by ready + due (both in chain-step time) keeps
+// HBM busy with early-ready work while the tasks the chain needs next come
+// first among equally ready ones.
+cudaError_t build_super_tasks(TriFactor& t) {
+  const int nb = t.nb, ns = t.ns, chs = super_chs(ns), np = (ns + chs - 1) / chs;
+  struct Item {
+    int key;
+    int4 v;
+  };
+  std::vector<Item> items;
+  for (int c = 0; c < np; ++c)
+    for (int I = kSB * (c * chs + kSLook + 1); I < nb; ++I) {
+      const int S = I / kSB, k0 = kSB * c * chs, k1 = kSB * std::min((c + 1) * chs, S - kSLook);
+      const int ready = k1 / kSB - 1, due = S;
+      items.push_back({ready + due, make_int4(0 | (c << 1), I, k0, k1 - k0)});
+    }
+  for (int c = 0; c < np; ++c)
+    for (int J = std::min(nb, kSB * (ns - c * chs - kSLook - 1)) - 1; J >= 0; --J) {
+      const int S = J / kSB;
+      const int top = std::min(nb, kSB * (ns - c * chs)), lo = kSB * std::max(S + kSLook + 1, ns - (c + 1) * chs);
+      // backward time runs from step ns - 1 down: t(s) = ns + (ns - 1 - s)
+      const int ready = ns + (ns - 1 - lo / kSB), due = ns + (ns - 1 - S);
+      items.push_back({ready + due, make_int4(1 | (c << 1), J, top - 1, top - lo)});
+    }
+  std::stable_sort(items.begin(), items.end(), [](const Item& x, const Item& y) { return x.key < y.key; });
+  std::vector<int4> list(items.size());
+  for (size_t i = 0; i < items.size(); ++i) list[i] = items[i].v;
+  cudaFree(t.stasks);
+  t.stasks = nullptr;
+  t.nstasks = (int)list.size();
+  if (list.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc(&t.stasks, list.size() * sizeof(int4));
+  if (e == cudaSuccess) e = cudaMemcpy(t.stasks, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice);
+  return e;
+}
+
+// super-block chain rows for a one-GPU factor (after dinv)
+cudaError_t prepare_super(TriFactor& t, cudaStream_t st) {
+  static const bool off = getenv("LTB_TRSV_NOSUPER") != nullptr;
+  if (t.P != 1 || t.nb > kSuperMaxNb || off) return cudaSuccess;
+  const int ns = (t.nb + kSB - 1) / kSB;
+  const size_t bytes = (size_t)ns * kSR * kSRowLen * sizeof(double);
+  cudaError_t e;
+  if (!t.sfwd || t.ns != ns) {
+    cudaFree(t.sfwd);
+    cudaFree(t.sbwd);
+    cudaFree(t.spart);
+    t.sfwd = t.sbwd = t.spart = nullptr;
+    const size_t pbytes = super_slot(t.nb, 2, 0, 0) * sizeof(double);
+    if ((e = cudaMalloc(&t.sfwd, bytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&t.sbwd, bytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&t.spart, pbytes)) != cudaSuccess) return e;
+    t.bytes += 2 * bytes + pbytes;
+  }
+  t.ns = ns;
+  if ((e = build_super_tasks(t)) != cudaSuccess) return e;
+  const int smem = 2 * kTB * kPad * (int)sizeof(double);
+  cudaFuncSetAttribute(super_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(super_m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaMemsetAsync(t.sfwd, 0, bytes, st);
+  cudaMemsetAsync(t.sbwd, 0, bytes, st);
+  super_inv_kernel<<<dim3(ns, kSB), 256, smem, st>>>(t.tiles, t.dinv, t.nb, t.sfwd);
+  super_transpose_kernel<<<dim3(kSR / 32, kSR / 32, ns), dim3(32, 8), 0, st>>>(t.sfwd, t.sbwd);
+  super_m_kernel<<<dim3(ns, kSB, 2 * kSLook), 256, smem, st>>>(t.tiles, t.nb, ns, t.sfwd, t.sbwd, t.sfwd);
+  return cudaGetLastError();
+}
+
 cudaError_t prepare(TriFactor& t, bool gen, uint64_t key, double scale, cudaStream_t st) {
   const int smem = 2 * kTB * kPad * (int)sizeof(double);
   cudaFuncSetAttribute(invert_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -986,6 +1525,7 @@ cudaError_t prepare(TriFactor& t, bool gen, uint64_t key, double scale, cudaStre
     chain_tiles_kernel<<<dim3(t.nb, t.look, 2), 256, smem, st>>>(gen, t.tiles, key, scale, t.n, t.dinv,
                                                                    t.mf, t.mb, t.nb, t.look);
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = prepare_super(t, st);
   if (e != cudaSuccess) return e;
   int h = 0;
   e = cudaMemcpyAsync(&h, t.status, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -1015,7 +1555,63 @@ DistArgs make_args(TriFactor* const* ts, const double* const* bs, int nloc, int 
   a.gsync = t0.gsync;
   a.status = t0.status;
   a.trace = t0.rank == 0 ? t0.trace : nullptr;
+  a.sfwd = t0.sfwd;
+  a.sbwd = t0.sbwd;
+  a.spart = t0.spart;
+  a.stask = t0.gsync + 2;
+  a.stlist = reinterpret_cast<const int4*>(t0.stasks);
+  a.ntasks = t0.nstasks;
+  a.ns = t0.ns;
+  a.nchain = kSChain;
   return a;
+}
+
+constexpr size_t kSuperWorkerSmem = kWorkerSmemOff + sizeof(SuperWorkerSmem) + kTaskQ * sizeof(int);
+constexpr size_t kSuperSmem = kSuperWorkerSmem > kSChainSmem ? kSuperWorkerSmem : kSChainSmem;
+static_assert(kSuperSmem <= 227 * 1024, "super kernel shared memory");
+int g_super_blocks[kMaxDevices];
+std::once_flag g_super_once;
+
+// co-resident CTAs of trsv_super_kernel on the current device
+cudaError_t super_blocks(int* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(g_super_once, [] {
+    for (int& v : g_super_blocks) v = -1;
+  });
+  std::lock_guard<std::mutex> lk(g_coop_mu);
+  int& cb = g_super_blocks[dev];
+  if (cb < 0) {  // once per device: the shared-memory opt-in and the occupancy
+    e = cudaFuncSetAttribute(trsv_super_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSuperSmem);
+    if (e != cudaSuccess) return e;
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_super_kernel, kThreads, kSuperSmem);
+    cb = sms * per;
+  }
+  *out = cb;
+  return cudaSuccess;
+}
+
+cudaError_t super_launch(const DistArgs& a, int grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSuperSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  static const bool no_coop = getenv("LTB_TRSV_NONCOOP") != nullptr;
+  cfg.numAttrs = no_coop ? 0 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_super_kernel, a);
+  if (e == cudaSuccess || no_coop || e == cudaErrorCooperativeLaunchTooLarge) return e;
+  cudaGetLastError();
+  cfg.numAttrs = 0;  // (as launch(): bounded waits, never a hang)
+  return cudaLaunchKernelEx(&cfg, trsv_super_kernel, a);
 }
 
 cudaError_t launch(const DistArgs& a, cudaStream_t st) {
@@ -1075,10 +1671,10 @@ cudaError_t trsv_alloc(TriFactor& t, int n, int P, int rank) {
     if ((e = cudaMalloc(&t.mb, chain * sizeof(double))) != cudaSuccess) return e;
   }
   if ((e = cudaMalloc(&t.recv, rl * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.gsync, 2 * sizeof(unsigned))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.gsync, 4 * sizeof(unsigned))) != cudaSuccess) return e;  // barrier + task counter
   if ((e = cudaMalloc(&t.status, sizeof(int))) != cudaSuccess) return e;
   cudaMemset(t.recv, 0, rl * sizeof(double));  // ready flags = 0
-  cudaMemset(t.gsync, 0, 2 * sizeof(unsigned));
+  cudaMemset(t.gsync, 0, 4 * sizeof(unsigned));
   cudaMemset(t.status, 0, sizeof(int));
   for (int p = 0; p < kMaxRanks; ++p) t.peer_recv[p] = nullptr;
   t.peer_recv[rank] = t.recv;
@@ -1092,6 +1688,10 @@ void trsv_free(TriFactor& t) {
   cudaFree(t.dinv);
   cudaFree(t.mf);
   cudaFree(t.mb);
+  cudaFree(t.sfwd);
+  cudaFree(t.sbwd);
+  cudaFree(t.spart);
+  cudaFree(t.stasks);
   cudaFree(t.recv);
   cudaFree(t.gsync);
   cudaFree(t.status);
@@ -1213,6 +1813,16 @@ std::mutex& trsv_device_mutex(int dev) {
 cudaError_t trsv_solve(TriFactor& t, const double* b, cudaStream_t st) {
   for (int p = 0; p < t.P; ++p)
     if (!t.peer_recv[p]) return cudaErrorInvalidValue;  // not connected
+  if (t.sfwd && t.P == 1) {
+    int blocks = 0;
+    cudaError_t e = super_blocks(&blocks);
+    if (e != cudaSuccess) return e;
+    if (blocks > kSChain) {
+      TriFactor* ts[1] = {&t};
+      const double* bs[1] = {b};
+      return super_launch(make_args(ts, bs, 1, 0), std::min(blocks, kSChain + t.nb), st);
+    }
+  }
   int blocks = 0;
   cudaError_t e = coop_blocks(t.look, &blocks);
   if (e != cudaSuccess) return e;

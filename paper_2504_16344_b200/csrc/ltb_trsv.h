@@ -21,6 +21,10 @@ constexpr int kMaxLook = 8;    // diagonal-chain lookahead depth bound (chain te
 // co-resident).  Every rank of a distributed factor picks the same depth.
 inline int trsv_look_for(int nb) { return nb <= 256 ? 8 : 4; }
 constexpr int kMaxRanks = 8;
+// one GPU up to this many 64-blocks solves through the super-block chain
+// (8 blocks per chain step); beyond, streaming the panel dominates and the
+// head/tail chain kernel runs
+constexpr int kSuperMaxNb = 512;
 
 // Row-cyclic block distribution over P ranks: rank r holds the 64-row block
 // rows I = r, r+P, r+2P, ... packed row after row (row I has I+1 tiles,
@@ -47,6 +51,14 @@ struct TriFactor {
   unsigned* gsync = nullptr;  // local grid barrier words
   int* status = nullptr;      // device error word (spin timeout / bad pivot)
   unsigned long long* trace = nullptr;  // diagnostic timestamps, 4 nb + 1 (optional)
+  // P = 1, nb <= kSuperMaxNb: rows [L_SS^{-1} | -M_S] / [L_SS^{-T} | -M'_S]
+  // of the super-block chain (ltb_trsv.cu trsv_super_kernel), ns blocks
+  double* sfwd = nullptr;
+  double* sbwd = nullptr;
+  double* spart = nullptr;  // the workers' partial sums
+  void* stasks = nullptr;   // their task list (int4 each)
+  int nstasks = 0;
+  int ns = 0;
   unsigned epoch = 0;
   size_t bytes = 0;
 };

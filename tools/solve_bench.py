@@ -1,5 +1,6 @@
 """K^{-1} apply latency at config 2 (n = 8192) and a larger n (dev tool):
-device time of solve_k_inplace on a CUDA tensor (CUDA events, median)."""
+device time of solve_k_inplace on a CUDA tensor (CUDA events, median).
+    python tools/solve_bench.py [nd:nt ...]"""
 import sys
 
 import torch
@@ -7,7 +8,10 @@ import torch
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import paper_2504_16344_b200 as ltb  # noqa: E402
 
-for nd, nt in [(64, 128), (600, 64)]:
+shapes = [(64, 128), (600, 64)]
+if len(sys.argv) > 1:  # nd:nt pairs
+    shapes = [tuple(int(v) for v in a.split(":")) for a in sys.argv[1:]]
+for nd, nt in shapes:
     g = ltb.MatvecPlan.generated(nd, 64, nt, seed=1, tag=ltb.KernelTag.Gstar)
     eng = ltb.InferenceEngine(g)
     eng.set_factor_generated(4321)
