@@ -773,6 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
 // thereby streamed by many SMs at once: a row-per-worker split leaves the
 // last rows (3.9 MB at n = 8192) to one SM each, which bounds the sweep.
 constexpr int kSLook = 2;                 // previous super blocks the chain applies itself
+// (super_chain hands y_{S-1} of one step on as y_{S-2} of the next: kSLook == 2)
 constexpr int kSRowLen = (1 + kSLook) * kSR;  // [inverse | -M1 | -M2] row
 constexpr size_t kSChainSmem = (size_t)(2 * kSRows * kSRowLen + kSRowLen) * sizeof(double) + 2 * sizeof(uint64_t);
 // super kernel workers: a kSRing-deep tile ring (deeper than the cluster
@@ -784,7 +785,7 @@ struct SuperWorkerSmem {
   double red[kQ][kTB];
   double sR[2 * kTB];
 };
-constexpr size_t kWorkerSmemOff = ((size_t)kSRing * kTile * sizeof(double) + kSRing * sizeof(uint64_t) + 127) / 128 * 128;
+constexpr size_t kWorkerSmemOff = ((size_t)kSRing * kTile * sizeof(double) + 2 * kSRing * sizeof(uint64_t) + 127) / 128 * 128;
 constexpr int kMaxParts = 8;
 
 // super blocks per task for ns super blocks: <= kMaxParts partials per row
@@ -827,47 +828,53 @@ LTB_DEV const double* super_task_tile(const RankView& rv, const SuperTask& k, in
                     : rv.tiles + (row_off(k.k0 - e, 0, 1) + (size_t)k.rc) * kTile;
 }
 
-// one worker's task stream: tasks are taken from a global counter (in the
-// order their inputs appear) when the TMA ring's issue cursor reaches them
-// (tid 0) and queued in shared memory for the consumer; every tile goes
-// through the ring, kRing tiles ahead across task boundaries
+// A worker CTA of the super kernel is 16 consumer warps + 1 producer warp.
+// The producer takes tasks from the global counter (in urgency order), queues
+// each task id in shared memory and streams its tiles into a kSRing-deep
+// TMA ring, refilling a stage once all 16 consumer warps released it (empty
+// barrier); the consumers pick the task id up after the task's first tile
+// landed (the producer's arrive on that full barrier releases the id) and
+// hand off a 64-value partial sum per task.
 constexpr int kTaskQ = kSRing + 2;
+constexpr int kSThreads = kThreads + 32;  // super kernel: + the producer warp
+
+LTB_DEV void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
 LTB_DEV void super_ring_issue(TileRing& r, unsigned g, const double* src, uint64_t policy) {
   const int s = g % kSRing;
+  if (g >= (unsigned)kSRing) mbar_wait(r.full + kSRing + s, (g / kSRing - 1) & 1);
   mbar_arrive_expect_tx(r.full + s, kTile * sizeof(double));
   bulk_g2s(r.stage + (size_t)s * kTile, src, kTile * sizeof(double), r.full + s, policy);
 }
 
-LTB_DEV void super_worker(const DistArgs& a, const RankView& rv, SuperWorkerSmem& sm, TileRing& ring, int* tq,
-                          uint64_t policy) {
+LTB_DEV void super_producer(const DistArgs& a, const RankView& rv, TileRing& ring, int* tq, uint64_t policy) {
+  unsigned issued = 0;
+  int m = 0;
+  for (;;) {
+    const long long t = (long long)atomicAdd(a.stask, 1u);
+    if (t >= a.ntasks) break;
+    SuperTask k;
+    super_task(a, t, &k);
+    tq[m++ % kTaskQ] = (int)t;  // released by the arrive of the task's first tile
+    for (int e = 0; e < k.nt; ++e) super_ring_issue(ring, issued++, super_task_tile(rv, k, e), policy);
+  }
+  // terminator: a plain arrive completes the next stage's phase with no data
+  const int s = issued % kSRing;
+  if (issued >= (unsigned)kSRing) mbar_wait(ring.full + kSRing + s, (issued / kSRing - 1) & 1);
+  tq[m % kTaskQ] = -1;
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ring.full + s)) : "memory");
+}
+
+LTB_DEV void super_consumer(const DistArgs& a, const RankView& rv, SuperWorkerSmem& sm, TileRing& ring,
+                            const int* tq) {
   const int tid = threadIdx.x, i = tid & 63, q = tid >> 6, nb = a.nb;
   const double* yf = rv.recv + off_yf(nb);
   const double* xb = rv.recv + off_xb(nb);
-  const long long ntasks = a.ntasks;
-  // issue cursor (tid 0 only): current task ik, next tile ie
-  int grabbed = 0, ie = 0;
-  SuperTask ik{};
-  bool ihave = true;
-  unsigned issued = 0, used = 0;
-  auto issue_one = [&]() {
-    while (ihave && (grabbed == 0 || ie >= ik.nt)) {
-      const long long t = (long long)atomicAdd(a.stask, 1u);
-      ihave = t < ntasks && super_task(a, t, &ik);
-      tq[grabbed % kTaskQ] = ihave ? (int)t : -1;
-      ++grabbed;
-      ie = 0;
-    }
-    if (!ihave) return;
-    super_ring_issue(ring, issued, super_task_tile(rv, ik, ie), policy);
-    ++issued;
-    ++ie;
-  };
-  if (tid == 0)
-    for (int s = 0; s < kSRing; ++s) issue_one();
+  unsigned used = 0;
+  long long w_y = 0, w_t = 0, n_tiles = 0, t_start = clock64();  // (trace) waits for y / x, for tiles
   for (int m = 0;; ++m) {
-    __syncthreads();  // tq[m] written (by tid 0, before this barrier)
-    const int t = tq[m % kTaskQ];
+    mbar_wait(ring.full + used % kSRing, (used / kSRing) & 1);  // the task's first tile (or the terminator)
+    const int t = *(volatile const int*)(tq + m % kTaskQ);
     if (t < 0) break;
     SuperTask k;
     super_task(a, t, &k);
@@ -887,14 +894,18 @@ LTB_DEV void super_worker(const DistArgs& a, const RankView& rv, SuperWorkerSmem
     vload(0);
     for (int e = 0; e < k.nt; ++e) {
       const unsigned g = used++;
+      long long c0 = clock64();
       if (k.dir == 0) {
         // y_J, columns [8q, 8q + 8) of tile L_IJ, row i
         poll_block<kCPT>(vraw, yf + (size_t)(k.k0 + e) * kTB + kCPT * q, 1, a.status);
         double yv[kCPT];
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) yv[c] = __longlong_as_double((long long)vraw[c]);
+        w_y += clock64() - c0;
         if (e + 1 < k.nt) vload(e + 1);
+        c0 = clock64();
         mbar_wait(ring.full + g % kSRing, (g / kSRing) & 1);
+        w_t += clock64() - c0;
         const double* T = ring.stage + (size_t)(g % kSRing) * kTile;
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) acc[c] = fma(T[(kCPT * q + c) * kTB + i], yv[c], acc[c]);
@@ -902,14 +913,20 @@ LTB_DEV void super_worker(const DistArgs& a, const RankView& rv, SuperWorkerSmem
         // x_T[j = i] times row i of tile L_TJ, columns [8q, 8q + 8)
         const double xj = vraw[0] != kSentinel ? __longlong_as_double((long long)vraw[0])
                                                : poll_value(xb + (size_t)(k.k0 - e) * kTB + i, a.status);
+        w_y += clock64() - c0;
         if (e + 1 < k.nt) vload(e + 1);
+        c0 = clock64();
         mbar_wait(ring.full + g % kSRing, (g / kSRing) & 1);
+        w_t += clock64() - c0;
         const double* T = ring.stage + (size_t)(g % kSRing) * kTile;
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) acc[c] = fma(T[(kCPT * q + c) * kTB + i], xj, acc[c]);
       }
-      __syncthreads();  // stage consumed
-      if (tid == 0) issue_one();
+      __syncwarp();  // this warp is done with the stage
+      if ((tid & 31) == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ring.full + kSRing + g % kSRing))
+                     : "memory");
+      ++n_tiles;
     }
     // reduce to the task's 64 partial sums
     double* out = a.spart + super_slot(nb, k.dir, k.rc, k.part);
@@ -918,7 +935,7 @@ LTB_DEV void super_worker(const DistArgs& a, const RankView& rv, SuperWorkerSmem
 #pragma unroll
       for (int c = 0; c < kCPT; ++c) v += acc[c];
       sm.red[q][i] = v;
-      __syncthreads();
+      consumers_sync();
       if (tid < kTB) out[tid] = handoff(red_sum(sm.red, tid));
     } else {
 #pragma unroll
@@ -932,9 +949,18 @@ LTB_DEV void super_worker(const DistArgs& a, const RankView& rv, SuperWorkerSmem
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) sm.sR[(i >> 5) * kTB + kCPT * q + c] = acc[c];
       }
-      __syncthreads();
+      consumers_sync();
       if (tid < kTB) out[tid] = handoff(sm.sR[tid] + sm.sR[kTB + tid]);
     }
+    consumers_sync();  // the reduction scratch is free again
+  }
+  if (a.trace && tid == 0) {
+    const int w = blockIdx.x - a.nchain;
+    a.trace[3 + 4 * a.ns + 3 * w] = (unsigned long long)w_y;
+    a.trace[3 + 4 * a.ns + 3 * w + 1] = (unsigned long long)w_t;
+    a.trace[3 + 4 * a.ns + 3 * w + 2] = (unsigned long long)(clock64() - t_start);
+    a.trace[3 + 4 * a.ns + 3 * 148 + 2 * w] = 0ull;
+    a.trace[3 + 4 * a.ns + 3 * 148 + 2 * w + 1] = (unsigned long long)n_tiles;
   }
 }
 
@@ -967,9 +993,26 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
     bulk_g2s(buf, rows_of(0), kBytes, bar, policy_evict_first());
     l2_prefetch(1);
   }
-  __syncthreads();
+  consumers_sync();
   constexpr int TPR = kThreads / kSRows;  // threads per row
   const int row = tid / TPR, sub = tid % TPR;
+  // Step u's own inputs -- the workers' partial sums of c_S / d_S and b_S /
+  // y_S -- are LOADED during step u - 1 (issue_in) and only resolved at the
+  // top of step u, so their round trip hides under step u - 1's critical
+  // path (its wait for the previous chain step's values).
+  unsigned long long praw[kMaxParts], hraw = 0ull;
+  int pnp = 0;
+  auto issue_in = [&](int u) {
+    const bool fw = u < ns;
+    const int S = fw ? u : 2 * ns - 1 - u, gr = S * kSR + tid;
+    pnp = gr < nrow ? (fw ? super_parts_f(S, chs) : super_parts_b(S, ns, chs)) : 0;
+    const double* ps = a.spart + super_slot(nb, fw ? 0 : 1, gr / kTB, 0) + gr % kTB;
+#pragma unroll
+    for (int c = 0; c < kMaxParts; ++c) praw[c] = c < pnp ? ld_relaxed_u64(ps + (size_t)c * kTB) : 0ull;
+    hraw = gr < nrow ? (fw ? (unsigned long long)__double_as_longlong(__ldg(rv.b + gr)) : ld_relaxed_u64(yf + gr))
+                     : 0ull;
+  };
+  issue_in(0);
   for (int u = 0; u < 2 * ns; ++u) {
     const bool fwd = u < ns;
     const int S = fwd ? u : 2 * ns - 1 - u;
@@ -980,29 +1023,23 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
       l2_prefetch(u + 2);
     }
     {
-      // [c_S; y_{S-1}] (forward) or [d_S; x_{S+1}] (backward), 0 past the factor
-      const int k = tid, gr = S * kSR + k, rc = gr / kTB, ii = gr % kTB;
+      // [c_S; -; y_{S-2}] (forward) or [d_S; -; x_{S+2}] (backward), 0 past the factor
+      const int k = tid, gr = S * kSR + k;
       double v = 0.0;
       if (gr < nrow) {
-        const int np = fwd ? super_parts_f(S, chs) : super_parts_b(S, ns, chs);
-        const double* ps = a.spart + super_slot(nb, fwd ? 0 : 1, rc, 0) + ii;
-        unsigned long long raw[kMaxParts];
-#pragma unroll
-        for (int c = 0; c < kMaxParts; ++c) raw[c] = c < np ? ld_relaxed_u64(ps + (size_t)c * kTB) : 0ull;
-        v = fwd ? __ldg(rv.b + gr) : poll_value(yf + gr, a.status);
-        poll_block<kMaxParts>(raw, ps, kTB, a.status);
+        const double* ps = a.spart + super_slot(nb, fwd ? 0 : 1, gr / kTB, 0) + gr % kTB;
+        poll_block<kMaxParts>(praw, ps, kTB, a.status);
+        v = (!fwd && hraw == kSentinel) ? poll_value(yf + gr, a.status) : __longlong_as_double((long long)hraw);
 #pragma unroll
         for (int c = 0; c < kMaxParts; ++c)
-          if (c < np) v -= __longlong_as_double((long long)raw[c]);
+          if (c < pnp) v -= __longlong_as_double((long long)praw[c]);
       }
       vin[k] = v;
-#pragma unroll
-      for (int d = 2; d <= kSLook; ++d) {
-        const int pS = fwd ? S - d : S + d, pr = pS * kSR + k;
-        vin[d * kSR + k] = (pS >= 0 && pS < ns && pr < nrow) ? poll_value((fwd ? yf : xb) + pr, a.status) : 0.0;
-      }
+      // y_{S-2} / x_{S+2}: this thread polled it in the previous step's phase B
+      const int pS = fwd ? S - 2 : S + 2;
+      vin[2 * kSR + k] = (pS >= 0 && pS < ns) ? vin[kSR + k] : 0.0;
     }
-    __syncthreads();
+    consumers_sync();
     if (a.trace && g == 0 && tid == 0) a.trace[2 + 2 * ns + u] = globaltimer();  // inputs resolved
     mbar_wait_bounded(bar + (u & 1), (u >> 1) & 1, a.status);
     const double* R = buf + (size_t)(u & 1) * kSRows * kSRowLen + (size_t)row * kSRowLen;
@@ -1013,17 +1050,18 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
     for (int q = 0; q < kSR / TPR; ++q) acc = fma(R[sub + q * TPR], vin[sub + q * TPR], acc);
 #pragma unroll 8
     for (int q = 2 * kSR / TPR; q < kSRowLen / TPR; ++q) acc = fma(R[sub + q * TPR], vin[sub + q * TPR], acc);
+    if (u + 1 < 2 * ns) issue_in(u + 1);
     {
       const int pS = fwd ? S - 1 : S + 1, pr = pS * kSR + tid;
       vin[kSR + tid] = (pS >= 0 && pS < ns && pr < nrow) ? poll_value((fwd ? yf : xb) + pr, a.status) : 0.0;
     }
-    __syncthreads();
+    consumers_sync();
 #pragma unroll
     for (int q = 0; q < kSR / TPR; ++q) acc = fma(R[kSR + sub + q * TPR], vin[kSR + sub + q * TPR], acc);
 #pragma unroll
     for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
     if ((tid & 31) == 0) part[row][sub >> 5] = acc;
-    __syncthreads();
+    consumers_sync();
     if (sub == 0) {
       double v = 0.0;
 #pragma unroll
@@ -1031,12 +1069,12 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
       const int gr = S * kSR + g * kSRows + row;
       if (gr < nrow) (fwd ? yf : xb)[gr] = handoff(v);
     }
-    __syncthreads();
+    consumers_sync();
     if (a.trace && g == 0 && tid == 0) a.trace[2 + u] = globaltimer();  // step published
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) trsv_super_kernel(const DistArgs a) {
+__global__ void __launch_bounds__(kSThreads, 1) trsv_super_kernel(const DistArgs a) {
   extern __shared__ __align__(128) unsigned char ring_smem[];
   const int nb = a.nb;
   const RankView rv = a.loc[0];
@@ -1045,7 +1083,8 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_super_kernel(const DistArgs 
     const size_t n1 = off_ready(nb), n2 = recv_len(nb, 1) - off_cf(nb), n3 = super_slot(nb, 2, 0, 0);
     unsigned long long* base = reinterpret_cast<unsigned long long*>(rv.recv);
     unsigned long long* sp = reinterpret_cast<unsigned long long*>(a.spart);
-    for (size_t e = (size_t)blockIdx.x * kThreads + threadIdx.x; e < n1 + n2 + n3; e += (size_t)gridDim.x * kThreads) {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n1 + n2 + n3;
+         e += (size_t)gridDim.x * blockDim.x) {
       if (e < n1) base[e] = kSentinel;
       else if (e < n1 + n2) base[off_cf(nb) + (e - n1)] = kSentinel;
       else sp[e - n1 - n2] = kSentinel;
@@ -1055,26 +1094,33 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_super_kernel(const DistArgs 
   grid_barrier(a.gsync, a.status);
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[1] = globaltimer();
   if ((int)blockIdx.x < a.nchain) {
-    super_chain(a, ring_smem, blockIdx.x);
+    if (threadIdx.x < kThreads) super_chain(a, ring_smem, blockIdx.x);
   } else {
     TileRing ring;
     ring.stage = reinterpret_cast<double*>(ring_smem);
     ring.full = reinterpret_cast<uint64_t*>(ring_smem + (size_t)kSRing * kTile * sizeof(double));
     ring.next = 0;
-    uint64_t policy = 0;
     if (threadIdx.x == 0) {
-      for (int st = 0; st < kSRing; ++st) mbar_init(ring.full + st, 1);
+      for (int st = 0; st < kSRing; ++st) {
+        mbar_init(ring.full + st, 1);
+        mbar_init(ring.full + kSRing + st, kThreads / 32);
+      }
       fence_mbar_init();
-      policy = policy_evict_first();
     }
     __syncthreads();
     SuperWorkerSmem& wsm = *reinterpret_cast<SuperWorkerSmem*>(ring_smem + kWorkerSmemOff);
     int* tq = reinterpret_cast<int*>(ring_smem + kWorkerSmemOff + sizeof(SuperWorkerSmem));
-    super_worker(a, rv, wsm, ring, tq, policy);
+    if (threadIdx.x >= kThreads) {
+      if (threadIdx.x == kThreads) super_producer(a, rv, ring, tq, policy_evict_first());
+    } else {
+      super_consumer(a, rv, wsm, ring, tq);
+    }
   }
+  __syncthreads();
   {
     const double* xb = rv.recv + off_xb(nb);
-    for (size_t e = (size_t)blockIdx.x * kThreads + threadIdx.x; e < (size_t)nb * kTB; e += (size_t)gridDim.x * kThreads)
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)nb * kTB;
+         e += (size_t)gridDim.x * blockDim.x)
       (void)poll_value(xb + e, a.status);
   }
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[2 + 4 * a.ns] = globaltimer();
@@ -1588,7 +1634,7 @@ cudaError_t super_blocks(int* out) {
     if (e != cudaSuccess) return e;
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_super_kernel, kThreads, kSuperSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trsv_super_kernel, kSThreads, kSuperSmem);
     cb = sms * per;
   }
   *out = cb;
@@ -1598,7 +1644,7 @@ cudaError_t super_blocks(int* out) {
 cudaError_t super_launch(const DistArgs& a, int grid, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kSThreads);
   cfg.dynamicSmemBytes = kSuperSmem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
