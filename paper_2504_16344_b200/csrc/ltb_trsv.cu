@@ -871,7 +871,6 @@ LTB_DEV void super_consumer(const DistArgs& a, const RankView& rv, SuperWorkerSm
   const double* yf = rv.recv + off_yf(nb);
   const double* xb = rv.recv + off_xb(nb);
   unsigned used = 0;
-  long long w_y = 0, w_t = 0, n_tiles = 0, t_start = clock64();  // (trace) waits for y / x, for tiles
   for (int m = 0;; ++m) {
     mbar_wait(ring.full + used % kSRing, (used / kSRing) & 1);  // the task's first tile (or the terminator)
     const int t = *(volatile const int*)(tq + m % kTaskQ);
@@ -894,18 +893,14 @@ LTB_DEV void super_consumer(const DistArgs& a, const RankView& rv, SuperWorkerSm
     vload(0);
     for (int e = 0; e < k.nt; ++e) {
       const unsigned g = used++;
-      long long c0 = clock64();
       if (k.dir == 0) {
         // y_J, columns [8q, 8q + 8) of tile L_IJ, row i
         poll_block<kCPT>(vraw, yf + (size_t)(k.k0 + e) * kTB + kCPT * q, 1, a.status);
         double yv[kCPT];
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) yv[c] = __longlong_as_double((long long)vraw[c]);
-        w_y += clock64() - c0;
         if (e + 1 < k.nt) vload(e + 1);
-        c0 = clock64();
         mbar_wait(ring.full + g % kSRing, (g / kSRing) & 1);
-        w_t += clock64() - c0;
         const double* T = ring.stage + (size_t)(g % kSRing) * kTile;
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) acc[c] = fma(T[(kCPT * q + c) * kTB + i], yv[c], acc[c]);
@@ -913,11 +908,8 @@ LTB_DEV void super_consumer(const DistArgs& a, const RankView& rv, SuperWorkerSm
         // x_T[j = i] times row i of tile L_TJ, columns [8q, 8q + 8)
         const double xj = vraw[0] != kSentinel ? __longlong_as_double((long long)vraw[0])
                                                : poll_value(xb + (size_t)(k.k0 - e) * kTB + i, a.status);
-        w_y += clock64() - c0;
         if (e + 1 < k.nt) vload(e + 1);
-        c0 = clock64();
         mbar_wait(ring.full + g % kSRing, (g / kSRing) & 1);
-        w_t += clock64() - c0;
         const double* T = ring.stage + (size_t)(g % kSRing) * kTile;
 #pragma unroll
         for (int c = 0; c < kCPT; ++c) acc[c] = fma(T[(kCPT * q + c) * kTB + i], xj, acc[c]);
@@ -926,7 +918,6 @@ LTB_DEV void super_consumer(const DistArgs& a, const RankView& rv, SuperWorkerSm
       if ((tid & 31) == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ring.full + kSRing + g % kSRing))
                      : "memory");
-      ++n_tiles;
     }
     // reduce to the task's 64 partial sums
     double* out = a.spart + super_slot(nb, k.dir, k.rc, k.part);
@@ -953,14 +944,6 @@ LTB_DEV void super_consumer(const DistArgs& a, const RankView& rv, SuperWorkerSm
       if (tid < kTB) out[tid] = handoff(sm.sR[tid] + sm.sR[kTB + tid]);
     }
     consumers_sync();  // the reduction scratch is free again
-  }
-  if (a.trace && tid == 0) {
-    const int w = blockIdx.x - a.nchain;
-    a.trace[3 + 4 * a.ns + 3 * w] = (unsigned long long)w_y;
-    a.trace[3 + 4 * a.ns + 3 * w + 1] = (unsigned long long)w_t;
-    a.trace[3 + 4 * a.ns + 3 * w + 2] = (unsigned long long)(clock64() - t_start);
-    a.trace[3 + 4 * a.ns + 3 * 148 + 2 * w] = 0ull;
-    a.trace[3 + 4 * a.ns + 3 * 148 + 2 * w + 1] = (unsigned long long)n_tiles;
   }
 }
 

@@ -24,7 +24,7 @@ constexpr int kMaxRanks = 8;
 // one GPU up to this many 64-blocks solves through the super-block chain
 // (8 blocks per chain step); beyond, streaming the panel dominates and the
 // head/tail chain kernel runs
-constexpr int kSuperMaxNb = 320;
+constexpr int kSuperMaxNb = 512;
 
 // Row-cyclic block distribution over P ranks: rank r holds the 64-row block
 // rows I = r, r+P, r+2P, ... packed row after row (row I has I+1 tiles,

@@ -34,13 +34,6 @@ inp = (a[2 + 2 * ns:2 + 4 * ns] - t0) / 1e3
 print(json.dumps({"n": nd * nt, "nb": nb, "ns": ns, "barrier_us": (a[1] - t0) / 1e3, "end_us": (a[2 + 4 * ns] - t0) / 1e3,
                   "step_inputs_us": [round(v, 2) for v in inp], "step_published_us": [round(v, 2) for v in pub],
                   "compute_us_median": float(np.median(pub - inp))}))
-nw = min(148 - 64, nb)
-wk = np.array(buf[3 + 4 * ns:3 + 4 * ns + 3 * nw], dtype=np.float64).reshape(nw, 3)
-print(json.dumps({"workers": nw, "thread0 cycles median": {"wait_y": float(np.median(wk[:, 0])), "wait_tile": float(np.median(wk[:, 1])),
-                  "busy_total": float(np.median(wk[:, 2]))}, "wait_y_max": float(wk[:, 0].max()), "wait_tile_max": float(wk[:, 1].max())}))
-wi = np.array(buf[3 + 4 * ns + 3 * 148:3 + 4 * ns + 3 * 148 + 2 * nw], dtype=np.float64).reshape(nw, 2)
-print(json.dumps({"issue_cycles_median": float(np.median(wi[:, 0])), "tiles_median": float(np.median(wi[:, 1])),
-                  "tiles_min": float(wi[:, 1].min()), "tiles_max": float(wi[:, 1].max())}))
 ts = []
 for _ in range(10):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
