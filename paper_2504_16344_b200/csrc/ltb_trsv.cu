@@ -1527,9 +1527,21 @@ cudaError_t prepare_super(TriFactor& t, cudaStream_t st) {
     cudaFree(t.spart);
     t.sfwd = t.sbwd = t.spart = nullptr;
     const size_t pbytes = super_slot(t.nb, 2, 0, 0) * sizeof(double);
-    if ((e = cudaMalloc(&t.sfwd, bytes)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&t.sbwd, bytes)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&t.spart, pbytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&t.sfwd, bytes)) != cudaSuccess || (e = cudaMalloc(&t.sbwd, bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&t.spart, pbytes)) != cudaSuccess) {
+      // no room for the super-chain rows (<= 1.5 GB at nb = 512): the
+      // cluster-chain kernel solves without them
+      cudaFree(t.sfwd);
+      cudaFree(t.sbwd);
+      cudaFree(t.spart);
+      t.sfwd = t.sbwd = t.spart = nullptr;
+      t.ns = 0;
+      if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return cudaSuccess;
+      }
+      return e;
+    }
     t.bytes += 2 * bytes + pbytes;
   }
   t.ns = ns;
