@@ -15,6 +15,6 @@ eng.set_factor_generated(seed)
 d = torch.rand(nd * nt, dtype=torch.float64, device="cuda")
 m = torch.empty(nm * nt, dtype=torch.float64, device="cuda")
 q = torch.empty(nq * nt, dtype=torch.float64, device="cuda")
-for _ in range(4):
-    sec = eng.infer_raw(d, m, q)
-print("infer+forecast %.3f ms" % (sec * 1e3))
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+ts = sorted(eng.infer_raw(d, m, q) for _ in range(reps))
+print("infer+forecast median %.3f ms (min %.3f, %d reps)" % (ts[len(ts) // 2] * 1e3, ts[0] * 1e3, reps))
