@@ -1529,7 +1529,7 @@ cudaError_t prepare_super(TriFactor& t, cudaStream_t st) {
     const size_t pbytes = super_slot(t.nb, 2, 0, 0) * sizeof(double);
     if ((e = cudaMalloc(&t.sfwd, bytes)) != cudaSuccess || (e = cudaMalloc(&t.sbwd, bytes)) != cudaSuccess ||
         (e = cudaMalloc(&t.spart, pbytes)) != cudaSuccess) {
-      // no room for the super-chain rows (<= 1.5 GB at nb = 512): the
+      // no room for the super-chain rows (<= 0.8 GB at nb = 512): the
       // cluster-chain kernel solves without them
       cudaFree(t.sfwd);
       cudaFree(t.sbwd);
