@@ -999,12 +999,6 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
   for (int u = 0; u < 2 * ns; ++u) {
     const bool fwd = u < ns;
     const int S = fwd ? u : 2 * ns - 1 - u;
-    if (tid == 0 && u + 1 < 2 * ns) {  // that buffer was consumed in step u - 1
-      const int nx = (u + 1) & 1;
-      mbar_arrive_expect_tx(bar + nx, kBytes);
-      bulk_g2s(buf + (size_t)nx * kSRows * kSRowLen, rows_of(u + 1), kBytes, bar + nx, policy_evict_first());
-      l2_prefetch(u + 2);
-    }
     {
       // [c_S; -; y_{S-2}] (forward) or [d_S; -; x_{S+2}] (backward), 0 past the factor
       const int k = tid, gr = S * kSR + k;
@@ -1022,8 +1016,14 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
       const int pS = fwd ? S - 2 : S + 2;
       vin[2 * kSR + k] = (pS >= 0 && pS < ns) ? vin[kSR + k] : 0.0;
     }
-    consumers_sync();
+    consumers_sync();  // inputs in; every thread is done with step u - 1 (and its row buffer)
     if (a.trace && g == 0 && tid == 0) a.trace[2 + 2 * ns + u] = globaltimer();  // inputs resolved
+    if (tid == 0 && u + 1 < 2 * ns) {  // step u + 1's rows into the buffer step u - 1 used
+      const int nx = (u + 1) & 1;
+      mbar_arrive_expect_tx(bar + nx, kBytes);
+      bulk_g2s(buf + (size_t)nx * kSRows * kSRowLen, rows_of(u + 1), kBytes, bar + nx, policy_evict_first());
+      l2_prefetch(u + 2);
+    }
     mbar_wait_bounded(bar + (u & 1), (u >> 1) & 1, a.status);
     const double* R = buf + (size_t)(u & 1) * kSRows * kSRowLen + (size_t)row * kSRowLen;
     // everything but the previous step's block first, then (the critical
@@ -1052,7 +1052,6 @@ LTB_DEV void super_chain(const DistArgs& a, unsigned char* dsm, int g) {
       const int gr = S * kSR + g * kSRows + row;
       if (gr < nrow) (fwd ? yf : xb)[gr] = handoff(v);
     }
-    consumers_sync();
     if (a.trace && g == 0 && tid == 0) a.trace[2 + u] = globaltimer();  // step published
   }
 }
