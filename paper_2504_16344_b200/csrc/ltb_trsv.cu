@@ -763,19 +763,22 @@ __global__ void __launch_bounds__(kThreads, 1) trsv_kernel(const DistArgs a) {
 // L_TS^T x_T (super-block indices): the workers' last inputs exist two chain
 // steps before the chain needs their sums.  A chain step is ONE dense
 // 512 x 1536 product [L_SS^{-1} | -M1_S | -M2_S] [c_S; y_{S-1}; y_{S-2}]
-// spread over kSChain CTAs
-// (kSRows rows each, the next step's rows prefetched by one bulk copy);
-// the chain CTAs exchange y / x through global memory (NaN-sentinel slots).
-// The panel sums are cut into tasks of at most chs super blocks of one tile
-// row (column), spread round-robin over the workers in the order their
-// inputs appear, each handing off a 64-value partial sum; the chain adds the
-// <= kMaxParts partials of a row when it assembles c_S / d_S.  Long rows are
-// thereby streamed by many SMs at once: a row-per-worker split leaves the
-// last rows (3.9 MB at n = 8192) to one SM each, which bounds the sweep.
+// spread over kSChain CTAs (kSRows rows each; the next step's rows arrive by
+// one bulk copy, the one after that is pulled into L2); the chain CTAs
+// exchange y / x through global memory (NaN-sentinel slots), and only the
+// poll of the previous step's values and its -M1 columns sit on the
+// step-to-step critical path.  The workers' panel sums are cut into TASKS of
+// at most chs super blocks of one tile row (column), taken from a global
+// counter in urgency order (build_super_tasks), each handing off a 64-value
+// partial sum; the chain adds the <= kMaxParts partials of a row when it
+// assembles c_S / d_S.  Long rows are thereby streamed by many SMs at once
+// (a row per worker leaves the last rows, 3.9 MB at n = 8192, to one SM
+// each, which bounds the sweep).
 constexpr int kSLook = 2;                 // previous super blocks the chain applies itself
 // (super_chain hands y_{S-1} of one step on as y_{S-2} of the next: kSLook == 2)
 constexpr int kSRowLen = (1 + kSLook) * kSR;  // [inverse | -M1 | -M2] row
-constexpr size_t kSChainSmem = (size_t)(2 * kSRows * kSRowLen + kSRowLen) * sizeof(double) + 2 * sizeof(uint64_t);
+constexpr size_t kSChainSmem =
+    (size_t)(2 * kSRows * kSRowLen + kSRowLen) * sizeof(double) + 2 * sizeof(uint64_t);
 // super kernel workers: a kSRing-deep tile ring (deeper than the cluster
 // kernel's: more bytes in flight per SM while HBM is saturated), then their
 // reduction scratch and task queue, all in the dynamic region the chain
@@ -785,14 +788,16 @@ struct SuperWorkerSmem {
   double red[kQ][kTB];
   double sR[2 * kTB];
 };
-constexpr size_t kWorkerSmemOff = ((size_t)kSRing * kTile * sizeof(double) + 2 * kSRing * sizeof(uint64_t) + 127) / 128 * 128;
+constexpr size_t kWorkerSmemOff =
+    ((size_t)kSRing * kTile * sizeof(double) + 2 * kSRing * sizeof(uint64_t) + 127) / 128 * 128;
 constexpr int kMaxParts = 8;
 
 // super blocks per task for ns super blocks: <= kMaxParts partials per row
 __host__ __device__ inline int super_chs(int ns) { return (ns + kMaxParts - 1) / kMaxParts; }
-// forward: row I (super block S = I / kSB) has panel super blocks [0, S - 1)
-// in parts of chs; backward: column J has [S + 2, ns), parts counted from the
-// top (part 0 = the highest super blocks, whose x comes first)
+// forward: row I (super block S = I / kSB) has panel super blocks
+// [0, S - kSLook) in parts of chs; backward: column J has [S + kSLook + 1,
+// ns), parts counted from the top (part 0 = the highest super blocks, whose
+// x comes first)
 __host__ __device__ inline int super_parts_f(int S, int chs) {
   return S > kSLook ? (S - kSLook + chs - 1) / chs : 0;
 }
