@@ -888,6 +888,15 @@ ltb_status apply_device(const ltb_plan* p, ltb_scratch* s, const double* in, dou
   return adjoint ? apply_adjoint_dev(p, s, in, out) : apply_dev(p, s, in, out);
 }
 cudaStream_t scratch_stream(ltb_scratch* s) { return s->stream; }
+// the device buffers a captured apply bakes in (ltb_engine.cu's graph key);
+// false while the scratch records per-stage timing events
+bool scratch_graph_key(const ltb_scratch* s, const void** out4) {
+  out4[0] = s->xhat;
+  out4[1] = s->dhat;
+  out4[2] = s->partials;
+  out4[3] = s->tickets;
+  return !s->timing;
+}
 ltb_status fm_from_host(const ltb_plan* p, ltb_scratch* s, const double* in_host, double* d_dev) {
   if (!p || !s || s->plan != p) return fail(LTB_INVALID, "apply: scratch was created for another plan");
   return fm_host_enqueue(p, s, in_host, d_dev);

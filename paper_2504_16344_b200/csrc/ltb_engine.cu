@@ -32,6 +32,7 @@ ltb_status set_error(ltb_status st, const char* msg);
 ltb_status apply_device(const ltb_plan* p, ltb_scratch* s, const double* in, double* out,
                         bool adjoint);
 cudaStream_t scratch_stream(ltb_scratch* s);
+bool scratch_graph_key(const ltb_scratch* s, const void** out4);
 int plan_device(const ltb_plan* p);
 void plan_dims(const ltb_plan* p, int* rows, int* cols, int* nt);
 void count_launches(uint64_t n);
@@ -98,6 +99,16 @@ struct ltb_engine {
   ltb_scratch* fq_scratch = nullptr;
   cudaStream_t fq_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // infer_map + forecast with device pointers replays one CUDA graph of its
+  // ~6 launches (K^-1, r2c, GEMV-H, c2r->r2c, GEMV-N, c2r) while the
+  // buffers it bakes in are unchanged (key) and the factor is the same
+  // (factor_gen); LTB_NO_GRAPH=1 launches eagerly
+  cudaGraphExec_t ig_exec = nullptr;
+  static constexpr int kGraphKey = 13;
+  const void* ig_key[kGraphKey] = {};
+  unsigned factor_gen = 0, ig_gen = 0;
+  bool ig_failed = false;  // the capture was refused for this key: eager launches
+  const void* ig_last[kGraphKey] = {};  // the previous call's key: capture on its second use in a row
   // The reference's online calls are const and re-entrant (solve_k_inplace /
   // infer_map are called from parallel_for workers, bayes_engine.cpp:252-256,
   // 389).  Here they share the staging buffers, the TRSV hand-off buffers and
@@ -174,6 +185,7 @@ ltb_status ltb_engine_destroy(ltb_engine* e) {
   if (e->f_scratch) ltb_scratch_destroy(e->f_scratch);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->ig_exec) cudaGraphExecDestroy(e->ig_exec);
   if (e->comm && e->nccl) e->nccl->CommDestroy(e->comm);
   release_phase3(e);
   delete e;
@@ -206,6 +218,7 @@ ltb_status factor_prepare(ltb_engine* e, int n) {
 
 ltb_status factor_finish(ltb_engine* e, cudaError_t err) {
   count_launches(2);
+  ++e->factor_gen;  // a captured infer graph refers to the previous factor
   if (err == cudaErrorInvalidValue)
     return efail(LTB_NUMERICAL, "set_factor: zero or non-finite diagonal in the Cholesky factor");
   ENG_CUDA(err);
@@ -646,7 +659,52 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
     if ((st = ensure(&e->stage_m, nm_nt)) != LTB_OK) return st;
     mout = e->stage_m;
   }
+  // device pointers + forecast: one graph of the whole chain (see ig_exec)
+  static const bool no_graph = getenv("LTB_NO_GRAPH") != nullptr;
+  const void* key[ltb_engine::kGraphKey] = {din, mout, qout, (const void*)strm, e->factor.tiles};
+  bool graphable = ptr_kind == LTB_PTR_DEVICE && q && e->world == 1 && !no_graph &&
+                   scratch_graph_key(s, key + 5) && scratch_graph_key(sq, key + 9);
+  const auto graph_body = [&]() -> ltb_status {
+    ltb_status rs = solve_dev(e, din, nullptr, strm);
+    if (rs == LTB_OK) rs = gstar_then_fq(e->g, s, e->fq, sq, trsv_result(e->factor), mout, qout, nullptr);
+    return rs;
+  };
+  const bool same = e->ig_gen == e->factor_gen && std::equal(key, key + ltb_engine::kGraphKey, e->ig_key);
+  const bool repeat = std::equal(key, key + ltb_engine::kGraphKey, e->ig_last);
+  std::copy(key, key + ltb_engine::kGraphKey, e->ig_last);
+  if (graphable && same && e->ig_failed) graphable = false;
+  // a new key runs eagerly once (callers alternating buffers never pay a capture)
+  if (graphable && !same && !repeat) graphable = false;
+  if (graphable && !(e->ig_exec && same)) {
+    if (e->ig_exec) cudaGraphExecDestroy(e->ig_exec);
+    e->ig_exec = nullptr;
+    cudaGraph_t gr = nullptr;
+    if (cudaStreamBeginCapture(strm, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const ltb_status rs = graph_body();
+      const cudaError_t ce = cudaStreamEndCapture(strm, &gr);
+      if (rs != LTB_OK || ce != cudaSuccess || !gr || cudaGraphInstantiate(&e->ig_exec, gr, 0) != cudaSuccess)
+        e->ig_exec = nullptr;
+      if (gr) cudaGraphDestroy(gr);
+    }
+    cudaGetLastError();  // a refused capture falls back to eager launches
+    std::copy(key, key + ltb_engine::kGraphKey, e->ig_key);
+    e->ig_gen = e->factor_gen;
+    e->ig_failed = e->ig_exec == nullptr;
+    graphable = e->ig_exec != nullptr;
+  }
   ENG_CUDA(cudaEventRecord(e->ev0, strm));
+  if (graphable) {
+    ENG_CUDA(cudaGraphLaunch(e->ig_exec, strm));
+    count_launches(6);
+    ENG_CUDA(cudaEventRecord(e->ev1, strm));
+    if ((st = check_solve_status(e, strm)) != LTB_OK) return st;
+    if (seconds) {
+      float ms = 0.f;
+      ENG_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+      *seconds = ms * 1e-3;
+    }
+    return LTB_OK;
+  }
   if (ptr_kind == LTB_PTR_HOST)
     ENG_CUDA(cudaMemcpyAsync(e->stage_in, d, nd_nt * sizeof(double), cudaMemcpyHostToDevice, strm));
   // y = K^{-1} d  (bayes_engine.cpp:312-313)
