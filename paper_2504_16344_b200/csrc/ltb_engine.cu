@@ -99,12 +99,12 @@ struct ltb_engine {
   ltb_scratch* fq_scratch = nullptr;
   cudaStream_t fq_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // infer_map + forecast with device pointers replays one CUDA graph of its
-  // ~6 launches (K^-1, r2c, GEMV-H, c2r->r2c, GEMV-N, c2r) while the
-  // buffers it bakes in are unchanged (key) and the factor is the same
-  // (factor_gen); LTB_NO_GRAPH=1 launches eagerly
+  // infer_map + forecast replays one CUDA graph of its launches (K^-1, r2c,
+  // GEMV-H, c2r->r2c, GEMV-N, c2r; with host pointers also the pinned
+  // copies) while the buffers it bakes in are unchanged (key) and the factor
+  // is the same (factor_gen); LTB_NO_GRAPH=1 launches eagerly
   cudaGraphExec_t ig_exec = nullptr;
-  static constexpr int kGraphKey = 13;
+  static constexpr int kGraphKey = 16;
   const void* ig_key[kGraphKey] = {};
   unsigned factor_gen = 0, ig_gen = 0;
   bool ig_failed = false;  // the capture was refused for this key: eager launches
@@ -659,16 +659,35 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
     if ((st = ensure(&e->stage_m, nm_nt)) != LTB_OK) return st;
     mout = e->stage_m;
   }
-  // device pointers + forecast: one graph of the whole chain (see ig_exec)
-  static const bool no_graph = getenv("LTB_NO_GRAPH") != nullptr;
-  const void* key[ltb_engine::kGraphKey] = {din, mout, qout, (const void*)strm, e->factor.tiles};
-  bool graphable = ptr_kind == LTB_PTR_DEVICE && q && e->world == 1 && !no_graph &&
-                   scratch_graph_key(s, key + 5) && scratch_graph_key(sq, key + 9);
-  const auto graph_body = [&]() -> ltb_status {
+  // the whole chain, launched eagerly or captured once into a CUDA graph
+  double* m_host = (ptr_kind == LTB_PTR_HOST) ? m_map : nullptr;
+  const auto body = [&]() -> ltb_status {
+    if (ptr_kind == LTB_PTR_HOST)
+      ENG_CUDA(cudaMemcpyAsync(e->stage_in, d, nd_nt * sizeof(double), cudaMemcpyHostToDevice, strm));
+    // y = K^{-1} d  (bayes_engine.cpp:312-313)
     ltb_status rs = solve_dev(e, din, nullptr, strm);
-    if (rs == LTB_OK) rs = gstar_then_fq(e->g, s, e->fq, sq, trsv_result(e->factor), mout, qout, nullptr);
-    return rs;
+    if (rs != LTB_OK) return rs;
+    // m_map = G* y  (:316-319); host m_map: copied out in column chunks while
+    // the rest of G* (and the forecast) run
+    if (q) {
+      // + q = F_q m_map, the c2r of m and the r2c for F_q in one pass
+      rs = gstar_then_fq(e->g, s, e->fq, sq, trsv_result(e->factor), mout, qout, m_host);
+    } else if (m_host) {
+      rs = adjoint_to_host(e->g, s, trsv_result(e->factor), mout, m_host);
+    } else {
+      rs = apply_device(e->g, s, trsv_result(e->factor), mout, true);
+    }
+    if (rs != LTB_OK) return rs;
+    if (ptr_kind == LTB_PTR_HOST && q)
+      ENG_CUDA(cudaMemcpyAsync(q, qout, nq_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
+    return LTB_OK;
   };
+  // Forecast calls replay a graph of their launches and copies (see ig_exec)
+  // once the same buffers come twice in a row; a refused capture (e.g.
+  // pageable host buffers) stays eager for that key.
+  static const bool no_graph = getenv("LTB_NO_GRAPH") != nullptr;
+  const void* key[ltb_engine::kGraphKey] = {d, m_map, q, din, mout, qout, (const void*)strm, e->factor.tiles};
+  bool graphable = q && e->world == 1 && !no_graph && scratch_graph_key(s, key + 8) && scratch_graph_key(sq, key + 12);
   const bool same = e->ig_gen == e->factor_gen && std::equal(key, key + ltb_engine::kGraphKey, e->ig_key);
   const bool repeat = std::equal(key, key + ltb_engine::kGraphKey, e->ig_last);
   std::copy(key, key + ltb_engine::kGraphKey, e->ig_last);
@@ -680,7 +699,7 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
     e->ig_exec = nullptr;
     cudaGraph_t gr = nullptr;
     if (cudaStreamBeginCapture(strm, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-      const ltb_status rs = graph_body();
+      const ltb_status rs = body();
       const cudaError_t ce = cudaStreamEndCapture(strm, &gr);
       if (rs != LTB_OK || ce != cudaSuccess || !gr || cudaGraphInstantiate(&e->ig_exec, gr, 0) != cudaSuccess)
         e->ig_exec = nullptr;
@@ -696,32 +715,9 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
   if (graphable) {
     ENG_CUDA(cudaGraphLaunch(e->ig_exec, strm));
     count_launches(6);
-    ENG_CUDA(cudaEventRecord(e->ev1, strm));
-    if ((st = check_solve_status(e, strm)) != LTB_OK) return st;
-    if (seconds) {
-      float ms = 0.f;
-      ENG_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
-      *seconds = ms * 1e-3;
-    }
-    return LTB_OK;
-  }
-  if (ptr_kind == LTB_PTR_HOST)
-    ENG_CUDA(cudaMemcpyAsync(e->stage_in, d, nd_nt * sizeof(double), cudaMemcpyHostToDevice, strm));
-  // y = K^{-1} d  (bayes_engine.cpp:312-313)
-  if ((st = solve_dev(e, din, nullptr, strm)) != LTB_OK) return st;
-  // m_map = G* y  (:316-319); host m_map: copied out in column chunks while
-  // the rest of G* (and the forecast) run
-  double* m_host = (ptr_kind == LTB_PTR_HOST) ? m_map : nullptr;
-  if (q) {
-    // + q = F_q m_map, the c2r of m and the r2c for F_q in one pass
-    if ((st = gstar_then_fq(e->g, s, e->fq, sq, trsv_result(e->factor), mout, qout, m_host)) != LTB_OK) return st;
-  } else if (m_host) {
-    if ((st = adjoint_to_host(e->g, s, trsv_result(e->factor), mout, m_host)) != LTB_OK) return st;
-  } else if ((st = apply_device(e->g, s, trsv_result(e->factor), mout, true)) != LTB_OK) {
+  } else if ((st = body()) != LTB_OK) {
     return st;
   }
-  if (ptr_kind == LTB_PTR_HOST && q)
-    ENG_CUDA(cudaMemcpyAsync(q, qout, nq_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
   ENG_CUDA(cudaEventRecord(e->ev1, strm));
   if ((st = check_solve_status(e, strm)) != LTB_OK) return st;
   if (seconds) {
