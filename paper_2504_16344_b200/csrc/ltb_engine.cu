@@ -77,6 +77,52 @@ struct Guard {
 
 }  // namespace
 
+namespace {
+// One captured CUDA graph of an engine call's launches / copies, replayed
+// while the buffers it bakes in (key) and the factor (gen) are unchanged.
+// A new key runs eagerly once and is captured on its second use in a row,
+// so callers alternating buffers never pay a capture; a refused capture
+// (e.g. pageable host memory) stays eager for that key.
+struct GraphCache {
+  static constexpr int kKey = 16;
+  cudaGraphExec_t exec = nullptr;
+  const void* key[kKey] = {};
+  const void* last[kKey] = {};
+  unsigned gen = 0;
+  bool failed = false;
+  ~GraphCache() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+  // true: the call is enqueued on st through the graph; false: run body eagerly
+  template <class Body>
+  bool replay(cudaStream_t st, const void* const* k, unsigned g, const Body& body) {
+    static const bool off = getenv("LTB_NO_GRAPH") != nullptr;
+    const bool same = gen == g && std::equal(k, k + kKey, key);
+    const bool repeat = std::equal(k, k + kKey, last);
+    std::copy(k, k + kKey, last);
+    if (off || (same && failed) || (!same && !repeat)) return false;
+    if (!(exec && same)) {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+      cudaGraph_t gr = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        const ltb_status rs = body();
+        const cudaError_t ce = cudaStreamEndCapture(st, &gr);
+        if (rs != LTB_OK || ce != cudaSuccess || !gr || cudaGraphInstantiate(&exec, gr, 0) != cudaSuccess)
+          exec = nullptr;
+        if (gr) cudaGraphDestroy(gr);
+      }
+      cudaGetLastError();  // a refused capture falls back to eager launches
+      std::copy(k, k + kKey, key);
+      gen = g;
+      failed = exec == nullptr;
+      if (!exec) return false;
+    }
+    return cudaGraphLaunch(exec, st) == cudaSuccess;
+  }
+};
+}  // namespace
+
 struct ltb_engine {
   const ltb_plan* g = nullptr;
   const ltb_plan* fq = nullptr;
@@ -99,16 +145,13 @@ struct ltb_engine {
   ltb_scratch* fq_scratch = nullptr;
   cudaStream_t fq_stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // infer_map + forecast replays one CUDA graph of its launches (K^-1, r2c,
+  // infer_map + forecast replays a CUDA graph of its launches (K^-1, r2c,
   // GEMV-H, c2r->r2c, GEMV-N, c2r; with host pointers also the pinned
-  // copies) while the buffers it bakes in are unchanged (key) and the factor
-  // is the same (factor_gen); LTB_NO_GRAPH=1 launches eagerly
-  cudaGraphExec_t ig_exec = nullptr;
-  static constexpr int kGraphKey = 16;
-  const void* ig_key[kGraphKey] = {};
-  unsigned factor_gen = 0, ig_gen = 0;
-  bool ig_failed = false;  // the capture was refused for this key: eager launches
-  const void* ig_last[kGraphKey] = {};  // the previous call's key: capture on its second use in a row
+  // copies) while the buffers it bakes in are unchanged and the factor is the
+  // same (factor_gen); LTB_NO_GRAPH=1 launches eagerly.  (A solve_k graph
+  // -- one kernel and a copy -- measured no gain.)
+  mutable GraphCache infer_graph;  // (const entry points, under the engine lock)
+  unsigned factor_gen = 0;
   // The reference's online calls are const and re-entrant (solve_k_inplace /
   // infer_map are called from parallel_for workers, bayes_engine.cpp:252-256,
   // 389).  Here they share the staging buffers, the TRSV hand-off buffers and
@@ -185,7 +228,6 @@ ltb_status ltb_engine_destroy(ltb_engine* e) {
   if (e->f_scratch) ltb_scratch_destroy(e->f_scratch);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
-  if (e->ig_exec) cudaGraphExecDestroy(e->ig_exec);
   if (e->comm && e->nccl) e->nccl->CommDestroy(e->comm);
   release_phase3(e);
   delete e;
@@ -682,38 +724,11 @@ ltb_status ltb_engine_infer_and_forecast(const ltb_engine* e_, ltb_scratch* s, c
       ENG_CUDA(cudaMemcpyAsync(q, qout, nq_nt * sizeof(double), cudaMemcpyDeviceToHost, strm));
     return LTB_OK;
   };
-  // Forecast calls replay a graph of their launches and copies (see ig_exec)
-  // once the same buffers come twice in a row; a refused capture (e.g.
-  // pageable host buffers) stays eager for that key.
-  static const bool no_graph = getenv("LTB_NO_GRAPH") != nullptr;
-  const void* key[ltb_engine::kGraphKey] = {d, m_map, q, din, mout, qout, (const void*)strm, e->factor.tiles};
-  bool graphable = q && e->world == 1 && !no_graph && scratch_graph_key(s, key + 8) && scratch_graph_key(sq, key + 12);
-  const bool same = e->ig_gen == e->factor_gen && std::equal(key, key + ltb_engine::kGraphKey, e->ig_key);
-  const bool repeat = std::equal(key, key + ltb_engine::kGraphKey, e->ig_last);
-  std::copy(key, key + ltb_engine::kGraphKey, e->ig_last);
-  if (graphable && same && e->ig_failed) graphable = false;
-  // a new key runs eagerly once (callers alternating buffers never pay a capture)
-  if (graphable && !same && !repeat) graphable = false;
-  if (graphable && !(e->ig_exec && same)) {
-    if (e->ig_exec) cudaGraphExecDestroy(e->ig_exec);
-    e->ig_exec = nullptr;
-    cudaGraph_t gr = nullptr;
-    if (cudaStreamBeginCapture(strm, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-      const ltb_status rs = body();
-      const cudaError_t ce = cudaStreamEndCapture(strm, &gr);
-      if (rs != LTB_OK || ce != cudaSuccess || !gr || cudaGraphInstantiate(&e->ig_exec, gr, 0) != cudaSuccess)
-        e->ig_exec = nullptr;
-      if (gr) cudaGraphDestroy(gr);
-    }
-    cudaGetLastError();  // a refused capture falls back to eager launches
-    std::copy(key, key + ltb_engine::kGraphKey, e->ig_key);
-    e->ig_gen = e->factor_gen;
-    e->ig_failed = e->ig_exec == nullptr;
-    graphable = e->ig_exec != nullptr;
-  }
+  // forecast calls replay a graph of their launches and copies (GraphCache)
+  const void* key[GraphCache::kKey] = {d, m_map, q, din, mout, qout, (const void*)strm, e->factor.tiles};
+  const bool graphable = q && e->world == 1 && scratch_graph_key(s, key + 8) && scratch_graph_key(sq, key + 12);
   ENG_CUDA(cudaEventRecord(e->ev0, strm));
-  if (graphable) {
-    ENG_CUDA(cudaGraphLaunch(e->ig_exec, strm));
+  if (graphable && e->infer_graph.replay(strm, key, e->factor_gen, body)) {
     count_launches(6);
   } else if ((st = body()) != LTB_OK) {
     return st;
