@@ -552,24 +552,37 @@ LTB_DEV void tile_update_ring(const double* const (&Li)[2], const double* const 
   const int wm = warp >> 2, wn = warp & 3;
   const int nch = kPer * kc;
   // chunk q (k columns [KS (q % kPer), +KS) of block column k + q / kPer)
-  // into ring stage q % S; always one commit group per call
+  // into ring stage q % S by bulk copies (TMA, 1-D): lane c of warp 0 moves
+  // one 512-byte tile column into its padded shared row (stride kUS keeps
+  // the DMMA fragment loads conflict free); they complete on full[q % S]
+  uint64_t* full = reinterpret_cast<uint64_t*>(usm + S * kStage);
   auto load = [&](int q) {
-    if (q < nch) {
-      const size_t off = (size_t)(q % kPer) * KS * kT;
-      const double* a = (q >= kPer ? Li[1] : Li[0]) + off;  // (not indexed: would go to local memory)
-      const double* bb = (q >= kPer ? Lj[1] : Lj[0]) + off;
-      double* sa = usm + (q % S) * kStage;
-      double* sb = sa + KS * kUS;
-      for (int c = tid; c < KS * kT / 2; c += kUpdThreads) {
-        const int l = c >> 5, m = 2 * (c & 31);
-        cp_async16(sa + l * kUS + m, a + l * kT + m, 16);
-        cp_async16(sb + l * kUS + m, bb + l * kT + m, 16);
-      }
+    if (q >= nch) return;
+    const size_t off = (size_t)(q % kPer) * KS * kT;
+    const double* a = (q >= kPer ? Li[1] : Li[0]) + off;  // (not indexed: would go to local memory)
+    const double* bb = (q >= kPer ? Lj[1] : Lj[0]) + off;
+    double* sa = usm + (q % S) * kStage;
+    if (lane == 0) mbar_arrive_expect_tx(full + q % S, 2 * KS * kT * sizeof(double));
+    __syncwarp();
+    if (lane < 2 * KS) {
+      const int c = lane % KS;
+      // the stage was last read by generic loads: order them before the async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint64_t pol;  // the L tiles are re-read by the whole block row / column: normal L2 priority
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+      bulk_g2s(sa + (lane < KS ? 0 : KS * kUS) + c * kUS, (lane < KS ? a : bb) + (size_t)c * kT,
+               kT * sizeof(double), full + q % S, pol);
     }
-    cp_commit();
   };
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(full + st, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
 #pragma unroll
-  for (int q = 0; q < S - 1; ++q) load(q);
+    for (int q = 0; q < S - 1; ++q) load(q);
+  }
   double acc[2][2][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -583,9 +596,9 @@ LTB_DEV void tile_update_ring(const double* const (&Li)[2], const double* const 
           acc[mt][nt8][2 * h + c] = Aij[col * kT + r];
         }
   for (int q = 0; q < nch; ++q) {
-    cp_wait<S - 2>();
-    __syncthreads();  // chunk q landed for every thread; stage (q - 1) % S is free
-    load(q + S - 1);
+    __syncthreads();  // every thread is done with stage (q - 1) % S
+    if (warp == 0) load(q + S - 1);
+    mbar_wait(full + q % S, (q / S) & 1);
     const double* sA = usm + (q % S) * kStage;
     const double* sB = sA + KS * kUS;
 #pragma unroll
@@ -605,7 +618,6 @@ LTB_DEV void tile_update_ring(const double* const (&Li)[2], const double* const 
         for (int nt8 = 0; nt8 < 2; ++nt8) dmma(acc[mt][nt8], a[mt][0], a[mt][1], bf[nt8]);
     }
   }
-  cp_wait<0>();
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -620,7 +632,7 @@ LTB_DEV void tile_update_ring(const double* const (&Li)[2], const double* const 
 }
 
 template <int KS, int S>
-constexpr size_t upd_smem() { return (size_t)S * 2 * KS * kUS * sizeof(double); }
+constexpr size_t upd_smem() { return (size_t)S * 2 * KS * kUS * sizeof(double) + S * sizeof(uint64_t); }
 
 // 16-column k stages, double buffered: 35 KB of shared memory and 62
 // registers -> 4 CTAs per SM (32-column stages / deeper rings measured
@@ -630,7 +642,7 @@ constexpr size_t kUpdSmem = upd_smem<kUpdKS, kUpdStages>();
 
 // tiles: mode 0, the lower triangle from (base, base); mode 1, block columns
 // base and base + 1 (i >= j); mode 2, block column base
-__global__ void __launch_bounds__(kUpdThreads)
+__global__ void __launch_bounds__(kUpdThreads, 4)
     chol_update_kernel(double* __restrict__ tiles, int nb, int k, int kc, int base, int mode) {
   int i, j;
   const int b = (int)blockIdx.x, m0 = nb - base;
@@ -1157,7 +1169,7 @@ LTB_DEV const double* dist_gathered(const DistCol& g, int c, int j, int P) {
 
 // own rows i > kl (kl = k + kc - 1), tiles j in (kl, i]:
 // A_ij -= sum_{c < kc} L_i,k+c L_j,k+c^T (column_only: just j = kl + 1, kc = 1)
-__global__ void __launch_bounds__(kUpdThreads)
+__global__ void __launch_bounds__(kUpdThreads, 4)
     dist_update_kernel(double* __restrict__ tiles, int r, int P, int k, int kc, int nb, const DistCol g0,
                        const DistCol g1, int column_only) {
   const int kl = k + kc - 1;
